@@ -1,0 +1,413 @@
+#!/usr/bin/env python
+"""Benchmark: one coupling step of the stochastic conservative transfer on B200.
+
+Workload (BASELINE.json configs[1], SURVEY.md section 8 "C2"): 3-D unit-cube tet pair,
+target n=55 Kuhn split (998,250 tets, 175,616 nodes, jitter 0.2h, seed 20), source
+n=55 mirrored Kuhn split (seed 10); mesh-backed source = P1 interpolant of
+sin(x)cos(y)cos(z)+2 located through the uniform grid; shared Sobol plan, N samples per
+element (default 64; the 16..256 sweep is reported under "sweep").
+
+A step = one online coupling step (the reference's own bench split, cli.py:272-293):
+fused MC load (plan -> map -> locate -> P1 eval -> accumulate, one launch) -> ordered
+node reduction -> [NCCL all-reduce of b over ranks] -> single-launch Jacobi PCG
+(tol 1e-12).  Setup (meshes, geometry, grid, incidence, mass matrix) is untimed.
+
+value = S / t_step (S = E_t * N samples per step, all ranks); ms_per_step = wall time
+per coupling step.  e2e = the same through the public API (transfer_mc on a NodalField
+whose coefficients are copied H2D from pinned memory each step, x read back D2H).
+
+Multi-GPU (torchrun): target elements are split into contiguous ranges (strong
+scaling); source mesh, grid and field are replicated; partial b vectors are summed
+with one NCCL all-reduce; the PCG is replicated per rank.
+
+``--impl reference``: the reference algorithm on the host CPU for the same config
+(the reference is 2-D only, so 3-D runs the oracle restatement: kind "port"), bounded
+sample, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+METRIC = "source-field samples/sec and transfer wall-time per coupling step at 1/2/4/8 B200"
+L2_FLUSH_BYTES = 256 << 20
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--samples", type=int, default=64)
+    ap.add_argument("--n", type=int, default=55, help="cubes per axis (C2: 55)")
+    ap.add_argument("--mode", default="sobol", choices=["sobol", "uniform", "philox"])
+    ap.add_argument("--sweep", default="16,32,64,128,256")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload_config(args, world):
+    return {"workload": "C2: 3-D unit-cube tet transfer, mesh-backed source, 1 coupling step",
+            "target": f"cube n={args.n} kuhn jitter0.2 seed20",
+            "source": f"cube n={args.n} kuhn_mirror jitter0.2 seed10",
+            "field": "sin(x)cos(y)cos(z)+2 (P1 interpolant on source)",
+            "samples_per_elem": args.samples, "plan": args.mode, "cg_tol": 1e-12,
+            "partition": f"contiguous target-element ranges x{world}", "l2": "flushed between timed steps",
+            "parallelism": f"dp{world}"}
+
+
+# --------------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self, index=0):
+        self.proc = None
+        self.index = index
+        self.path = ROOT / "gpurun_out" / f"clocks_bench_{os.getpid()}.csv"
+
+    def __enter__(self):
+        try:
+            self.path.parent.mkdir(exist_ok=True)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}",
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.fh,
+                stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+            self.fh.close()
+
+    def summary(self):
+        try:
+            rows = [r.split(",") for r in self.path.read_text().strip().splitlines() if r.strip()]
+        except Exception:
+            rows = []
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in rows]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for nm, v in zip(names, r[3:7]):
+                if v.strip() == "Active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][1]),
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+# --------------------------------------------------------------------- ours
+def build_problem(args, tt):
+    tgt = tt.generate_cube_mesh(args.n, 0.2, seed=20, split="kuhn")
+    src = tt.generate_cube_mesh(args.n, 0.2, seed=10, split="kuhn_mirror")
+    field = tt.get_field("smooth", dim=3)
+    fs = tt.NodalField.from_function(src, field.fn)
+    loc = tt.UniformGridLocator.build(src)
+    _ = tgt.device.incidence
+    mass = tgt.device.mass
+    return tgt, src, fs, loc, mass
+
+
+def fp64_peak(tt, torch):
+    """Measured DFMA issue ceiling (TFLOP/s) from tt_fp64_peak_probe."""
+    import ctypes as C
+    from paper_2603_00538_b200 import _lib
+    blocks, threads = C.c_int(0), C.c_int(0)
+    _lib.call("tt_fp64_peak_probe", 0, None, C.byref(blocks), C.byref(threads), None)
+    sink = torch.empty(blocks.value * threads.value, dtype=torch.float64, device="cuda")
+    iters = 2000
+    best = 0.0
+    for _ in range(4):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        _lib.call("tt_fp64_peak_probe", iters, _lib.ptr(sink), None, None, _lib.stream_handle())
+        e.record()
+        e.synchronize()
+        ms = s.elapsed_time(e)
+        flops = 2.0 * 8 * 16 * iters * blocks.value * threads.value
+        best = max(best, flops / (ms * 1e-3) / 1e12)
+    return best
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_2603_00538_b200 as tt
+    from paper_2603_00538_b200.fem import decode_result, pcg_device
+    from paper_2603_00538_b200.montecarlo import load_vector, _raise_status
+    from paper_2603_00538_b200 import _lib
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    tgt, src, fs, loc, mass = build_problem(args, tt)
+    box = tt.MeshBackedField(fs, loc)
+    E = tgt.n_elems
+    e_lo, e_hi = E * rank // world, E * (rank + 1) // world
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+    status = _lib.status_word()
+
+    def step(plan, ev=None):
+        if ev is not None:
+            ev[0].record()
+        b = load_vector(tgt, box, plan, e_lo, e_hi, deterministic=True, check=False, status=status)
+        if ev is not None:
+            ev[1].record()
+        if world > 1:
+            dist.all_reduce(b)
+        x, best_x, res = pcg_device(mass, b, tol=1e-12)
+        return x, res
+
+    def timed(plan, steps, warmup, kernel_events=True):
+        for _ in range(warmup):
+            step(plan)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        tot, ker = [], []
+        for _ in range(steps):
+            flush.zero_()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ks = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            s.record()
+            x, res = step(plan, ks if kernel_events else None)
+            e.record()
+            tot.append((s, e))
+            ker.append(ks)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ms = sum(s.elapsed_time(e) for s, e in tot)
+        kms = [a.elapsed_time(b) for a, b in ker] if kernel_events else []
+        return ms, kms, x, res
+
+    plan = tt.SamplePlan.build(args.samples, args.mode, 0, dim=3)
+    with ClockSampler(local) as clk:
+        ms, kms, x, res = timed(plan, args.steps, args.warmup)
+    r = decode_result(res)
+    _raise_status(int(status.item()))
+    assert r.converged, "PCG did not converge"
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item()) / args.steps
+    S = E * args.samples
+    value = S / (ms_step * 1e-3)
+    load_ms = statistics.mean(kms)   # mc_load + reduce_nodes, per step
+
+    # --- dominant kernel alone (mc_load_kernel), CUDA events on the launch stream
+    from paper_2603_00538_b200.montecarlo import element_contributions
+    contrib = torch.empty((e_hi - e_lo, 4), dtype=torch.float64, device="cuda")
+    kt = []
+    for i in range(args.warmup + args.steps):
+        flush.zero_()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        element_contributions(tgt, box, plan, e_lo, e_hi, out=contrib, status=status)
+        e.record()
+        if i >= args.warmup:
+            kt.append((s, e))
+    torch.cuda.synchronize()
+    k_ms = statistics.mean(a.elapsed_time(b) for a, b in kt)
+    E_loc = e_hi - e_lo
+    n_cells = loc.dims[0] * loc.dims[1] * loc.dims[2]
+    alg_bytes = (E_loc * (4 * 4 + 8 * 3 * 4 + 8 + 8 * 4)       # target conn, coords, measure, contrib
+                 + 8 * (n_cells + 1) + 4 * int(loc.cell_elems_dev.numel())
+                 + src.n_elems * (8 * 12 + 4 * 4) + 8 * src.n_nodes)
+    peak_hbm = None
+    try:
+        peak_hbm = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"]
+        peak_src = "measured"
+    except Exception:
+        peak_hbm, peak_src = 6650.0, "fallback"
+    achieved = alg_bytes / (k_ms * 1e-3) / 1e9
+    fp64 = fp64_peak(tt, torch)
+
+    # --- e2e: public API, pinned host coefficients in, x out, every step
+    c_host = torch.from_numpy(fs.coeffs.copy()).pin_memory()
+    x_host = torch.empty(tgt.n_nodes, dtype=torch.float64).pin_memory()
+    c_dev = torch.empty(src.n_nodes, dtype=torch.float64, device="cuda")
+
+    def e2e_step():
+        c_dev.copy_(c_host, non_blocking=True)
+        field = tt.NodalField(src, c_dev)
+        b = load_vector(tgt, tt.MeshBackedField(field, loc), plan, e_lo, e_hi)
+        if world > 1:
+            dist.all_reduce(b)
+        xx = tt.cg_solve(mass, b, tol=1e-12)
+        x_host.copy_(xx, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+    for _ in range(args.warmup):
+        e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev = []
+    for _ in range(args.steps):
+        flush.zero_()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        e2e_step()
+        e.record()
+        ev.append((s, e))
+    torch.cuda.synchronize()
+    e2e_ms = torch.tensor([sum(a.elapsed_time(b) for a, b in ev) / args.steps], dtype=torch.float64,
+                          device="cuda")
+    if world > 1:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_ms = float(e2e_ms.item())
+
+    # --- samples/element sweep (same step, fewer repetitions)
+    sweep = {}
+    if args.sweep:
+        for n in [int(v) for v in args.sweep.split(",") if v]:
+            p = tt.SamplePlan.build(n, args.mode, 0, dim=3)
+            m, km, _, rr = timed(p, max(2, args.steps // 3), 1)
+            tt_ = torch.tensor([m / max(2, args.steps // 3)], dtype=torch.float64, device="cuda")
+            if world > 1:
+                dist.all_reduce(tt_, op=dist.ReduceOp.MAX)
+            sweep[str(n)] = {"ms_per_step": round(float(tt_.item()), 4),
+                             "samples_per_s": E * n / (float(tt_.item()) * 1e-3),
+                             "load_ms": round(statistics.mean(km), 4)}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args, tgt, src, fs, seconds=args.cpu_seconds)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (generated meshes, analytic field interpolated on the source)",
+            "config": workload_config(args, world),
+            "load_ms_per_step": load_ms, "pcg_iterations": int(r.iterations),
+            "e2e": {"value": S / (e2e_ms * 1e-3), "unit": "samples/s", "ms_per_step": e2e_ms,
+                    "h2d_bytes_per_step": src.n_nodes * 8, "d2h_bytes_per_step": tgt.n_nodes * 8,
+                    "api": "NodalField(pinned->device) + MeshBackedField + load_vector + cg_solve"},
+            "roofline": {"bound": "hbm", "kernel": "mc_load_kernel<3,SHARED,MESH,32>",
+                         "achieved": achieved, "peak": peak_hbm, "unit": "GB/s",
+                         "frac": achieved / peak_hbm, "peak_source": peak_src,
+                         "traffic": None, "kernel_ms": k_ms, "algorithmic_bytes": alg_bytes,
+                         "note": "fused on-the-fly kernel: <1 compulsory HBM byte per sample; "
+                                 "its ceiling is FP64 issue / L1 gather, see fp64_peak_tflops"},
+            "fp64_peak_tflops": fp64,
+            "sweep": sweep,
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+            "gpu_launches": 3 * args.steps,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# --------------------------------------------------------------------- CPU
+def cpu_baseline(args, tgt, src, fs, seconds=12.0):
+    """The oracle restatement (numpy, 3-D) on a bounded sample of the same workload."""
+    import numpy as np
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import tt_oracle as O
+    t0 = time.perf_counter()
+    g = O.Grid(src.nodes, src.elements)
+    setup_s = time.perf_counter() - t0
+    lam = O.bary_map(O.sobol(args.samples, 3))
+    coeffs = np.asarray(fs.coeffs)
+    srcf = lambda P: O.mesh_backed_eval(g, coeffs, P)  # noqa: E731
+    area = tgt.elem_areas
+    threads = os.cpu_count() or 1
+    n_el, done, t_used = 256, 0, 0.0
+    while t_used < seconds and done < tgt.n_elems:
+        lo, hi = done, min(done + n_el, tgt.n_elems)
+        t = time.perf_counter()
+        sub = tgt.elements[lo:hi]
+        bounds = [(a, min(a + O.CHUNK, hi - lo)) for a in range(0, hi - lo, O.CHUNK)]
+        from concurrent.futures import ThreadPoolExecutor
+
+        def run(b):
+            return O.accumulate(tgt.nodes, sub, area[lo:hi], lam, srcf, b)
+        with ThreadPoolExecutor(max_workers=threads) as ex:
+            list(ex.map(run, bounds))
+        t_used += time.perf_counter() - t
+        done = hi
+        n_el = min(n_el * 2, 65536)
+    sps = done * args.samples / t_used
+    return {"value": sps, "unit": "samples/s", "cores": threads, "kind": "port",
+            "sample": f"oracle 3-D MC load on the first {done} of {tgt.n_elems} target elements, "
+                      f"N={args.samples} ({done * args.samples} samples, {t_used:.1f} s); "
+                      f"grid setup {setup_s:.1f} s untimed",
+            "impl": "oracle/tt_oracle.py (numpy restatement; reference is 2-D only)"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import numpy as np
+    sys.path.insert(0, str(ROOT))
+    import paper_2603_00538_b200.mesh as M   # host-only mesh generators (no GPU use)
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import tt_oracle as O
+    tgt = M.generate_cube_mesh(args.n, 0.2, seed=20, split="kuhn")
+    src = M.generate_cube_mesh(args.n, 0.2, seed=10, split="kuhn_mirror")
+
+    class _F:
+        coeffs = np.sin(src.nodes[:, 0]) * np.cos(src.nodes[:, 1]) * np.cos(src.nodes[:, 2]) + 2
+    cpu = cpu_baseline(args, tgt, src, _F, seconds=args.cpu_seconds)
+    # the PCG on the full target mesh (scipy CSR, the reference's solver) once
+    t = time.perf_counter()
+    Mm = O.mass_matrix(tgt.n_nodes, tgt.elements, tgt.elem_areas, 3)
+    rhs = Mm @ np.ones(tgt.n_nodes)
+    O.cg_solve(Mm, rhs, tol=1e-12)
+    cg_s = time.perf_counter() - t
+    S = tgt.n_elems * args.samples
+    step_s = S / cpu["value"] + cg_s
+    value = S / step_s
+    cpu_line = dict(cpu)
+    cpu_line["value"] = value
+    cpu_line["sample"] += f"; step = extrapolated load + full-size PCG ({cg_s:.2f} s)"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(args, world), "cpu_baseline": cpu_line,
+            "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,249 @@
+/*
+ * tt_b200.h -- C ABI of the B200-native Monte-Carlo conservative transfer library
+ * (libtt_b200.so).  Plain pointers and sizes only; every pointer to array data is a
+ * DEVICE pointer unless the comment says "host"; every call is stream-ordered on the
+ * caller's cudaStream_t (passed as void*; NULL = legacy default stream) and returns a
+ * TT_* status code (launch/parameter errors).  Data-dependent errors raised inside
+ * kernels (non-finite source values, strict-outside samples) are OR-ed into a caller
+ * supplied device int32 status word as TT_FLAG_* bits.
+ *
+ * Reference interfaces replaced (all in /root/reference/pkg/src/tritransfer):
+ *   tt_locate_many        <- _kernels.locate_many            _kernels/_compiled.pyx:127-175
+ *                            (the reference's only native FFI seam; same argument list)
+ *   tt_locate             <- UniformGridLocator.locate_many   locate.py:76-88 (d = 2, 3)
+ *   tt_nearest / tt_snap  <- UniformGridLocator.nearest_element locate.py:97-127 and the
+ *                            snap branch of MeshBackedField    montecarlo.py:53-63
+ *   tt_grid_count/_fill   <- UniformGridLocator.build          locate.py:33-74
+ *   tt_plan_sobol         <- sobol.sobol_2d                    sobol.py:34-52 (d = 2, 3)
+ *   tt_plan_pcg64         <- SamplePlan.build(mode="uniform")  montecarlo.py:100-102
+ *   tt_bary_map           <- montecarlo.bary_map               montecarlo.py:68-77
+ *   tt_plan_philox        <- (new) per-element counter-based streams
+ *   tt_geometry           <- TriMesh areas/_bary_inv/centroids mesh.py:24-29,136-159
+ *   tt_bbox               <- TriMesh.bbox                      mesh.py:110-111
+ *   tt_mc_load            <- montecarlo._accumulate            montecarlo.py:110-141
+ *                            (+ SourceField.__call__: AnalyticField :20-29,
+ *                             MeshBackedField :49-65, NodalField.eval_in_elements fem.py:36-38)
+ *   tt_mc_cache_ids       <- MCTransferOperator.__init__ localisation transfer.py:74-87
+ *   tt_map_points         <- einsum("nj,ejd->end")             montecarlo.py:123-124
+ *   tt_eval_points        <- SourceField.__call__ on given points
+ *   tt_incidence_*        <- (support for np.add.at ordering)  montecarlo.py:144-147
+ *   tt_reduce_nodes       <- montecarlo._reduce_to_nodes       montecarlo.py:144-147
+ *   tt_mass_*             <- fem.assemble_mass_matrix          fem.py:78-110
+ *   tt_pcg                <- fem.cg_solve                      fem.py:113-152
+ *   tt_integrate_p1       <- fem.integrate_field               fem.py:155-161
+ */
+#ifndef TT_B200_H
+#define TT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (mapped onto errors.py exceptions by the host layer) ---- */
+#define TT_OK                   0
+#define TT_ERR_INVALID_PARAMETER 1  /* errors.InvalidParameter   errors.py:29-30 */
+#define TT_ERR_DIMENSION_MISMATCH 2 /* errors.DimensionMismatch  errors.py:37-38 */
+#define TT_ERR_CUDA             3   /* launch / runtime failure (tt_last_error has text) */
+#define TT_ERR_CAPACITY         4   /* a fixed per-row / per-cell capacity was exceeded */
+
+/* ---- device status flags written by kernels ---- */
+#define TT_FLAG_NONFINITE        1  /* SourceEvalFailed: non-finite f  montecarlo.py:126-127 */
+#define TT_FLAG_OUTSIDE_STRICT   2  /* SourceEvalFailed: strict policy montecarlo.py:55-57 */
+#define TT_FLAG_CAPACITY         4  /* row/list capacity exceeded in assembly            */
+#define TT_FLAG_INVALID_DENSITY  8  /* InvalidDensity: p <= 0          montecarlo.py:129-130 */
+
+/* ---- enums ---- */
+#define TT_PLAN_SHARED  0   /* one (N, k) barycentric table shared by all elements (reference) */
+#define TT_PLAN_PHILOX  1   /* per-element Philox4x32-10 streams, mapped in-register          */
+
+#define TT_SRC_EXPR     0   /* analytic field: postfix program evaluated in-kernel            */
+#define TT_SRC_MESH     1   /* P1 nodal field on a source mesh + uniform-grid locator          */
+#define TT_SRC_VALUES   2   /* precomputed values f[e - e_lo, j] (host black boxes)             */
+#define TT_SRC_CACHED   3   /* P1 nodal field at cached source element ids (MCTransferOperator):
+                               lambda_s recomputed, clipped >= 0 and renormalised, transfer.py:84-87 */
+
+#define TT_OUTSIDE_SNAP   0
+#define TT_OUTSIDE_STRICT 1
+
+/* expression opcodes (postfix); operands: x, y, z coordinates and constants */
+#define TT_OP_CONST 0
+#define TT_OP_X     1
+#define TT_OP_Y     2
+#define TT_OP_Z     3
+#define TT_OP_ADD   4
+#define TT_OP_SUB   5
+#define TT_OP_MUL   6
+#define TT_OP_DIV   7
+#define TT_OP_POW   8
+#define TT_OP_NEG   9
+#define TT_OP_SIN   10
+#define TT_OP_COS   11
+#define TT_OP_EXP   12
+#define TT_OP_SQRT  13
+#define TT_OP_LOG   14
+#define TT_OP_TAN   15
+#define TT_OP_ABS   16
+#define TT_OP_SQUARE 17
+#define TT_EXPR_MAX_OPS 64
+#define TT_EXPR_MAX_STACK 16
+
+/* ---- descriptors (host structs holding device pointers) ---- */
+typedef struct tt_mesh {
+    int32_t dim;              /* 2 = triangles, 3 = tetrahedra; k = dim + 1 vertices */
+    int32_t reserved;
+    int64_t n_nodes;
+    int64_t n_elems;
+    const double*  nodes;     /* (n_nodes, dim) row-major */
+    const int32_t* elems;     /* (n_elems, k) row-major, positively oriented */
+    const double*  measure;   /* (n_elems,) |area| / |volume| (may be NULL where unused) */
+} tt_mesh_t;
+
+/* Packed per-element locate record: binv (dim x dim, row-major) then origin (dim);
+ * stride TT_REC_STRIDE(dim) doubles (64 B in 2-D, 128 B in 3-D: one aligned line). */
+#define TT_REC_STRIDE(dim) ((dim) == 2 ? 8 : 16)
+
+typedef struct tt_grid {
+    int32_t dim;
+    int32_t n[3];             /* cells per axis; n[2] = 1 in 2-D; cell = (ix*n1 + iy)*n2 + iz */
+    double  lo[3];            /* mesh bbox (min corner) */
+    double  hi[3];            /* mesh bbox (max corner) */
+    int64_t n_elems;
+    const int64_t* cell_start;  /* (n0*n1*n2 + 1) CSR offsets */
+    const int32_t* cell_elems;  /* ascending element ids per cell */
+    const double*  rec;         /* (n_elems, TT_REC_STRIDE(dim)) packed binv/origin */
+    const double*  centroids;   /* (n_elems, dim) */
+} tt_grid_t;
+
+typedef struct tt_plan {
+    int32_t  kind;            /* TT_PLAN_SHARED | TT_PLAN_PHILOX */
+    int32_t  dim;
+    int64_t  n_samples;       /* N samples per element */
+    const double* lam;        /* SHARED: (N, dim+1) barycentric table */
+    uint64_t seed;            /* PHILOX: key */
+} tt_plan_t;
+
+typedef struct tt_expr {
+    int32_t n_ops;
+    int32_t ops[TT_EXPR_MAX_OPS];
+    double  consts[TT_EXPR_MAX_OPS];
+} tt_expr_t;
+
+typedef struct tt_source {
+    int32_t kind;             /* TT_SRC_* */
+    int32_t outside;          /* TT_OUTSIDE_SNAP | TT_OUTSIDE_STRICT (mesh sources) */
+    int32_t dim;              /* point dimension the source is queried in (2 or 3) */
+    int32_t reserved;
+    tt_expr_t expr;           /* TT_SRC_EXPR program (passed by value into the kernel) */
+    tt_grid_t grid;           /* TT_SRC_MESH locator over the source mesh */
+    const int32_t* src_elems; /* TT_SRC_MESH (E_s, k) */
+    const double*  coeffs;    /* TT_SRC_MESH (n_s,) nodal coefficients */
+    const double*  values;    /* TT_SRC_VALUES (e_hi - e_lo, N) */
+    const int32_t* cached_ids;/* TT_SRC_CACHED (e_hi - e_lo, N) source element per sample */
+} tt_source_t;
+
+typedef struct tt_pcg_result {
+    int64_t iterations;       /* iterations performed */
+    double  residual;         /* final relative recurrence residual */
+    double  best_residual;    /* best relative residual seen */
+    int32_t converged;        /* 1 if residual <= tol */
+    int32_t zero_rhs;         /* 1 if ||b|| == 0 (x = 0 returned) */
+} tt_pcg_result_t;
+
+/* ---- library ---- */
+const char* tt_last_error(void);
+int tt_version(void);
+int tt_device_sm_count(int* out);   /* host int */
+
+/* ---- plans ---- */
+int tt_plan_sobol(int dim, int64_t count, int64_t skip, double* param /* (count, dim) */,
+                  void* stream);
+int tt_plan_pcg64(int dim, int64_t count, uint64_t state_hi, uint64_t state_lo,
+                  uint64_t inc_hi, uint64_t inc_lo, double* param, void* stream);
+int tt_bary_map(int dim, int64_t count, const double* param, double* lam /* (count, dim+1) */,
+                void* stream);
+int tt_plan_philox(int dim, int64_t e_lo, int64_t e_hi, int64_t n_samples, uint64_t seed,
+                   double* param /* (e_hi-e_lo, N, dim) */, void* stream);
+
+/* ---- geometry ---- */
+int tt_geometry(const tt_mesh_t* mesh, double* signed_measure /* (E,) or NULL */,
+                double* rec /* (E, TT_REC_STRIDE) or NULL */, double* centroids /* or NULL */,
+                void* stream);
+int tt_bbox(int dim, int64_t n_nodes, const double* nodes, double* out /* (2, dim): lo, hi */,
+            void* stream);
+
+/* ---- uniform-grid locator ---- */
+int tt_grid_count(const tt_mesh_t* mesh, const tt_grid_t* grid /* dims + bbox used */,
+                  int64_t* cell_start /* (ncells + 1): exclusive scan of counts */,
+                  void* stream);
+int tt_grid_fill(const tt_mesh_t* mesh, const tt_grid_t* grid /* dims, bbox, cell_start */,
+                 int32_t* cell_elems, int64_t* cursor_scratch /* (ncells) */, void* stream);
+int tt_locate(const tt_grid_t* grid, const double* points, int64_t count, double eps,
+              int32_t* elem /* (count,) -1 = outside */, double* lam /* (count, dim+1) */,
+              void* stream);
+int tt_locate_many(const double* points, int64_t count, int nx, int ny,
+                   const double* bbox_host /* host (xmin, ymin, xmax, ymax) */,
+                   const int64_t* cell_start, const int32_t* cell_elems,
+                   const double* binv /* (E,2,2) */, const double* origin /* (E,2) */,
+                   double eps, int32_t* elem, double* lam /* (count,3) */, void* stream);
+int tt_nearest(const tt_grid_t* grid, const double* points, int64_t count,
+               int32_t* elem /* out */, void* stream);
+int tt_snap(const tt_grid_t* grid, const double* points, int64_t count,
+            int32_t* elem /* in/out: -1 entries replaced */, double* lam /* in/out */,
+            void* stream);
+
+/* ---- Monte-Carlo load ---- */
+int tt_map_points(const tt_mesh_t* target, int64_t e_lo, int64_t e_hi, const tt_plan_t* plan,
+                  double* points /* (e_hi-e_lo, N, dim) */, void* stream);
+int tt_eval_points(const tt_source_t* src, const double* points, int64_t count,
+                   double* values, int32_t* status, void* stream);
+int tt_mc_load(const tt_mesh_t* target, int64_t e_lo, int64_t e_hi, const tt_plan_t* plan,
+               const tt_source_t* src,
+               double* contrib /* (e_hi-e_lo, k) or NULL */,
+               double* b /* (n_nodes) atomically accumulated when contrib == NULL */,
+               int32_t* status, void* stream);
+
+int tt_mc_cache_ids(const tt_mesh_t* target, int64_t e_lo, int64_t e_hi, const tt_plan_t* plan,
+                    const tt_grid_t* grid, int32_t* ids /* (e_hi-e_lo, N): located or snapped */,
+                    void* stream);
+
+/* ---- node reduction / incidence (deterministic np.add.at order) ---- */
+int tt_incidence_count(const tt_mesh_t* mesh, int64_t* inc_start /* (n_nodes+1) */,
+                       void* stream);
+int tt_incidence_fill(const tt_mesh_t* mesh, const int64_t* inc_start,
+                      int32_t* inc /* (E*k) entries e*k+a, ascending per node */,
+                      int64_t* cursor_scratch /* (n_nodes) */, void* stream);
+int tt_reduce_nodes(int64_t n_nodes, int k, const int64_t* inc_start, const int32_t* inc,
+                    int64_t e_lo, int64_t e_hi, const double* contrib, double* b,
+                    void* stream);
+
+/* ---- P1 mass matrix (CSR, exactly symmetric) ---- */
+int tt_mass_pattern(const tt_mesh_t* mesh, const int64_t* inc_start, const int32_t* inc,
+                    int64_t* row_ptr /* (n_nodes+1) exclusive scan of row lengths */,
+                    int32_t* status, void* stream);
+int tt_mass_fill(const tt_mesh_t* mesh, const int64_t* inc_start, const int32_t* inc,
+                 const double* local_host /* host (k, k) reference-element mass */,
+                 const int64_t* row_ptr, int32_t* cols, double* vals, void* stream);
+
+/* ---- Jacobi-preconditioned CG (single cooperative launch) ---- */
+int64_t tt_pcg_workspace_doubles(int64_t n);
+int tt_pcg(int64_t n, const int64_t* row_ptr, const int32_t* cols, const double* vals,
+           const double* b, double tol, int64_t maxiter, double* x, double* best_x,
+           double* work /* tt_pcg_workspace_doubles(n) */, tt_pcg_result_t* result /* device */,
+           void* stream);
+int tt_spmv(int64_t n, const int64_t* row_ptr, const int32_t* cols, const double* vals,
+            const double* x, double* y, void* stream);
+
+/* ---- reporting ---- */
+int tt_integrate_p1(const tt_mesh_t* mesh, const double* coeffs, double* out /* device scalar */,
+                    void* stream);
+
+/* ---- measurement helpers ---- */
+int tt_fp64_peak_probe(int64_t iters, double* sink /* (blocks*threads) */, int* blocks_out,
+                       int* threads_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TT_B200_H */

@@ -1,0 +1,189 @@
+"""ctypes binding of the C ABI in ``include/tt_b200.h`` (libtt_b200.so).
+
+This is the only place the host layer crosses into native code.  There is no CPU
+fallback: if the library or a CUDA device is missing every entry point raises
+``DeviceUnavailable`` (loudly, at first use).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import torch
+
+from .errors import (DeviceUnavailable, DimensionMismatch, InvalidParameter,
+                     TransferError)
+
+LIB_PATH = Path(__file__).resolve().parent / "libtt_b200.so"
+
+TT_OK, TT_ERR_INVALID_PARAMETER, TT_ERR_DIMENSION_MISMATCH, TT_ERR_CUDA, TT_ERR_CAPACITY = 0, 1, 2, 3, 4
+TT_FLAG_NONFINITE, TT_FLAG_OUTSIDE_STRICT, TT_FLAG_CAPACITY, TT_FLAG_INVALID_DENSITY = 1, 2, 4, 8
+TT_PLAN_SHARED, TT_PLAN_PHILOX = 0, 1
+TT_SRC_EXPR, TT_SRC_MESH, TT_SRC_VALUES, TT_SRC_CACHED = 0, 1, 2, 3
+TT_OUTSIDE_SNAP, TT_OUTSIDE_STRICT = 0, 1
+TT_EXPR_MAX_OPS, TT_EXPR_MAX_STACK = 64, 16
+
+OPS = {"const": 0, "x": 1, "y": 2, "z": 3, "add": 4, "sub": 5, "mul": 6, "div": 7,
+       "pow": 8, "neg": 9, "sin": 10, "cos": 11, "exp": 12, "sqrt": 13, "log": 14,
+       "tan": 15, "abs": 16, "square": 17}
+
+
+def rec_stride(dim: int) -> int:
+    return 8 if dim == 2 else 16
+
+
+class tt_mesh_t(C.Structure):
+    _fields_ = [("dim", C.c_int32), ("reserved", C.c_int32), ("n_nodes", C.c_int64),
+                ("n_elems", C.c_int64), ("nodes", C.c_void_p), ("elems", C.c_void_p),
+                ("measure", C.c_void_p)]
+
+
+class tt_grid_t(C.Structure):
+    _fields_ = [("dim", C.c_int32), ("n", C.c_int32 * 3), ("lo", C.c_double * 3),
+                ("hi", C.c_double * 3), ("n_elems", C.c_int64), ("cell_start", C.c_void_p),
+                ("cell_elems", C.c_void_p), ("rec", C.c_void_p), ("centroids", C.c_void_p)]
+
+
+class tt_plan_t(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("dim", C.c_int32), ("n_samples", C.c_int64),
+                ("lam", C.c_void_p), ("seed", C.c_uint64)]
+
+
+class tt_expr_t(C.Structure):
+    _fields_ = [("n_ops", C.c_int32), ("ops", C.c_int32 * TT_EXPR_MAX_OPS),
+                ("consts", C.c_double * TT_EXPR_MAX_OPS)]
+
+
+class tt_source_t(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("outside", C.c_int32), ("dim", C.c_int32),
+                ("reserved", C.c_int32), ("expr", tt_expr_t), ("grid", tt_grid_t),
+                ("src_elems", C.c_void_p), ("coeffs", C.c_void_p), ("values", C.c_void_p),
+                ("cached_ids", C.c_void_p)]
+
+
+class tt_pcg_result_t(C.Structure):
+    _fields_ = [("iterations", C.c_int64), ("residual", C.c_double),
+                ("best_residual", C.c_double), ("converged", C.c_int32),
+                ("zero_rhs", C.c_int32)]
+
+
+_P = C.c_void_p
+_I64 = C.c_int64
+_I = C.c_int
+_D = C.c_double
+_U64 = C.c_uint64
+
+_SIGNATURES = {
+    "tt_last_error": ([], C.c_char_p),
+    "tt_version": ([], _I),
+    "tt_device_sm_count": ([C.POINTER(_I)], _I),
+    "tt_plan_sobol": ([_I, _I64, _I64, _P, _P], _I),
+    "tt_plan_pcg64": ([_I, _I64, _U64, _U64, _U64, _U64, _P, _P], _I),
+    "tt_bary_map": ([_I, _I64, _P, _P, _P], _I),
+    "tt_plan_philox": ([_I, _I64, _I64, _I64, _U64, _P, _P], _I),
+    "tt_geometry": ([C.POINTER(tt_mesh_t), _P, _P, _P, _P], _I),
+    "tt_bbox": ([_I, _I64, _P, _P, _P], _I),
+    "tt_grid_count": ([C.POINTER(tt_mesh_t), C.POINTER(tt_grid_t), _P, _P], _I),
+    "tt_grid_fill": ([C.POINTER(tt_mesh_t), C.POINTER(tt_grid_t), _P, _P, _P], _I),
+    "tt_locate": ([C.POINTER(tt_grid_t), _P, _I64, _D, _P, _P, _P], _I),
+    "tt_locate_many": ([_P, _I64, _I, _I, C.POINTER(_D), _P, _P, _P, _P, _D, _P, _P, _P], _I),
+    "tt_nearest": ([C.POINTER(tt_grid_t), _P, _I64, _P, _P], _I),
+    "tt_snap": ([C.POINTER(tt_grid_t), _P, _I64, _P, _P, _P], _I),
+    "tt_map_points": ([C.POINTER(tt_mesh_t), _I64, _I64, C.POINTER(tt_plan_t), _P, _P], _I),
+    "tt_eval_points": ([C.POINTER(tt_source_t), _P, _I64, _P, _P, _P], _I),
+    "tt_mc_load": ([C.POINTER(tt_mesh_t), _I64, _I64, C.POINTER(tt_plan_t),
+                    C.POINTER(tt_source_t), _P, _P, _P, _P], _I),
+    "tt_mc_cache_ids": ([C.POINTER(tt_mesh_t), _I64, _I64, C.POINTER(tt_plan_t),
+                         C.POINTER(tt_grid_t), _P, _P], _I),
+    "tt_incidence_count": ([C.POINTER(tt_mesh_t), _P, _P], _I),
+    "tt_incidence_fill": ([C.POINTER(tt_mesh_t), _P, _P, _P, _P], _I),
+    "tt_reduce_nodes": ([_I64, _I, _P, _P, _I64, _I64, _P, _P, _P], _I),
+    "tt_mass_pattern": ([C.POINTER(tt_mesh_t), _P, _P, _P, _P, _P], _I),
+    "tt_mass_fill": ([C.POINTER(tt_mesh_t), _P, _P, C.POINTER(_D), _P, _P, _P, _P], _I),
+    "tt_pcg_workspace_doubles": ([_I64], _I64),
+    "tt_pcg": ([_I64, _P, _P, _P, _P, _D, _I64, _P, _P, _P, _P, _P], _I),
+    "tt_spmv": ([_I64, _P, _P, _P, _P, _P, _P], _I),
+    "tt_integrate_p1": ([C.POINTER(tt_mesh_t), _P, _P, _P], _I),
+    "tt_fp64_peak_probe": ([_I64, _P, C.POINTER(_I), C.POINTER(_I), _P], _I),
+}
+
+EXPORTED = tuple(_SIGNATURES)
+
+_lib = None
+
+
+def load_library(require_device: bool = True):
+    """Load libtt_b200.so (and check for a CUDA device unless told otherwise)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise DeviceUnavailable(
+                f"{LIB_PATH.name} is not built; run __graft_entry__.build() "
+                "(there is no CPU fallback)")
+        lib = C.CDLL(str(LIB_PATH))
+        for name, (args, res) in _SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = lib
+    if require_device and not torch.cuda.is_available():
+        raise DeviceUnavailable("no CUDA device visible: this framework has no CPU path")
+    return _lib
+
+
+def lib():
+    return load_library(True)
+
+
+def stream_handle(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def check(code: int, what: str = ""):
+    if code == TT_OK:
+        return
+    msg = (_lib.tt_last_error() or b"").decode(errors="replace")
+    text = f"{what}: {msg}" if what else msg
+    if code == TT_ERR_INVALID_PARAMETER:
+        raise InvalidParameter(text)
+    if code == TT_ERR_DIMENSION_MISMATCH:
+        raise DimensionMismatch(text)
+    raise TransferError(f"CUDA library error {code}: {text}")
+
+
+def call(name: str, *args):
+    fn = getattr(lib(), name)
+    check(fn(*args), name)
+
+
+def ptr(t) -> C.c_void_p:
+    if t is None:
+        return C.c_void_p(None)
+    return C.c_void_p(t.data_ptr())
+
+
+def device() -> torch.device:
+    lib()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def sm_count() -> int:
+    out = C.c_int(0)
+    lib().tt_device_sm_count(C.byref(out))
+    return out.value
+
+
+def status_word() -> torch.Tensor:
+    return torch.zeros(1, dtype=torch.int32, device=device())
+
+
+def mesh_desc(dim, n_nodes, n_elems, nodes, elems, measure=None) -> tt_mesh_t:
+    return tt_mesh_t(dim, 0, n_nodes, n_elems, ptr(nodes).value, ptr(elems).value,
+                     ptr(measure).value)
+
+
+if os.environ.get("TT_B200_EAGER_LOAD"):
+    load_library(False)

@@ -1,0 +1,247 @@
+// Shared device helpers for libtt_b200 (sm_100a).
+//
+// Bit-exactness contract: every operation that feeds an element id, a grid cell or a
+// barycentric coordinate that the reference computes in plain IEEE double (numpy /
+// Cython compiled without FMA, SURVEY.md finding 5) is written with the explicit
+// round-to-nearest intrinsics below, which nvcc never contracts into DFMA.  Reductions
+// whose order differs from the reference anyway (load vector sums, CG dots) may use FMA.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+#include "../../include/tt_b200.h"
+
+#define TT_HD __host__ __device__ __forceinline__
+#define TT_D __device__ __forceinline__
+
+namespace tt {
+
+// -------------------------------------------------------------- exact arithmetic
+TT_D double mul(double a, double b) { return __dmul_rn(a, b); }
+TT_D double add(double a, double b) { return __dadd_rn(a, b); }
+TT_D double sub(double a, double b) { return __dsub_rn(a, b); }
+TT_D double div(double a, double b) { return __ddiv_rn(a, b); }
+
+// C `(int)t` as compiled for x86-64 (cvttsd2si): truncation, and INT_MIN for NaN or
+// out-of-range values (the reference's `<int>` cast, _compiled.pyx:151-152).
+TT_D int c_int_cast(double t) {
+    return (t > -2147483649.0 && t < 2147483648.0) ? (int)t : (int)0x80000000;
+}
+
+// cell index along one axis: trunc(((v - lo) / (hi - lo)) * n), clamped to [0, n-1]
+TT_D int axis_cell(double v, double lo, double hi, int n) {
+    int i = c_int_cast(mul(div(sub(v, lo), sub(hi, lo)), (double)n));
+    i = i < 0 ? 0 : i;
+    return i > n - 1 ? n - 1 : i;
+}
+
+// -------------------------------------------------------------- error plumbing
+void set_error(const char* fmt, ...);
+int cuda_status(cudaError_t e, const char* what);
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline int launch_check(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    return cuda_status(e, what);
+}
+
+inline unsigned grid_for(int64_t n, int block) {
+    int64_t g = (n + block - 1) / block;
+    if (g < 1) g = 1;
+    if (g > 0x7fffffff) g = 0x7fffffff;
+    return (unsigned)g;
+}
+
+int sm_count();
+
+// --------------------------------------------------------------- locate records
+template <int D>
+struct Rec {
+    double b[D][D];
+    double o[D];
+};
+
+// Packed record load: 2-D = 6 doubles of an 8-double (64 B) slot, 3-D = 12 of 16 (128 B).
+template <int D>
+TT_D void load_rec(const double* __restrict__ rec, int64_t e, Rec<D>& r) {
+    if constexpr (D == 2) {
+        const double2* p = reinterpret_cast<const double2*>(rec + e * 8);
+        double2 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
+        r.b[0][0] = a.x; r.b[0][1] = a.y; r.b[1][0] = b.x; r.b[1][1] = b.y;
+        r.o[0] = c.x; r.o[1] = c.y;
+    } else {
+        const double2* p = reinterpret_cast<const double2*>(rec + e * 16);
+        double2 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
+        double2 d = __ldg(p + 3), f = __ldg(p + 4), g = __ldg(p + 5);
+        r.b[0][0] = a.x; r.b[0][1] = a.y; r.b[0][2] = b.x;
+        r.b[1][0] = b.y; r.b[1][1] = c.x; r.b[1][2] = c.y;
+        r.b[2][0] = d.x; r.b[2][1] = d.y; r.b[2][2] = f.x;
+        r.o[0] = f.y; r.o[1] = g.x; r.o[2] = g.y;
+    }
+}
+
+// lambda_i = (b_i0*rx + b_i1*ry) [+ b_i2*rz]; lambda_last = ((1 - l0) - l1) [- l2]
+// (_compiled.pyx:162-167; mesh.py:161-169)
+template <int D>
+TT_D void bary_from_rec(const Rec<D>& r, const double* x, double* lam) {
+    double rel[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) rel[c] = sub(x[c], r.o[c]);
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        double acc = add(mul(r.b[i][0], rel[0]), mul(r.b[i][1], rel[1]));
+        if constexpr (D == 3) acc = add(acc, mul(r.b[i][2], rel[2]));
+        lam[i] = acc;
+    }
+    double last = sub(sub(1.0, lam[0]), lam[1]);
+    if constexpr (D == 3) last = sub(last, lam[2]);
+    lam[D] = last;
+}
+
+template <int D>
+TT_D bool inside_eps(const double* lam, double eps) {
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i <= D; ++i) ok = ok && (lam[i] >= -eps);
+    return ok;
+}
+
+// point = ((l0*v0 + l1*v1) + l2*v2) [+ l3*v3] per coordinate (montecarlo.py:123-124)
+template <int D>
+TT_D void map_point(const double* lam, const double (*v)[D], double* x) {
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+        double acc = add(mul(lam[0], v[0][c]), mul(lam[1], v[1][c]));
+        acc = add(acc, mul(lam[2], v[2][c]));
+        if constexpr (D == 3) acc = add(acc, mul(lam[3], v[3][c]));
+        x[c] = acc;
+    }
+}
+
+// --------------------------------------------------------------- grid descriptor
+struct GridDev {
+    int n0, n1, n2;
+    double lo[3], hi[3];
+    const int64_t* __restrict__ cell_start;
+    const int32_t* __restrict__ cell_elems;
+    const double* __restrict__ rec;
+    const double* __restrict__ centroids;
+};
+
+inline GridDev to_dev(const tt_grid_t& g) {
+    GridDev d;
+    d.n0 = g.n[0]; d.n1 = g.n[1]; d.n2 = g.dim == 3 ? g.n[2] : 1;
+    for (int c = 0; c < 3; ++c) { d.lo[c] = g.lo[c]; d.hi[c] = g.hi[c]; }
+    d.cell_start = g.cell_start; d.cell_elems = g.cell_elems;
+    d.rec = g.rec; d.centroids = g.centroids;
+    return d;
+}
+
+template <int D>
+TT_D int64_t point_cell(const GridDev& g, const double* x) {
+    int ix = axis_cell(x[0], g.lo[0], g.hi[0], g.n0);
+    int iy = axis_cell(x[1], g.lo[1], g.hi[1], g.n1);
+    int64_t c = (int64_t)ix * g.n1 + iy;
+    if constexpr (D == 3) c = c * g.n2 + axis_cell(x[2], g.lo[2], g.hi[2], g.n2);
+    return c;
+}
+
+// First ascending candidate of the point's cell whose lambdas are all >= -eps
+// (_compiled.pyx:147-174).  Returns -1 (OUTSIDE) when none qualifies.
+template <int D>
+TT_D int locate_point(const GridDev& g, const double* x, double eps, double* lam) {
+    int64_t c = point_cell<D>(g, x);
+    int64_t j0 = __ldg(g.cell_start + c), j1 = __ldg(g.cell_start + c + 1);
+    for (int64_t j = j0; j < j1; ++j) {
+        int e = __ldg(g.cell_elems + j);
+        Rec<D> r;
+        load_rec<D>(g.rec, e, r);
+        double l[D + 1];
+        bary_from_rec<D>(r, x, l);
+        if (inside_eps<D>(l, eps)) {
+#pragma unroll
+            for (int i = 0; i <= D; ++i) lam[i] = l[i];
+            return e;
+        }
+    }
+    return -1;
+}
+
+// Expanding-ring nearest centroid, lowest id on ties, stop one ring after the first
+// non-empty ring (locate.py:97-127).  d2 = (dx*dx + dy*dy) [+ dz*dz].
+template <int D>
+TT_D int nearest_element(const GridDev& g, const double* x) {
+    int home[3];
+    const int n[3] = {g.n0, g.n1, g.n2};
+    for (int c = 0; c < D; ++c) {
+        double t = mul(div(sub(x[c], g.lo[c]), sub(g.hi[c], g.lo[c])), (double)n[c]);
+        // np.clip(t, 0, n-1) then int(): clip in double first (locate.py:102-103)
+        t = t < 0.0 ? 0.0 : t;
+        t = t > (double)(n[c] - 1) ? (double)(n[c] - 1) : t;
+        home[c] = (int)t;
+    }
+    if constexpr (D == 2) home[2] = 0;
+    int best = -1;
+    double best_d2 = __longlong_as_double(0x7ff0000000000000LL);  // +inf
+    int first = -1;
+    int max_ring = n[0] > n[1] ? n[0] : n[1];
+    if constexpr (D == 3) max_ring = max_ring > n[2] ? max_ring : n[2];
+    for (int ring = 0; ring <= max_ring; ++ring) {
+        if (first >= 0 && ring > first + 1) break;
+        const int rz = (D == 3) ? ring : 0;
+        for (int cx = home[0] - ring; cx <= home[0] + ring; ++cx) {
+            if (cx < 0 || cx >= n[0]) continue;
+            for (int cy = home[1] - ring; cy <= home[1] + ring; ++cy) {
+                if (cy < 0 || cy >= n[1]) continue;
+                for (int cz = home[2] - rz; cz <= home[2] + rz; ++cz) {
+                    if (cz < 0 || cz >= n[2]) continue;
+                    int dx = abs(cx - home[0]), dy = abs(cy - home[1]), dz = abs(cz - home[2]);
+                    int cheb = dx > dy ? dx : dy;
+                    cheb = cheb > dz ? cheb : dz;
+                    if (cheb != ring) continue;
+                    int64_t c = ((int64_t)cx * n[1] + cy) * n[2] + cz;
+                    int64_t j0 = g.cell_start[c], j1 = g.cell_start[c + 1];
+                    for (int64_t j = j0; j < j1; ++j) {
+                        int e = g.cell_elems[j];
+                        double d2 = 0.0;
+                        {
+                            double d0 = sub(g.centroids[(int64_t)e * D + 0], x[0]);
+                            double d1 = sub(g.centroids[(int64_t)e * D + 1], x[1]);
+                            d2 = add(mul(d0, d0), mul(d1, d1));
+                            if constexpr (D == 3) {
+                                double dd = sub(g.centroids[(int64_t)e * D + 2], x[2]);
+                                d2 = add(d2, mul(dd, dd));
+                            }
+                        }
+                        if (d2 < best_d2 || (d2 == best_d2 && e < best)) { best = e; best_d2 = d2; }
+                        if (first < 0) first = ring;
+                    }
+                }
+            }
+        }
+    }
+    return best;
+}
+
+// Snapped barycentrics: clip(lambda, 0) / sum (montecarlo.py:58-63)
+template <int D>
+TT_D void snap_lambda(const GridDev& g, int e, const double* x, double* lam) {
+    Rec<D> r;
+    load_rec<D>(g.rec, e, r);
+    bary_from_rec<D>(r, x, lam);
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i <= D; ++i) {
+        lam[i] = lam[i] < 0.0 ? 0.0 : lam[i];
+    }
+    s = add(lam[0], lam[1]);
+#pragma unroll
+    for (int i = 2; i <= D; ++i) s = add(s, lam[i]);
+#pragma unroll
+    for (int i = 0; i <= D; ++i) lam[i] = div(lam[i], s);
+}
+
+}  // namespace tt

@@ -1,0 +1,422 @@
+// P1 mass matrix (CSR, exactly symmetric) and single-launch Jacobi PCG (fem.py:78-152).
+//
+// Mass assembly is row-owned: row i is built from node i's incidence list (element
+// entries ascending), so every value is a fixed-order sum over ascending elements and
+// M[i][j] and M[j][i] are the same sum -- symmetric to the last bit like the reference's
+// mirrored upper triangle (fem.py:94-109), with no atomics and no global sort.
+//
+// PCG runs as ONE cooperative kernel (grid = co-resident blocks on all 148 SMs): the
+// CSR and the five vectors of a 1M-element mesh fit in the 126 MB L2, so an iteration
+// is three grid-wide barriers around L2-bandwidth vector work instead of ~6 kernel
+// launches and a host round-trip for the convergence test.  Dot products are
+// per-block partials reduced in a fixed order by every block, so all blocks see the
+// identical scalars (uniform control flow) and results are run-to-run deterministic.
+#include <cooperative_groups.h>
+#include <cub/cub.cuh>
+#include "tt_common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace tt {
+
+constexpr int kMaxRow = 256;  // max distinct columns per mass-matrix row
+
+// distinct neighbour nodes of row i (including i), ascending
+__device__ int row_columns(int i, int k, const int64_t* __restrict__ inc_start,
+                           const int32_t* __restrict__ inc, const int32_t* __restrict__ elems,
+                           int* cols) {
+    int n = 0;
+    for (int64_t q = inc_start[i]; q < inc_start[i + 1]; ++q) {
+        const int64_t e = inc[q] / k;
+        for (int a = 0; a < k; ++a) {
+            const int c = elems[e * k + a];
+            // insert into sorted unique list
+            int pos = n;
+            bool dup = false;
+            for (int t = 0; t < n; ++t) {
+                if (cols[t] == c) { dup = true; break; }
+                if (cols[t] > c) { pos = t; break; }
+            }
+            if (dup) continue;
+            if (n >= kMaxRow) return -1;
+            for (int t = n; t > pos; --t) cols[t] = cols[t - 1];
+            cols[pos] = c;
+            ++n;
+        }
+    }
+    return n;
+}
+
+__global__ void mass_count_kernel(int64_t n_nodes, int k, const int64_t* __restrict__ inc_start,
+                                  const int32_t* __restrict__ inc, const int32_t* __restrict__ elems,
+                                  unsigned long long* __restrict__ lens, int32_t* __restrict__ status) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n_nodes) return;
+    int cols[kMaxRow];
+    int n = row_columns((int)i, k, inc_start, inc, elems, cols);
+    if (n < 0) { atomicOr(status, TT_FLAG_CAPACITY); n = 0; }
+    lens[i] = (unsigned long long)n;
+}
+
+struct LocalMass {
+    double m[16];
+};
+
+__global__ void mass_fill_kernel(int64_t n_nodes, int k, const int64_t* __restrict__ inc_start,
+                                 const int32_t* __restrict__ inc, const int32_t* __restrict__ elems,
+                                 const double* __restrict__ measure, LocalMass local,
+                                 const int64_t* __restrict__ row_ptr, int32_t* __restrict__ cols_out,
+                                 double* __restrict__ vals_out) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n_nodes) return;
+    int cols[kMaxRow];
+    int n = row_columns((int)i, k, inc_start, inc, elems, cols);
+    if (n < 0) return;
+    const int64_t base = row_ptr[i];
+    for (int t = 0; t < n; ++t) {
+        const int c = cols[t];
+        double s = 0.0;
+        bool any = false;
+        for (int64_t q = inc_start[i]; q < inc_start[i + 1]; ++q) {
+            const int64_t ea = inc[q];
+            const int64_t e = ea / k;
+            const int ai = (int)(ea - e * k);
+            int ac = -1;
+            for (int a = 0; a < k; ++a)
+                if (elems[e * k + a] == c) ac = a;
+            if (ac < 0) continue;
+            const int lo = ai < ac ? ai : ac, hi = ai < ac ? ac : ai;
+            // area * local[lo][hi]: the upper-triangle entry (fem.py:93-100)
+            const double v = mul(measure[e], local.m[lo * k + hi]);
+            s = any ? add(s, v) : v;
+            any = true;
+        }
+        cols_out[base + t] = c;
+        vals_out[base + t] = s;
+    }
+}
+
+// ------------------------------------------------------------------------- PCG
+struct PcgArgs {
+    int64_t n;
+    const int64_t* __restrict__ rp;
+    const int32_t* __restrict__ ci;
+    const double* __restrict__ v;
+    const double* __restrict__ b;
+    double tol;
+    int64_t maxiter;
+    double* __restrict__ x;
+    double* __restrict__ best_x;
+    double* __restrict__ r;
+    double* __restrict__ z;
+    double* __restrict__ p;
+    double* __restrict__ ap;
+    double* __restrict__ dinv;
+    double* __restrict__ part;  // 3 * gridDim.x partial slots
+    tt_pcg_result_t* res;
+};
+
+constexpr int kPcgBlock = 512;
+constexpr int kRowG = 8;  // lanes per CSR row in the SpMV
+
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (w == 0) {
+        t = (l < (int)(blockDim.x >> 5)) ? sh[l] : 0.0;
+        for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+    }
+    return t;  // valid in warp 0
+}
+
+// every block reduces the same partials in the same order -> identical scalar everywhere
+__device__ __forceinline__ double grid_total(const double* part, double* sh) {
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double t = 0.0;
+        for (int i = threadIdx.x; i < (int)gridDim.x; i += 32) t += __ldcg(part + i);
+        for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+        if (threadIdx.x == 0) sh[32] = t;
+    }
+    __syncthreads();
+    return sh[32];
+}
+
+__global__ void __launch_bounds__(kPcgBlock) pcg_kernel(PcgArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double sh[33];
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+    const int nb = gridDim.x;
+    double* partA = a.part;
+    double* partB = a.part + nb;
+    double* partC = a.part + 2 * nb;
+    const int64_t n = a.n;
+
+    // init: dinv, x = 0, r = b, z = dinv r, p = z
+    double bb = 0.0, rz_p = 0.0;
+    for (int64_t i = tid; i < n; i += nthreads) {
+        double d = 0.0;
+        for (int64_t q = a.rp[i]; q < a.rp[i + 1]; ++q)
+            if (a.ci[q] == i) d = a.v[q];
+        const double di = 1.0 / d;
+        const double bi = a.b[i];
+        a.dinv[i] = di;
+        a.x[i] = 0.0;
+        a.best_x[i] = 0.0;
+        a.r[i] = bi;
+        const double zi = di * bi;
+        a.z[i] = zi;
+        a.p[i] = zi;
+        bb += bi * bi;
+        rz_p += bi * zi;
+    }
+    bb = block_sum(bb, sh);
+    if (threadIdx.x == 0) partB[blockIdx.x] = bb;
+    rz_p = block_sum(rz_p, sh);
+    if (threadIdx.x == 0) partC[blockIdx.x] = rz_p;
+    grid.sync();
+    const double bnorm = sqrt(grid_total(partB, sh));
+    double rz = grid_total(partC, sh);
+    if (bnorm == 0.0) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            a.res->iterations = 0; a.res->residual = 0.0; a.res->best_residual = 0.0;
+            a.res->converged = 1; a.res->zero_rhs = 1;
+        }
+        return;
+    }
+    double best = bnorm / bnorm;  // ||r0|| / ||b||  (fem.py:136)
+    constexpr int kRowsPerWarp = 32 / kRowG;
+    const int64_t warp_id = tid >> 5, nwarps = nthreads >> 5;
+    const int lane = threadIdx.x & 31;
+    const int sub = lane % kRowG;
+    double res = best;
+    for (int64_t it = 0; it < a.maxiter; ++it) {
+        // ---- phase 1: Ap = M p, partial p.Ap (kRowG lanes per row, warp-uniform loop)
+        double pap = 0.0;
+        for (int64_t w0 = warp_id * kRowsPerWarp; w0 < n; w0 += nwarps * kRowsPerWarp) {
+            const int64_t i = w0 + lane / kRowG;
+            double s = 0.0;
+            if (i < n) {
+                for (int64_t q = a.rp[i] + sub; q < a.rp[i + 1]; q += kRowG)
+                    s += a.v[q] * __ldcg(a.p + a.ci[q]);
+            }
+#pragma unroll
+            for (int off = kRowG / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+            if (i < n && sub == 0) {
+                a.ap[i] = s;
+                pap += __ldcg(a.p + i) * s;
+            }
+        }
+        pap = block_sum(pap, sh);
+        if (threadIdx.x == 0) partA[blockIdx.x] = pap;
+        grid.sync();
+        // ---- phase 2: alpha, x += alpha p, r -= alpha Ap, z = dinv r; partial rr, rz
+        const double alpha = rz / grid_total(partA, sh);
+        double rr = 0.0, rzn = 0.0;
+        for (int64_t i = tid; i < n; i += nthreads) {
+            const double pi = __ldcg(a.p + i);
+            const double xi = a.x[i] + alpha * pi;
+            const double ri = a.r[i] - alpha * __ldcg(a.ap + i);
+            const double zi = a.dinv[i] * ri;
+            a.x[i] = xi;
+            a.r[i] = ri;
+            a.z[i] = zi;
+            rr += ri * ri;
+            rzn += ri * zi;
+        }
+        rr = block_sum(rr, sh);
+        if (threadIdx.x == 0) partB[blockIdx.x] = rr;
+        rzn = block_sum(rzn, sh);
+        if (threadIdx.x == 0) partC[blockIdx.x] = rzn;
+        grid.sync();
+        // ---- phase 3: residual test, best iterate, p = z + beta p
+        res = sqrt(grid_total(partB, sh)) / bnorm;
+        const double rz_new = grid_total(partC, sh);
+        const bool improved = res < best;
+        if (improved) {
+            best = res;
+            for (int64_t i = tid; i < n; i += nthreads) a.best_x[i] = a.x[i];
+        }
+        if (res <= a.tol) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                a.res->iterations = it + 1; a.res->residual = res; a.res->best_residual = best;
+                a.res->converged = 1; a.res->zero_rhs = 0;
+            }
+            return;
+        }
+        const double beta = rz_new / rz;
+        for (int64_t i = tid; i < n; i += nthreads) a.p[i] = a.z[i] + beta * __ldcg(a.p + i);
+        rz = rz_new;
+        grid.sync();
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        a.res->iterations = a.maxiter; a.res->residual = res; a.res->best_residual = best;
+        a.res->converged = 0; a.res->zero_rhs = 0;
+    }
+}
+
+__global__ void spmv_kernel(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                            const double* __restrict__ v, const double* __restrict__ x,
+                            double* __restrict__ y) {
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t i = tid / kRowG;
+    const int sub = threadIdx.x % kRowG;
+    double s = 0.0;
+    if (i < n)
+        for (int64_t q = rp[i] + sub; q < rp[i + 1]; q += kRowG) s += v[q] * __ldg(x + ci[q]);
+#pragma unroll
+    for (int off = kRowG / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (i < n && sub == 0) y[i] = s;
+}
+
+// integral of a P1 field: sum_e |T| * (c . w), w = rule.points^T rule.weights (fem.py:155-161)
+__global__ void integrate_kernel(int64_t E, int k, const int32_t* __restrict__ elems,
+                                 const double* __restrict__ measure, const double* __restrict__ c,
+                                 LocalMass w, double* __restrict__ part) {
+    __shared__ double sh[33];
+    double s = 0.0;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        double t = 0.0;
+        for (int a = 0; a < k; ++a) t += c[elems[e * k + a]] * w.m[a];
+        s += measure[e] * t;
+    }
+    s = block_sum(s, sh);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+__global__ void sum_parts_kernel(int nparts, const double* __restrict__ part, double* __restrict__ out) {
+    if (threadIdx.x < 32) {
+        double t = 0.0;
+        for (int i = threadIdx.x; i < nparts; i += 32) t += part[i];
+        for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+        if (threadIdx.x == 0) *out = t;
+    }
+}
+
+static int pcg_grid_blocks(int64_t n) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg_kernel, kPcgBlock, 0);
+    if (per_sm < 1) per_sm = 1;
+    int64_t maxb = (int64_t)sm_count() * per_sm;
+    int64_t need = (n * kRowG + kPcgBlock - 1) / kPcgBlock;
+    if (need < 1) need = 1;
+    return (int)(need < maxb ? need : maxb);
+}
+
+}  // namespace tt
+
+using namespace tt;
+
+extern "C" int tt_mass_pattern(const tt_mesh_t* m, const int64_t* inc_start, const int32_t* inc,
+                               int64_t* row_ptr, int32_t* status, void* stream) {
+    if (!m || (m->dim != 2 && m->dim != 3)) {
+        set_error("tt_mass_pattern: bad mesh");
+        return TT_ERR_INVALID_PARAMETER;
+    }
+    auto s = as_stream(stream);
+    const int k = m->dim + 1;
+    unsigned long long* lens = nullptr;
+    int st = cuda_status(cudaMallocAsync((void**)&lens, sizeof(unsigned long long) * (m->n_nodes + 1), s),
+                         "mass lens alloc");
+    if (st) return st;
+    cudaMemsetAsync(row_ptr, 0, sizeof(int64_t), s);
+    if (m->n_nodes)
+        mass_count_kernel<<<grid_for(m->n_nodes, 128), 128, 0, s>>>(m->n_nodes, k, inc_start, inc,
+                                                                    m->elems, lens, status);
+    size_t tmp_bytes = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, lens,
+                                  reinterpret_cast<unsigned long long*>(row_ptr + 1), m->n_nodes, s);
+    void* tmp = nullptr;
+    st = cuda_status(cudaMallocAsync(&tmp, tmp_bytes, s), "scan tmp alloc");
+    if (!st) {
+        cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, lens,
+                                      reinterpret_cast<unsigned long long*>(row_ptr + 1), m->n_nodes, s);
+        st = launch_check("mass pattern");
+        cudaFreeAsync(tmp, s);
+    }
+    cudaFreeAsync(lens, s);
+    return st;
+}
+
+extern "C" int tt_mass_fill(const tt_mesh_t* m, const int64_t* inc_start, const int32_t* inc,
+                            const double* local_host, const int64_t* row_ptr, int32_t* cols,
+                            double* vals, void* stream) {
+    if (!m || (m->dim != 2 && m->dim != 3) || !m->measure || !local_host) {
+        set_error("tt_mass_fill: bad arguments");
+        return TT_ERR_INVALID_PARAMETER;
+    }
+    const int k = m->dim + 1;
+    LocalMass lm;
+    for (int i = 0; i < 16; ++i) lm.m[i] = i < k * k ? local_host[i] : 0.0;
+    if (m->n_nodes)
+        mass_fill_kernel<<<grid_for(m->n_nodes, 128), 128, 0, as_stream(stream)>>>(
+            m->n_nodes, k, inc_start, inc, m->elems, m->measure, lm, row_ptr, cols, vals);
+    return launch_check("mass_fill_kernel");
+}
+
+extern "C" int64_t tt_pcg_workspace_doubles(int64_t n) { return 6 * n + 3 * 148 * 32 + 64; }
+
+extern "C" int tt_pcg(int64_t n, const int64_t* rp, const int32_t* ci, const double* v,
+                      const double* b, double tol, int64_t maxiter, double* x, double* best_x,
+                      double* work, tt_pcg_result_t* result, void* stream) {
+    if (n < 1 || maxiter < 0) {
+        set_error("tt_pcg: bad size");
+        return TT_ERR_INVALID_PARAMETER;
+    }
+    PcgArgs a;
+    a.n = n; a.rp = rp; a.ci = ci; a.v = v; a.b = b; a.tol = tol; a.maxiter = maxiter;
+    a.x = x; a.best_x = best_x;
+    a.r = work; a.z = work + n; a.p = work + 2 * n; a.ap = work + 3 * n; a.dinv = work + 4 * n;
+    a.part = work + 5 * n;
+    a.res = result;
+    int blocks = pcg_grid_blocks(n);
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    void* args[] = {&a};
+    cudaError_t e = cudaLaunchCooperativeKernel((void*)pcg_kernel, dim3(blocks), dim3(kPcgBlock), args,
+                                                0, as_stream(stream));
+    return cuda_status(e, "pcg_kernel (cooperative launch)");
+}
+
+extern "C" int tt_spmv(int64_t n, const int64_t* rp, const int32_t* ci, const double* v,
+                       const double* x, double* y, void* stream) {
+    if (n == 0) return TT_OK;
+    spmv_kernel<<<grid_for(n * kRowG, 256), 256, 0, as_stream(stream)>>>(n, rp, ci, v, x, y);
+    return launch_check("spmv_kernel");
+}
+
+extern "C" int tt_integrate_p1(const tt_mesh_t* m, const double* coeffs, double* out, void* stream) {
+    if (!m || (m->dim != 2 && m->dim != 3) || !m->measure) {
+        set_error("tt_integrate_p1: bad mesh");
+        return TT_ERR_INVALID_PARAMETER;
+    }
+    const int k = m->dim + 1;
+    LocalMass w;
+    for (int i = 0; i < 16; ++i) w.m[i] = 0.0;
+    // w = rule.points^T @ rule.weights for the degree-2 rule (fem.py:158-160)
+    if (k == 3) {
+        const double P[3][3] = {{2.0 / 3, 1.0 / 6, 1.0 / 6}, {1.0 / 6, 2.0 / 3, 1.0 / 6}, {1.0 / 6, 1.0 / 6, 2.0 / 3}};
+        for (int a = 0; a < 3; ++a) {
+            double s = 0.0;
+            for (int q = 0; q < 3; ++q) s += P[q][a] * (1.0 / 3);
+            w.m[a] = s;
+        }
+    } else {
+        for (int a = 0; a < 4; ++a) w.m[a] = 0.25;
+    }
+    auto s = as_stream(stream);
+    const int nparts = sm_count() * 2;
+    double* part = nullptr;
+    int st = cuda_status(cudaMallocAsync((void**)&part, sizeof(double) * nparts, s), "integrate alloc");
+    if (st) return st;
+    integrate_kernel<<<nparts, 256, 0, s>>>(m->n_elems, k, m->elems, m->measure, coeffs, w, part);
+    sum_parts_kernel<<<1, 32, 0, s>>>(nparts, part, out);
+    st = launch_check("integrate kernels");
+    cudaFreeAsync(part, s);
+    return st;
+}

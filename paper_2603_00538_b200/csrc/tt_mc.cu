@@ -1,0 +1,568 @@
+// Fused Monte-Carlo load assembly (montecarlo.py:110-147) for P1 simplices, d = 2, 3.
+//
+// One kernel does plan -> point map -> black-box source query -> f*lambda accumulation:
+//   * a lane GROUP of G lanes (G in {8, 16, 32}) owns one target element; its lanes
+//     stride over the element's N samples, so the 32 lanes of a warp query points of
+//     one (or a few spatially adjacent) elements: the source-side candidate lists and
+//     locate records they touch are shared and come from L1 (broadcast loads);
+//   * per-lane k-vector accumulators in registers, then a G-lane xor-shuffle tree
+//     (warp-aggregated reduction) -> one write of contrib[e, 0..k) per element, or one
+//     atomicAdd per (element, vertex) into b when no contribution buffer is given;
+//   * nothing per-sample touches HBM: shared-plan lambdas are an L1-resident (N, k)
+//     table, Philox plans are generated in-register, and the source field is either an
+//     analytic postfix program (kernel parameter space) or a P1 nodal field located
+//     through the uniform grid in-register (locate + snap + gather).
+// The element contribution is (sum_j f_j lambda_j) / (N * (1/|T|)) -- the reference's
+// (f / (n p)) @ lam with the per-element constant factored out (montecarlo.py:128-131).
+#include <cub/cub.cuh>
+#include "tt_common.cuh"
+#include "tt_philox.cuh"
+
+namespace tt {
+
+struct SrcDev {
+    int kind;
+    int outside;
+    GridDev grid;
+    const int32_t* __restrict__ src_elems;
+    const double* __restrict__ coeffs;
+    const double* __restrict__ values;
+    const int32_t* __restrict__ cached;
+};
+
+template <int D>
+__device__ __forceinline__ double eval_expr(const tt_expr_t& p, const double* x) {
+    double st[TT_EXPR_MAX_STACK];
+    int sp = 0;
+    for (int i = 0; i < p.n_ops; ++i) {
+        const int op = p.ops[i];
+        switch (op) {
+            case TT_OP_CONST: st[sp++] = p.consts[i]; break;
+            case TT_OP_X: st[sp++] = x[0]; break;
+            case TT_OP_Y: st[sp++] = x[1]; break;
+            case TT_OP_Z: st[sp++] = (D == 3) ? x[D - 1] : 0.0; break;
+            case TT_OP_ADD: --sp; st[sp - 1] = st[sp - 1] + st[sp]; break;
+            case TT_OP_SUB: --sp; st[sp - 1] = st[sp - 1] - st[sp]; break;
+            case TT_OP_MUL: --sp; st[sp - 1] = st[sp - 1] * st[sp]; break;
+            case TT_OP_DIV: --sp; st[sp - 1] = st[sp - 1] / st[sp]; break;
+            case TT_OP_POW: --sp; st[sp - 1] = pow(st[sp - 1], st[sp]); break;
+            case TT_OP_SQUARE: st[sp - 1] = st[sp - 1] * st[sp - 1]; break;
+            case TT_OP_NEG: st[sp - 1] = -st[sp - 1]; break;
+            case TT_OP_SIN: st[sp - 1] = sin(st[sp - 1]); break;
+            case TT_OP_COS: st[sp - 1] = cos(st[sp - 1]); break;
+            case TT_OP_EXP: st[sp - 1] = exp(st[sp - 1]); break;
+            case TT_OP_SQRT: st[sp - 1] = sqrt(st[sp - 1]); break;
+            case TT_OP_LOG: st[sp - 1] = log(st[sp - 1]); break;
+            case TT_OP_TAN: st[sp - 1] = tan(st[sp - 1]); break;
+            case TT_OP_ABS: st[sp - 1] = fabs(st[sp - 1]); break;
+            default: break;
+        }
+    }
+    return sp > 0 ? st[0] : 0.0;
+}
+
+// MeshBackedField.__call__ (montecarlo.py:49-65) + eval_in_elements (fem.py:36-38)
+template <int D>
+__device__ __forceinline__ double eval_mesh(const SrcDev& s, const double* x, int& flags) {
+    constexpr int K = D + 1;
+    double l[K];
+    int e = locate_point<D>(s.grid, x, 1e-12, l);
+    if (e < 0) {
+        if (s.outside == TT_OUTSIDE_STRICT) {
+            flags |= TT_FLAG_OUTSIDE_STRICT;
+            return 0.0;
+        }
+        e = nearest_element<D>(s.grid, x);
+        snap_lambda<D>(s.grid, e, x, l);
+    }
+    const int32_t* conn = s.src_elems + (int64_t)e * K;
+    double f = mul(__ldg(s.coeffs + __ldg(conn)), l[0]);
+#pragma unroll
+    for (int i = 1; i < K; ++i) f = add(f, mul(__ldg(s.coeffs + __ldg(conn + i)), l[i]));
+    return f;
+}
+
+// cached source element: lambda_s for ALL samples clipped >= 0 and renormalised
+// (transfer.py:84-87), then the P1 gather
+template <int D>
+__device__ __forceinline__ double eval_cached(const SrcDev& s, const double* x, int e) {
+    constexpr int K = D + 1;
+    double l[K];
+    snap_lambda<D>(s.grid, e, x, l);
+    const int32_t* conn = s.src_elems + (int64_t)e * K;
+    double f = mul(__ldg(s.coeffs + __ldg(conn)), l[0]);
+#pragma unroll
+    for (int i = 1; i < K; ++i) f = add(f, mul(__ldg(s.coeffs + __ldg(conn + i)), l[i]));
+    return f;
+}
+
+template <int D, int SRC>
+__device__ __forceinline__ double eval_source(const SrcDev& s, const tt_expr_t& expr,
+                                              const double* x, int64_t vidx, int& flags) {
+    if constexpr (SRC == TT_SRC_EXPR) return eval_expr<D>(expr, x);
+    else if constexpr (SRC == TT_SRC_MESH) return eval_mesh<D>(s, x, flags);
+    else if constexpr (SRC == TT_SRC_CACHED) return eval_cached<D>(s, x, __ldg(s.cached + vidx));
+    else return __ldg(s.values + vidx);
+}
+
+template <int D>
+__device__ __forceinline__ void philox_lambda(uint64_t seed, int64_t e, int64_t j, double* lam) {
+    double xi[3];
+    philox_uniforms(seed, (uint64_t)e, (uint64_t)j, xi);
+    if constexpr (D == 2) {
+        double r = __dsqrt_rn(xi[0]);
+        lam[0] = sub(1.0, r);
+        lam[1] = mul(r, sub(1.0, xi[1]));
+        lam[2] = mul(r, xi[1]);
+    } else {
+        double r = cbrt(xi[0]);
+        double q = __dsqrt_rn(xi[1]);
+        double rq = mul(r, q);
+        lam[0] = sub(1.0, r);
+        lam[1] = mul(r, sub(1.0, q));
+        lam[2] = mul(rq, sub(1.0, xi[2]));
+        lam[3] = mul(rq, xi[2]);
+    }
+}
+
+struct TargetDev {
+    const double* __restrict__ nodes;
+    const int32_t* __restrict__ elems;
+    const double* __restrict__ measure;
+};
+
+struct PlanDev {
+    int64_t n;
+    const double* __restrict__ lam;
+    uint64_t seed;
+};
+
+template <int D>
+__device__ __forceinline__ void load_elem(const TargetDev& t, int64_t e, double (*v)[D]) {
+    constexpr int K = D + 1;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+        int64_t n = __ldg(t.elems + e * K + i);
+#pragma unroll
+        for (int c = 0; c < D; ++c) v[i][c] = __ldg(t.nodes + n * D + c);
+    }
+}
+
+template <int D, int PLAN, int SRC, int G>
+__global__ void __launch_bounds__(256) mc_load_kernel(TargetDev t, int64_t e_lo, int64_t e_hi,
+                                                      PlanDev plan, SrcDev src,
+                                                      const __grid_constant__ tt_expr_t expr,
+                                                      double* __restrict__ contrib,
+                                                      double* __restrict__ b,
+                                                      int32_t* __restrict__ status) {
+    constexpr int K = D + 1;
+    constexpr int EPW = 32 / G;  // elements per warp tile
+    const int lane = threadIdx.x & 31;
+    const int sub_lane = lane % G;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t n_el = e_hi - e_lo;
+    const int64_t N = plan.n;
+    int flags = 0;
+
+    for (int64_t tile = warp; tile * EPW < n_el; tile += nwarps) {
+        const int64_t le = tile * EPW + lane / G;  // local element index
+        const bool active = le < n_el;
+        const int64_t e = e_lo + le;
+        double acc[K];
+#pragma unroll
+        for (int i = 0; i < K; ++i) acc[i] = 0.0;
+        if (active) {
+            double v[K][D];
+            load_elem<D>(t, e, v);
+            for (int64_t j = sub_lane; j < N; j += G) {
+                double lam[K];
+                if constexpr (PLAN == TT_PLAN_SHARED) {
+#pragma unroll
+                    for (int i = 0; i < K; ++i) lam[i] = __ldg(plan.lam + j * K + i);
+                } else {
+                    philox_lambda<D>(plan.seed, e, j, lam);
+                }
+                double x[D];
+                map_point<D>(lam, v, x);
+                double f = eval_source<D, SRC>(src, expr, x, le * N + j, flags);
+                if (!isfinite(f)) flags |= TT_FLAG_NONFINITE;
+#pragma unroll
+                for (int i = 0; i < K; ++i) acc[i] = fma(f, lam[i], acc[i]);
+            }
+        }
+        // G-lane xor tree (groups are aligned power-of-two lane ranges)
+#pragma unroll
+        for (int off = G / 2; off > 0; off >>= 1)
+#pragma unroll
+            for (int i = 0; i < K; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], off);
+        if (active && sub_lane == 0) {
+            // (sum f lam) / (N p), p = 1/|T|  (montecarlo.py:128-131, :135-141)
+            const double q = (double)N * (1.0 / __ldg(t.measure + e));
+            if (contrib) {
+#pragma unroll
+                for (int i = 0; i < K; ++i) contrib[le * K + i] = acc[i] / q;
+            } else {
+#pragma unroll
+                for (int i = 0; i < K; ++i) atomicAdd(b + __ldg(t.elems + e * K + i), acc[i] / q);
+            }
+        }
+    }
+    if (flags) atomicOr(status, flags);
+}
+
+template <int D>
+__global__ void map_points_kernel(TargetDev t, int64_t e_lo, int64_t n_el, int plan_kind,
+                                  PlanDev plan, double* __restrict__ pts) {
+    constexpr int K = D + 1;
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n_el * plan.n) return;
+    int64_t le = i / plan.n, j = i % plan.n, e = e_lo + le;
+    double v[K][D];
+    load_elem<D>(t, e, v);
+    double lam[K];
+    if (plan_kind == TT_PLAN_SHARED) {
+        for (int c = 0; c < K; ++c) lam[c] = plan.lam[j * K + c];
+    } else {
+        philox_lambda<D>(plan.seed, e, j, lam);
+    }
+    double x[D];
+    map_point<D>(lam, v, x);
+    for (int c = 0; c < D; ++c) pts[i * D + c] = x[c];
+}
+
+template <int D, int SRC>
+__global__ void eval_points_kernel(SrcDev src, const __grid_constant__ tt_expr_t expr,
+                                   const double* __restrict__ pts, int64_t count,
+                                   double* __restrict__ out, int32_t* __restrict__ status) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int flags = 0;
+    if (i < count) {
+        double x[D];
+        for (int c = 0; c < D; ++c) x[c] = pts[i * D + c];
+        double f = eval_source<D, SRC>(src, expr, x, i, flags);
+        if (!isfinite(f)) flags |= TT_FLAG_NONFINITE;
+        out[i] = f;
+    }
+    if (flags) atomicOr(status, flags);
+}
+
+template <int D, int PLAN>
+__global__ void cache_ids_kernel(TargetDev t, int64_t e_lo, int64_t n_el, PlanDev plan, GridDev g,
+                                 int32_t* __restrict__ ids) {
+    constexpr int K = D + 1;
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n_el * plan.n) return;
+    const int64_t le = i / plan.n, j = i % plan.n, e = e_lo + le;
+    double v[K][D];
+    load_elem<D>(t, e, v);
+    double lam[K];
+    if constexpr (PLAN == TT_PLAN_SHARED) {
+#pragma unroll
+        for (int c = 0; c < K; ++c) lam[c] = __ldg(plan.lam + j * K + c);
+    } else {
+        philox_lambda<D>(plan.seed, e, j, lam);
+    }
+    double x[D], l[K];
+    map_point<D>(lam, v, x);
+    int es = locate_point<D>(g, x, 1e-12, l);
+    if (es < 0) es = nearest_element<D>(g, x);  // transfer.py:79-81
+    ids[i] = es;
+}
+
+// b[n] = sum over the node's incidences (e*k + a ascending) of contrib[e - e_lo, a],
+// starting from 0.0 -- exactly np.add.at's accumulation order (montecarlo.py:146).
+__global__ void reduce_nodes_kernel(int64_t n_nodes, int k, const int64_t* __restrict__ inc_start,
+                                    const int32_t* __restrict__ inc, int64_t e_lo, int64_t e_hi,
+                                    const double* __restrict__ contrib, double* __restrict__ b) {
+    int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (n >= n_nodes) return;
+    double s = 0.0;
+    for (int64_t q = inc_start[n]; q < inc_start[n + 1]; ++q) {
+        int64_t ea = inc[q];
+        int64_t e = ea / k;
+        if (e < e_lo || e >= e_hi) continue;
+        s = add(s, contrib[(e - e_lo) * k + (ea - e * k)]);
+    }
+    b[n] = s;
+}
+
+__global__ void incidence_count_kernel(int64_t nent, const int32_t* __restrict__ elems,
+                                       unsigned long long* __restrict__ counts) {
+    int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (q >= nent) return;
+    atomicAdd(counts + elems[q], 1ull);
+}
+
+__global__ void incidence_fill_kernel(int64_t nent, const int32_t* __restrict__ elems,
+                                      unsigned long long* __restrict__ cursor,
+                                      int32_t* __restrict__ inc) {
+    int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (q >= nent) return;
+    unsigned long long pos = atomicAdd(cursor + elems[q], 1ull);
+    inc[pos] = (int32_t)q;  // q = e*k + a
+}
+
+__global__ void segment_sort_kernel2(int64_t nseg, const int64_t* __restrict__ start,
+                                     int32_t* __restrict__ vals) {
+    int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (s >= nseg) return;
+    int64_t a = start[s], b = start[s + 1];
+    for (int64_t i = a + 1; i < b; ++i) {
+        int32_t v = vals[i];
+        int64_t j = i - 1;
+        while (j >= a && vals[j] > v) { vals[j + 1] = vals[j]; --j; }
+        vals[j + 1] = v;
+    }
+}
+
+static SrcDev to_src(const tt_source_t& s) {
+    SrcDev d;
+    d.kind = s.kind;
+    d.outside = s.outside;
+    d.grid = to_dev(s.grid);
+    d.src_elems = s.src_elems;
+    d.coeffs = s.coeffs;
+    d.values = s.values;
+    d.cached = s.cached_ids;
+    return d;
+}
+
+template <int D, int PLAN, int SRC, int G>
+static int launch_mc(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_plan_t* p,
+                     const tt_source_t* s, double* contrib, double* b, int32_t* status,
+                     cudaStream_t st) {
+    TargetDev td{t->nodes, t->elems, t->measure};
+    PlanDev pd{p->n_samples, p->lam, p->seed};
+    SrcDev sd = to_src(*s);
+    constexpr int EPW = 32 / G;
+    const int64_t tiles = (e_hi - e_lo + EPW - 1) / EPW;
+    const int block = 256;
+    int64_t blocks = (tiles + 7) / 8;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mc_load_kernel<D, PLAN, SRC, G>, block, 0);
+    if (per_sm < 1) per_sm = 1;
+    const int64_t cap = (int64_t)sm_count() * per_sm * 16;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    mc_load_kernel<D, PLAN, SRC, G><<<(unsigned)blocks, block, 0, st>>>(td, e_lo, e_hi, pd, sd,
+                                                                        s->expr, contrib, b, status);
+    return launch_check("mc_load_kernel");
+}
+
+template <int D, int PLAN, int SRC>
+static int dispatch_g(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_plan_t* p,
+                      const tt_source_t* s, double* contrib, double* b, int32_t* status,
+                      cudaStream_t st) {
+    const int64_t N = p->n_samples;
+    if (N <= 8) return launch_mc<D, PLAN, SRC, 8>(t, e_lo, e_hi, p, s, contrib, b, status, st);
+    if (N <= 16) return launch_mc<D, PLAN, SRC, 16>(t, e_lo, e_hi, p, s, contrib, b, status, st);
+    return launch_mc<D, PLAN, SRC, 32>(t, e_lo, e_hi, p, s, contrib, b, status, st);
+}
+
+template <int D, int PLAN>
+static int dispatch_src(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_plan_t* p,
+                        const tt_source_t* s, double* contrib, double* b, int32_t* status,
+                        cudaStream_t st) {
+    switch (s->kind) {
+        case TT_SRC_EXPR: return dispatch_g<D, PLAN, TT_SRC_EXPR>(t, e_lo, e_hi, p, s, contrib, b, status, st);
+        case TT_SRC_MESH: return dispatch_g<D, PLAN, TT_SRC_MESH>(t, e_lo, e_hi, p, s, contrib, b, status, st);
+        case TT_SRC_VALUES: return dispatch_g<D, PLAN, TT_SRC_VALUES>(t, e_lo, e_hi, p, s, contrib, b, status, st);
+        case TT_SRC_CACHED: return dispatch_g<D, PLAN, TT_SRC_CACHED>(t, e_lo, e_hi, p, s, contrib, b, status, st);
+    }
+    set_error("tt_mc_load: unknown source kind %d", s->kind);
+    return TT_ERR_INVALID_PARAMETER;
+}
+
+template <int D>
+static int dispatch_plan(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_plan_t* p,
+                         const tt_source_t* s, double* contrib, double* b, int32_t* status,
+                         cudaStream_t st) {
+    if (p->kind == TT_PLAN_SHARED) return dispatch_src<D, TT_PLAN_SHARED>(t, e_lo, e_hi, p, s, contrib, b, status, st);
+    if (p->kind == TT_PLAN_PHILOX) return dispatch_src<D, TT_PLAN_PHILOX>(t, e_lo, e_hi, p, s, contrib, b, status, st);
+    set_error("tt_mc_load: unknown plan kind %d", p->kind);
+    return TT_ERR_INVALID_PARAMETER;
+}
+
+static int check_source(const tt_source_t* s, int dim) {
+    if (!s) { set_error("null source"); return TT_ERR_INVALID_PARAMETER; }
+    if (s->dim != dim) {
+        set_error("source dimension %d does not match target dimension %d", s->dim, dim);
+        return TT_ERR_DIMENSION_MISMATCH;
+    }
+    if (s->kind == TT_SRC_EXPR) {
+        if (s->expr.n_ops < 1 || s->expr.n_ops > TT_EXPR_MAX_OPS) {
+            set_error("expression program length %d out of range", s->expr.n_ops);
+            return TT_ERR_INVALID_PARAMETER;
+        }
+    } else if (s->kind == TT_SRC_MESH) {
+        if (s->grid.dim != dim || !s->grid.cell_start || !s->grid.rec || !s->coeffs || !s->src_elems) {
+            set_error("mesh-backed source: incomplete descriptor or dimension mismatch");
+            return TT_ERR_DIMENSION_MISMATCH;
+        }
+    } else if (s->kind == TT_SRC_CACHED) {
+        if (s->grid.dim != dim || !s->grid.rec || !s->coeffs || !s->src_elems || !s->cached_ids) {
+            set_error("cached source: incomplete descriptor or dimension mismatch");
+            return TT_ERR_DIMENSION_MISMATCH;
+        }
+    } else if (s->kind == TT_SRC_VALUES) {
+        if (!s->values) { set_error("values source without values"); return TT_ERR_INVALID_PARAMETER; }
+    } else {
+        set_error("unknown source kind %d", s->kind);
+        return TT_ERR_INVALID_PARAMETER;
+    }
+    return TT_OK;
+}
+
+}  // namespace tt
+
+using namespace tt;
+
+extern "C" int tt_mc_load(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_plan_t* p,
+                          const tt_source_t* s, double* contrib, double* b, int32_t* status,
+                          void* stream) {
+    if (!t || !p || (t->dim != 2 && t->dim != 3) || p->dim != t->dim) {
+        set_error("tt_mc_load: target/plan dimension mismatch");
+        return TT_ERR_DIMENSION_MISMATCH;
+    }
+    if (e_lo < 0 || e_hi > t->n_elems || e_lo > e_hi || p->n_samples < 1) {
+        set_error("tt_mc_load: bad element range or sample count");
+        return TT_ERR_INVALID_PARAMETER;
+    }
+    if (p->kind == TT_PLAN_SHARED && !p->lam) {
+        set_error("tt_mc_load: shared plan without lambda table");
+        return TT_ERR_INVALID_PARAMETER;
+    }
+    if (!contrib && !b) {
+        set_error("tt_mc_load: need contrib or b output");
+        return TT_ERR_INVALID_PARAMETER;
+    }
+    int st = check_source(s, t->dim);
+    if (st) return st;
+    if (e_hi == e_lo) return TT_OK;
+    if (t->dim == 2) return dispatch_plan<2>(t, e_lo, e_hi, p, s, contrib, b, status, as_stream(stream));
+    return dispatch_plan<3>(t, e_lo, e_hi, p, s, contrib, b, status, as_stream(stream));
+}
+
+extern "C" int tt_mc_cache_ids(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_plan_t* p,
+                               const tt_grid_t* g, int32_t* ids, void* stream) {
+    if (!t || !p || !g || p->dim != t->dim || g->dim != t->dim || e_lo < 0 || e_hi > t->n_elems ||
+        e_lo > e_hi) {
+        set_error("tt_mc_cache_ids: bad arguments");
+        return TT_ERR_INVALID_PARAMETER;
+    }
+    const int64_t total = (e_hi - e_lo) * p->n_samples;
+    if (total == 0) return TT_OK;
+    TargetDev td{t->nodes, t->elems, t->measure};
+    PlanDev pd{p->n_samples, p->lam, p->seed};
+    GridDev gd = to_dev(*g);
+    auto s = as_stream(stream);
+    const unsigned nb = grid_for(total, 256);
+    if (t->dim == 2) {
+        if (p->kind == TT_PLAN_SHARED) cache_ids_kernel<2, TT_PLAN_SHARED><<<nb, 256, 0, s>>>(td, e_lo, e_hi - e_lo, pd, gd, ids);
+        else cache_ids_kernel<2, TT_PLAN_PHILOX><<<nb, 256, 0, s>>>(td, e_lo, e_hi - e_lo, pd, gd, ids);
+    } else {
+        if (p->kind == TT_PLAN_SHARED) cache_ids_kernel<3, TT_PLAN_SHARED><<<nb, 256, 0, s>>>(td, e_lo, e_hi - e_lo, pd, gd, ids);
+        else cache_ids_kernel<3, TT_PLAN_PHILOX><<<nb, 256, 0, s>>>(td, e_lo, e_hi - e_lo, pd, gd, ids);
+    }
+    return launch_check("cache_ids_kernel");
+}
+
+extern "C" int tt_map_points(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_plan_t* p,
+                             double* pts, void* stream) {
+    if (!t || !p || p->dim != t->dim || e_lo < 0 || e_hi > t->n_elems || e_lo > e_hi) {
+        set_error("tt_map_points: bad arguments");
+        return TT_ERR_INVALID_PARAMETER;
+    }
+    int64_t total = (e_hi - e_lo) * p->n_samples;
+    if (total == 0) return TT_OK;
+    TargetDev td{t->nodes, t->elems, t->measure};
+    PlanDev pd{p->n_samples, p->lam, p->seed};
+    auto s = as_stream(stream);
+    if (t->dim == 2)
+        map_points_kernel<2><<<grid_for(total, 256), 256, 0, s>>>(td, e_lo, e_hi - e_lo, p->kind, pd, pts);
+    else
+        map_points_kernel<3><<<grid_for(total, 256), 256, 0, s>>>(td, e_lo, e_hi - e_lo, p->kind, pd, pts);
+    return launch_check("map_points_kernel");
+}
+
+extern "C" int tt_eval_points(const tt_source_t* src, const double* pts, int64_t count,
+                              double* out, int32_t* status, void* stream) {
+    if (!src) { set_error("null source"); return TT_ERR_INVALID_PARAMETER; }
+    const int dim = src->dim;
+    if (dim != 2 && dim != 3) { set_error("tt_eval_points: source dim must be 2 or 3"); return TT_ERR_INVALID_PARAMETER; }
+    int st = check_source(src, dim);
+    if (st) return st;
+    if (count == 0) return TT_OK;
+    SrcDev sd = to_src(*src);
+    auto s = as_stream(stream);
+    const unsigned g = grid_for(count, 256);
+    if (dim == 2) {
+        if (src->kind == TT_SRC_EXPR) eval_points_kernel<2, TT_SRC_EXPR><<<g, 256, 0, s>>>(sd, src->expr, pts, count, out, status);
+        else if (src->kind == TT_SRC_MESH) eval_points_kernel<2, TT_SRC_MESH><<<g, 256, 0, s>>>(sd, src->expr, pts, count, out, status);
+        else eval_points_kernel<2, TT_SRC_VALUES><<<g, 256, 0, s>>>(sd, src->expr, pts, count, out, status);
+    } else {
+        if (src->kind == TT_SRC_EXPR) eval_points_kernel<3, TT_SRC_EXPR><<<g, 256, 0, s>>>(sd, src->expr, pts, count, out, status);
+        else if (src->kind == TT_SRC_MESH) eval_points_kernel<3, TT_SRC_MESH><<<g, 256, 0, s>>>(sd, src->expr, pts, count, out, status);
+        else eval_points_kernel<3, TT_SRC_VALUES><<<g, 256, 0, s>>>(sd, src->expr, pts, count, out, status);
+    }
+    return launch_check("eval_points_kernel");
+}
+
+extern "C" int tt_incidence_count(const tt_mesh_t* m, int64_t* inc_start, void* stream) {
+    if (!m || (m->dim != 2 && m->dim != 3)) {
+        set_error("tt_incidence_count: bad mesh");
+        return TT_ERR_INVALID_PARAMETER;
+    }
+    auto s = as_stream(stream);
+    const int64_t nent = m->n_elems * (m->dim + 1);
+    unsigned long long* counts = nullptr;
+    int st = cuda_status(cudaMallocAsync((void**)&counts, sizeof(unsigned long long) * (m->n_nodes + 1), s),
+                         "incidence counts alloc");
+    if (st) return st;
+    cudaMemsetAsync(counts, 0, sizeof(unsigned long long) * (m->n_nodes + 1), s);
+    cudaMemsetAsync(inc_start, 0, sizeof(int64_t), s);
+    if (nent) incidence_count_kernel<<<grid_for(nent, 256), 256, 0, s>>>(nent, m->elems, counts);
+    size_t tmp_bytes = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, counts,
+                                  reinterpret_cast<unsigned long long*>(inc_start + 1), m->n_nodes, s);
+    void* tmp = nullptr;
+    st = cuda_status(cudaMallocAsync(&tmp, tmp_bytes, s), "scan tmp alloc");
+    if (!st) {
+        cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, counts,
+                                      reinterpret_cast<unsigned long long*>(inc_start + 1), m->n_nodes, s);
+        st = launch_check("incidence count/scan");
+        cudaFreeAsync(tmp, s);
+    }
+    cudaFreeAsync(counts, s);
+    return st;
+}
+
+extern "C" int tt_incidence_fill(const tt_mesh_t* m, const int64_t* inc_start, int32_t* inc,
+                                 int64_t* cursor, void* stream) {
+    if (!m || (m->dim != 2 && m->dim != 3)) {
+        set_error("tt_incidence_fill: bad mesh");
+        return TT_ERR_INVALID_PARAMETER;
+    }
+    const int64_t nent = m->n_elems * (m->dim + 1);
+    if (nent >= 0x7fffffffLL) {
+        set_error("tt_incidence_fill: e*k index exceeds int32");
+        return TT_ERR_CAPACITY;
+    }
+    auto s = as_stream(stream);
+    cudaMemcpyAsync(cursor, inc_start, sizeof(int64_t) * m->n_nodes, cudaMemcpyDeviceToDevice, s);
+    if (nent)
+        incidence_fill_kernel<<<grid_for(nent, 256), 256, 0, s>>>(
+            nent, m->elems, reinterpret_cast<unsigned long long*>(cursor), inc);
+    segment_sort_kernel2<<<grid_for(m->n_nodes, 256), 256, 0, s>>>(m->n_nodes, inc_start, inc);
+    return launch_check("incidence fill/sort");
+}
+
+extern "C" int tt_reduce_nodes(int64_t n_nodes, int k, const int64_t* inc_start, const int32_t* inc,
+                               int64_t e_lo, int64_t e_hi, const double* contrib, double* b,
+                               void* stream) {
+    if (n_nodes == 0) return TT_OK;
+    reduce_nodes_kernel<<<grid_for(n_nodes, 256), 256, 0, as_stream(stream)>>>(
+        n_nodes, k, inc_start, inc, e_lo, e_hi, contrib, b);
+    return launch_check("reduce_nodes_kernel");
+}

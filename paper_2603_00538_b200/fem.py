@@ -1,0 +1,236 @@
+"""P1 finite elements on the GPU: nodal fields, mass matrix, Jacobi PCG
+(reference: fem.py:1-173).
+
+``assemble_mass_matrix`` builds an exactly symmetric CSR on the device
+(``tt_mass_pattern`` / ``tt_mass_fill``, row-owned, fixed-order sums); ``cg_solve``
+is one cooperative CUDA launch running the reference's Jacobi-preconditioned CG
+recurrence with best-iterate tracking (``tt_pcg``).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from functools import cached_property
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import DimensionMismatch, MeshMismatch, NoConvergence, TransferError
+from .quadrature import QuadratureRule, local_mass, simplex_rule
+
+
+class NodalField:
+    """Scalar P1 field: one coefficient per mesh node (fem.py:15-38).
+
+    Coefficients live on the device (``coeffs_dev``); ``coeffs`` is the host view,
+    copied on first access.
+    """
+
+    def __init__(self, mesh, coeffs):
+        self.mesh = mesh
+        if isinstance(coeffs, torch.Tensor):
+            t = coeffs.to(device=_lib.device(), dtype=torch.float64).reshape(-1).contiguous()
+            self._host = None
+        else:
+            arr = np.asarray(coeffs, dtype=np.float64)
+            if arr.shape != (mesh.n_nodes,):
+                raise DimensionMismatch(
+                    f"{arr.shape[0] if arr.ndim else 0} coefficients for {mesh.n_nodes} nodes")
+            if not np.all(np.isfinite(arr)):
+                raise DimensionMismatch("non-finite field coefficient")
+            t = torch.from_numpy(np.ascontiguousarray(arr)).to(_lib.device())
+            self._host = arr
+        if t.shape != (mesh.n_nodes,):
+            raise DimensionMismatch(f"{t.shape[0]} coefficients for {mesh.n_nodes} nodes")
+        self.coeffs_dev = t
+
+    @property
+    def coeffs(self) -> np.ndarray:
+        if self._host is None:
+            self._host = self.coeffs_dev.cpu().numpy()
+        return self._host
+
+    @classmethod
+    def from_function(cls, mesh, fn) -> "NodalField":
+        """Nodal interpolant of ``fn(x, y[, z])`` (fem.py:30-34)."""
+        cols = [mesh.nodes[:, c] for c in range(mesh.DIM)]
+        return cls(mesh, np.asarray(fn(*cols), dtype=np.float64))
+
+    def eval_in_elements(self, elems, lam):
+        """Field values at barycentric points ``lam`` (K, k) of elements ``elems``."""
+        dev = self.coeffs_dev.device
+        e = torch.as_tensor(np.asarray(elems), device=dev, dtype=torch.int64)
+        l_ = torch.as_tensor(np.asarray(lam, dtype=np.float64), device=dev)
+        c = self.coeffs_dev[self.mesh.device.elems[e].long()]
+        out = c[:, 0] * l_[:, 0]
+        for i in range(1, c.shape[1]):
+            out = out + c[:, i] * l_[:, i]
+        return out.cpu().numpy()
+
+
+def eval_basis(lam) -> np.ndarray:
+    """P1 basis values at barycentric coordinates (identity for linears)."""
+    return np.asarray(lam, dtype=np.float64)
+
+
+class SparseSymMatrix:
+    """Symmetric positive-definite CSR matrix resident on the device (fem.py:46-75)."""
+
+    def __init__(self, n: int, row_ptr: torch.Tensor, cols: torch.Tensor, vals: torch.Tensor):
+        self.n = n
+        self.row_ptr_dev = row_ptr
+        self.cols_dev = cols
+        self.vals_dev = vals
+        self._ws = None
+
+    @property
+    def shape(self):
+        return (self.n, self.n)
+
+    @property
+    def nnz(self) -> int:
+        return int(self.vals_dev.numel())
+
+    @cached_property
+    def csr(self):
+        import scipy.sparse as sp
+        return sp.csr_matrix((self.vals_dev.cpu().numpy(), self.cols_dev.cpu().numpy(),
+                              self.row_ptr_dev.cpu().numpy()), shape=self.shape)
+
+    @property
+    def row_offsets(self) -> np.ndarray:
+        return self.row_ptr_dev.cpu().numpy()
+
+    @property
+    def col_indices(self) -> np.ndarray:
+        return self.cols_dev.cpu().numpy()
+
+    @property
+    def values(self) -> np.ndarray:
+        return self.vals_dev.cpu().numpy()
+
+    @property
+    def diagonal(self) -> np.ndarray:
+        return self.csr.diagonal()
+
+    def matvec(self, x):
+        was_np = not isinstance(x, torch.Tensor)
+        xd = torch.as_tensor(np.asarray(x, dtype=np.float64) if was_np else x,
+                             device=self.vals_dev.device, dtype=torch.float64).contiguous()
+        if xd.shape != (self.n,):
+            raise DimensionMismatch(f"vector of length {xd.shape} for {self.n}x{self.n} matrix")
+        y = torch.empty(self.n, dtype=torch.float64, device=xd.device)
+        _lib.call("tt_spmv", self.n, _lib.ptr(self.row_ptr_dev), _lib.ptr(self.cols_dev),
+                  _lib.ptr(self.vals_dev), _lib.ptr(xd), _lib.ptr(y), _lib.stream_handle())
+        return y.cpu().numpy() if was_np else y
+
+    __matmul__ = matvec
+
+    def workspace(self):
+        if self._ws is None:
+            nd = int(_lib.lib().tt_pcg_workspace_doubles(self.n))
+            dev = self.vals_dev.device
+            self._ws = (torch.empty(nd, dtype=torch.float64, device=dev),
+                        torch.zeros(4, dtype=torch.float64, device=dev))  # tt_pcg_result_t
+        return self._ws
+
+
+def assemble_mass_matrix(mesh, rule: QuadratureRule | None = None) -> SparseSymMatrix:
+    """P1 mass matrix, exact for the default degree-2 rule (fem.py:78-110); off-diagonal
+    entries are the same fixed-order sums for (i, j) and (j, i): symmetric to the bit."""
+    if rule is None:
+        rule = simplex_rule(mesh.DIM, 2)
+    k = mesh.DIM + 1
+    local = np.ascontiguousarray(local_mass(rule), dtype=np.float64)
+    if local.shape != (k, k):
+        raise DimensionMismatch(f"rule with {local.shape[0]} barycentrics on a {k}-vertex mesh")
+    dm = mesh.device
+    inc_start, inc = dm.incidence
+    dev = dm.nodes.device
+    row_ptr = torch.empty(mesh.n_nodes + 1, dtype=torch.int64, device=dev)
+    status = _lib.status_word()
+    desc = dm.desc()
+    s = _lib.stream_handle()
+    _lib.call("tt_mass_pattern", C.byref(desc), _lib.ptr(inc_start), _lib.ptr(inc),
+              _lib.ptr(row_ptr), _lib.ptr(status), s)
+    if int(status.item()) & _lib.TT_FLAG_CAPACITY:
+        raise TransferError("mass matrix row exceeds the 256-column device capacity")
+    nnz = int(row_ptr[-1].item())
+    cols = torch.empty(nnz, dtype=torch.int32, device=dev)
+    vals = torch.empty(nnz, dtype=torch.float64, device=dev)
+    lh = (C.c_double * (k * k))(*local.ravel().tolist())
+    _lib.call("tt_mass_fill", C.byref(desc), _lib.ptr(inc_start), _lib.ptr(inc), lh,
+              _lib.ptr(row_ptr), _lib.ptr(cols), _lib.ptr(vals), s)
+    return SparseSymMatrix(mesh.n_nodes, row_ptr, cols, vals)
+
+
+class PcgResult:
+    __slots__ = ("iterations", "residual", "best_residual", "converged", "zero_rhs")
+
+
+def pcg_device(M: SparseSymMatrix, b: torch.Tensor, tol: float = 1e-12,
+               maxiter: int | None = None, x: torch.Tensor | None = None,
+               best_x: torch.Tensor | None = None):
+    """Launch the single-kernel PCG; returns (x, best_x, result tensor) without syncing."""
+    n = M.n
+    maxiter = 10 * n if maxiter is None else int(maxiter)
+    work, res = M.workspace()
+    x = x if x is not None else torch.empty(n, dtype=torch.float64, device=b.device)
+    best_x = best_x if best_x is not None else torch.empty(n, dtype=torch.float64, device=b.device)
+    _lib.call("tt_pcg", n, _lib.ptr(M.row_ptr_dev), _lib.ptr(M.cols_dev), _lib.ptr(M.vals_dev),
+              _lib.ptr(b), float(tol), maxiter, _lib.ptr(x), _lib.ptr(best_x), _lib.ptr(work),
+              _lib.ptr(res), _lib.stream_handle())
+    return x, best_x, res
+
+
+def decode_result(res: torch.Tensor) -> PcgResult:
+    raw = res.cpu().numpy().tobytes()
+    r = _lib.tt_pcg_result_t.from_buffer_copy(raw[:C.sizeof(_lib.tt_pcg_result_t)])
+    out = PcgResult()
+    for f in PcgResult.__slots__:
+        setattr(out, f, getattr(r, f))
+    return out
+
+
+def cg_solve(M: SparseSymMatrix, b, tol: float = 1e-12, maxiter: int | None = None):
+    """Jacobi-preconditioned CG for ``M x = b`` (fem.py:113-152): stops when the
+    recurrence residual ||r||/||b|| <= tol; raises ``NoConvergence`` carrying the best
+    iterate after ``maxiter`` (default 10 n) iterations; b = 0 returns zeros."""
+    was_np = not isinstance(b, torch.Tensor)
+    bd = torch.as_tensor(np.asarray(b, dtype=np.float64) if was_np else b,
+                         device=M.vals_dev.device, dtype=torch.float64).contiguous()
+    if bd.shape != (M.n,):
+        raise DimensionMismatch(f"rhs length {tuple(bd.shape)} for {M.n}x{M.n} matrix")
+    x, best_x, res = pcg_device(M, bd, tol, maxiter)
+    r = decode_result(res)
+    if r.zero_rhs:
+        x = torch.zeros_like(bd)
+    if not r.converged:
+        bx = best_x.cpu().numpy() if was_np else best_x
+        raise NoConvergence(bx, float(r.best_residual), int(r.iterations))
+    return x.cpu().numpy() if was_np else x
+
+
+def integrate_field(field: NodalField, rule: QuadratureRule | None = None) -> float:
+    """Integral of a P1 field over the mesh (fem.py:155-161), device reduction."""
+    dm = field.mesh.device
+    out = torch.empty(1, dtype=torch.float64, device=dm.nodes.device)
+    desc = dm.desc()
+    _lib.call("tt_integrate_p1", C.byref(desc), _lib.ptr(field.coeffs_dev), _lib.ptr(out),
+              _lib.stream_handle())
+    return float(out.item())
+
+
+def basis_integrals(mesh, device: bool = False):
+    """Integrals of the basis functions = mass-matrix row sums (fem.py:164-168)."""
+    dm = mesh.device
+    k = mesh.DIM + 1
+    contrib = (dm.measure / k).unsqueeze(1).expand(-1, k).contiguous()
+    b = dm.reduce_nodes(contrib)
+    return b if device else b.cpu().numpy()
+
+
+def check_same_mesh(a: NodalField, b: NodalField) -> None:
+    if a.mesh is not b.mesh:
+        raise MeshMismatch("fields live on different meshes")

@@ -1,0 +1,90 @@
+"""Monte-Carlo transfer pipelines and the cached-localisation operator
+(reference: transfer.py:46-163, MC parts).
+
+``transfer_mc`` = fused load (``tt_mc_load``) -> ordered node reduction -> mass
+matrix (cached on the immutable target mesh) -> single-launch PCG.
+``MCTransferOperator`` splits the work like a coupling loop: the source element of
+every sample is located once at construction (``tt_mc_cache_ids``: locate + snap,
+4 bytes per sample); ``apply`` re-evaluates the nodal source field at the cached
+elements with clipped/renormalised barycentrics -- the reference's sparse load
+matrix R applied to the coefficients (transfer.py:84-115) without materialising R.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _lib
+from .errors import DimensionMismatch
+from .fem import NodalField, cg_solve
+from .locate import UniformGridLocator
+from .montecarlo import SamplePlan, _raise_status, load_vector
+
+
+def transfer_mc(target, source, plan: SamplePlan, cg_tol: float = 1e-12, workers: int = 1,
+                *, deterministic: bool = True) -> NodalField:
+    """One-shot stochastic transfer from a black-box pointwise source (transfer.py:158-163)."""
+    b = load_vector(target, source, plan, deterministic=deterministic)
+    mass = target.device.mass
+    return NodalField(target, cg_solve(mass, b, tol=cg_tol))
+
+
+class MCTransferOperator:
+    """Monte-Carlo Galerkin projection with localisation done once (transfer.py:46-129)."""
+
+    def __init__(self, target, source_mesh, plan: SamplePlan, cg_tol: float = 1e-12,
+                 source_locator: UniformGridLocator | None = None):
+        if target.DIM != source_mesh.DIM or plan.dim != target.DIM:
+            raise DimensionMismatch("target, source mesh and plan dimensions differ")
+        self.target = target
+        self.source_mesh = source_mesh
+        self.plan = plan
+        self.cg_tol = cg_tol
+        self.mass = target.device.mass
+        self.locator = source_locator or UniformGridLocator.build(source_mesh)
+        dm = target.device
+        self.src_elem_dev = torch.empty((target.n_elems, plan.n_samples), dtype=torch.int32,
+                                        device=dm.nodes.device)
+        mdesc, pdesc, gdesc = dm.desc(), plan.desc(), self.locator.desc()
+        _lib.call("tt_mc_cache_ids", C.byref(mdesc), 0, target.n_elems, C.byref(pdesc),
+                  C.byref(gdesc), _lib.ptr(self.src_elem_dev), _lib.stream_handle())
+
+    @property
+    def _src_elem(self):
+        return self.src_elem_dev.cpu().numpy()
+
+    def load(self, source_field: NodalField, check: bool = True) -> torch.Tensor:
+        """b = R c on the device (cached source elements, no relocalisation)."""
+        if source_field.mesh is not self.source_mesh and \
+                source_field.mesh.n_nodes != self.source_mesh.n_nodes:
+            raise DimensionMismatch("field is not on the operator's source mesh")
+        dm = self.target.device
+        k = self.target.DIM + 1
+        s = _lib.tt_source_t()
+        s.kind = _lib.TT_SRC_CACHED
+        s.dim = self.target.DIM
+        s.grid = self.locator.desc()
+        s.src_elems = _lib.ptr(self.source_mesh.device.elems).value
+        s.coeffs = _lib.ptr(source_field.coeffs_dev).value
+        s.cached_ids = _lib.ptr(self.src_elem_dev).value
+        contrib = torch.empty((self.target.n_elems, k), dtype=torch.float64, device=dm.nodes.device)
+        status = _lib.status_word()
+        mdesc, pdesc = dm.desc(), self.plan.desc()
+        _lib.call("tt_mc_load", C.byref(mdesc), 0, self.target.n_elems, C.byref(pdesc), C.byref(s),
+                  _lib.ptr(contrib), None, _lib.ptr(status), _lib.stream_handle())
+        b = dm.reduce_nodes(contrib)
+        if check:
+            _raise_status(int(status.item()))
+        return b
+
+    def apply(self, source_field: NodalField) -> NodalField:
+        """Transfer a nodal field on the source mesh (precomputed localisation)."""
+        b = self.load(source_field)
+        return NodalField(self.target, cg_solve(self.mass, b, tol=self.cg_tol))
+
+    def apply_sampled(self, source) -> NodalField:
+        """Transfer from a pointwise black box, re-querying every sample."""
+        b = load_vector(self.target, source, self.plan)
+        return NodalField(self.target, cg_solve(self.mass, b, tol=self.cg_tol))

@@ -1,0 +1,377 @@
+"""GPU parity: the CUDA path (libtt_b200.so through the C ABI) against the reference's
+golden fixtures (tests/golden/ref_2d.npz) and the oracle restatement.
+
+Bars: integer ids / CSR arrays / plans bit-exact; load vectors
+normwise ||db||_inf / ||b||_inf <= 1e-12; solutions x <= 1e-12 with cg_tol 1e-14 on
+both sides; conservation compared in absolute terms.
+"""
+
+import numpy as np
+import pytest
+
+import tt_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+REL_B = 1e-12
+
+
+def _rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+
+
+@pytest.fixture(scope="module")
+def tt():
+    import paper_2603_00538_b200 as tt
+    return tt
+
+
+@pytest.fixture(scope="module")
+def c1(tt, golden):
+    tgt = tt.TriMesh.from_arrays(golden["c1t_nodes"], golden["c1t_elements"])
+    src = tt.TriMesh.from_arrays(golden["c1s_nodes"], golden["c1s_elements"])
+    return tgt, src
+
+
+# ------------------------------------------------------------------- plans
+def test_sobol_plans_bit_exact(tt, golden):
+    from paper_2603_00538_b200.sobol import sobol_2d, sobol
+    assert np.array_equal(sobol_2d(300), golden["sobol_300"])
+    assert np.array_equal(sobol_2d(100, skip=200), golden["sobol_100_skip200"])
+    p = tt.SamplePlan.build(1600, "sobol", 0)
+    assert np.array_equal(p.parametric, golden["plan_sobol1600_param"])
+    assert np.array_equal(p.barycentric, golden["plan_sobol1600_bary"])
+    assert np.array_equal(tt.SamplePlan.build(400, "sobol", 2).parametric, golden["plan_sobol400s2_param"])
+    assert np.array_equal(sobol(4096, 3), O.sobol(4096, 3))
+
+
+def test_uniform_plan_pcg64_bit_exact(tt, golden):
+    p = tt.SamplePlan.build(64, "uniform", 3)
+    assert np.array_equal(p.parametric, golden["plan_unif64s3_param"])
+    assert np.array_equal(p.barycentric, golden["plan_unif64s3_bary"])
+    for seed in (0, 7, 2**40 + 3):
+        q = tt.SamplePlan.build(1000, "uniform", seed, dim=3)
+        assert np.array_equal(q.parametric, np.random.default_rng(seed).random((1000, 3)))
+
+
+def test_philox_param_matches_oracle(tt):
+    import torch
+    from paper_2603_00538_b200 import _lib
+    par = torch.empty((7, 33, 3), dtype=torch.float64, device="cuda")
+    _lib.call("tt_plan_philox", 3, 5, 12, 33, 0xDEADBEEF12345, _lib.ptr(par), _lib.stream_handle())
+    assert np.array_equal(par.cpu().numpy(), O.philox_param(np.arange(5, 12), 33, 3, 0xDEADBEEF12345))
+
+
+def test_bary_map_3d_close_to_oracle(tt):
+    par = O.sobol(2048, 3)
+    got = tt.SamplePlan(2048, "sobol", 0, par).barycentric
+    np.testing.assert_allclose(got, O.bary_map(par), rtol=0, atol=2e-16)
+
+
+# ----------------------------------------------------------------- geometry / grid
+def test_mesh_generators_match_reference(tt, golden):
+    t = tt.generate_square_mesh(25, 0.2, seed=20, diagonal="right")
+    s = tt.generate_square_mesh(40, 0.2, seed=10, diagonal="left")
+    a = tt.generate_square_mesh(6, 0.3, seed=4, diagonal="alternating")
+    for m, tag in ((t, "c1t"), (s, "c1s"), (a, "alt")):
+        assert np.array_equal(m.nodes, golden[f"{tag}_nodes"])
+        assert np.array_equal(m.elements, golden[f"{tag}_elements"])
+        assert np.array_equal(m.elem_areas, golden[f"{tag}_areas"])
+        assert np.array_equal(m.device.measure.cpu().numpy(), golden[f"{tag}_areas"])
+
+
+def test_geometry_records_bit_exact(tt, golden, c1):
+    _, src = c1
+    binv, origin = src._bary_inv
+    assert np.array_equal(binv, golden["c1s_binv"]) and np.array_equal(origin, golden["c1s_origin"])
+    assert np.array_equal(src.device.centroids.cpu().numpy(), golden["c1s_centroids"])
+
+
+def test_grid_build_bit_exact(tt, golden, c1):
+    _, src = c1
+    loc = tt.UniformGridLocator.build(src)
+    assert (loc.nx, loc.ny) == (56, 56)
+    assert np.array_equal(loc.cell_start, golden["c1s_cell_start"])
+    assert np.array_equal(loc.cell_elems, golden["c1s_cell_elems"])
+
+
+def test_grid_build_3d_matches_oracle(tt):
+    m = tt.generate_cube_mesh(9, 0.2, seed=10, split="kuhn_mirror")
+    loc = tt.UniformGridLocator.build(m)
+    g = O.Grid(m.nodes, m.elements)
+    assert loc.dims == g.dims
+    assert np.array_equal(loc.cell_start, g.cell_start)
+    assert np.array_equal(loc.cell_elems, g.cell_elems)
+
+
+# ----------------------------------------------------------------- localisation
+def test_locate_bit_exact(tt, golden, c1):
+    _, src = c1
+    loc = tt.UniformGridLocator.build(src)
+    e, lam = loc.locate_many(golden["loc_pts"])
+    assert np.array_equal(e, golden["loc_elem"])
+    assert np.array_equal(lam, golden["loc_lam"])
+    e2, l2 = loc.locate_many(np.concatenate([src.nodes, 0.5 * (src.elem_coords[:, 0] + src.elem_coords[:, 1])]))
+    assert np.array_equal(e2, golden["vm_elem"]) and np.array_equal(l2, golden["vm_lam"])
+
+
+def test_locate_sample_points_bit_exact(tt, golden, c1):
+    tgt, src = c1
+    loc = tt.UniformGridLocator.build(src)
+    from paper_2603_00538_b200.montecarlo import map_points
+    plan = tt.SamplePlan(1600, "sobol", 0, golden["plan_sobol1600_param"], golden["plan_sobol1600_bary"])
+    pts = map_points(tgt, plan, 0, 20).reshape(-1, 2)
+    ref_pts = np.einsum("nj,ejd->end", golden["plan_sobol1600_bary"], tgt.elem_coords[:20]).reshape(-1, 2)
+    assert np.array_equal(pts.cpu().numpy(), ref_pts)
+    e, lam = loc.locate_many(pts)
+    assert np.array_equal(e.cpu().numpy(), golden["c1_sample_elem"])
+    assert np.array_equal(lam.cpu().numpy(), golden["c1_sample_lam"])
+
+
+def test_reference_seam_locate_many(tt, golden):
+    from paper_2603_00538_b200.locate import locate_many
+    n = int(np.sqrt(len(golden["c1s_elements"])))
+    nodes = golden["c1s_nodes"]
+    bbox = (*nodes.min(axis=0), *nodes.max(axis=0))
+    e, lam = locate_many(golden["loc_pts"], n, n, bbox, golden["c1s_cell_start"], golden["c1s_cell_elems"],
+                         golden["c1s_binv"], golden["c1s_origin"], 1e-12)
+    assert np.array_equal(e, golden["loc_elem"]) and np.array_equal(lam, golden["loc_lam"])
+
+
+def test_nearest_element_bit_exact(tt, golden, c1):
+    _, src = c1
+    loc = tt.UniformGridLocator.build(src)
+    assert np.array_equal(loc.nearest_many(golden["near_pts"]), golden["near_elem"])
+
+
+def test_locate_3d_matches_oracle_incl_outside_and_ties(tt):
+    m = tt.generate_cube_mesh(8, 0.25, seed=3)
+    loc = tt.UniformGridLocator.build(m)
+    g = O.Grid(m.nodes, m.elements)
+    rng = np.random.default_rng(5)
+    pts = np.concatenate([rng.random((20000, 3)) * 1.2 - 0.1, m.nodes,
+                          0.5 * (m.elem_coords[:, 0] + m.elem_coords[:, 1]),
+                          (m.elem_coords[:, 0] + m.elem_coords[:, 1] + m.elem_coords[:, 2]) / 3.0])
+    e, lam = loc.locate_many(pts)
+    eo, lo = g.locate_many(pts)
+    assert np.array_equal(e, eo)
+    assert np.array_equal(lam, lo)
+    out = pts[eo < 0][:300]
+    assert len(out) > 50
+    assert np.array_equal(loc.nearest_many(out), [g.nearest_element(p) for p in out])
+
+
+def test_snap_lambda_matches_oracle(tt, golden):
+    curved = tt.TriMesh.from_arrays(golden["curv_nodes"], golden["curv_elements"])
+    loc = tt.UniformGridLocator.build(curved)
+    g = O.Grid(curved.nodes, curved.elements)
+    pts = np.random.default_rng(2).random((3000, 2)) * 1.1 - 0.05
+    e, lam = loc.snap_many(pts)
+    eo, lo = g.locate_many(pts)
+    out = np.flatnonzero(eo < 0)
+    assert len(out) > 100
+    for i in out:
+        eo[i] = g.nearest_element(pts[i])
+    lo[out] = O.snap_lambda(g, eo[out], pts[out])
+    assert np.array_equal(e, eo)
+    assert np.array_equal(lam, lo)
+
+
+# ----------------------------------------------------------------- load vectors
+def test_load_analytic_injected_plan(tt, golden, c1):
+    tgt, _ = c1
+    plan = tt.SamplePlan(1600, "sobol", 0, golden["plan_sobol1600_param"], golden["plan_sobol1600_bary"])
+    b = tt.assemble_load_mc(tgt, tt.get_field("smooth"), plan)
+    assert _rel(b, golden["b_c1_analytic_smooth"]) <= REL_B
+    b = tt.assemble_load_mc(tgt, tt.get_field("linear"), plan)
+    assert _rel(b, golden["b_c1_analytic_linear"]) <= REL_B
+
+
+def test_load_traced_lambda_and_uniform_plan(tt, golden, c1):
+    tgt, _ = c1
+    f = tt.AnalyticField(lambda x, y: np.sin(x) * np.cos(y) + 2)
+    assert f.program(2) is not None
+    plan = tt.SamplePlan.build(64, "uniform", 3)
+    b = tt.assemble_load_mc(tgt, f, plan)
+    assert _rel(b, golden["b_c1_unif64_smooth"]) <= REL_B
+
+
+def test_load_host_black_box_path(tt, golden, c1):
+    tgt, _ = c1
+    calls = []
+
+    def fn(x, y):
+        calls.append(len(x))
+        return np.where(x > -1, np.sin(x) * np.cos(y) + 2, 0.0)   # np.where: not traceable
+    f = tt.AnalyticField(fn)
+    assert f.program(2) is None
+    plan = tt.SamplePlan.build(1600, "sobol", 0)
+    b = tt.assemble_load_mc(tgt, f, plan)
+    assert calls and _rel(b, golden["b_c1_analytic_smooth"]) <= REL_B
+
+
+def test_load_mesh_backed(tt, golden, c1):
+    tgt, src = c1
+    fs = tt.NodalField(src, golden["c1s_coeffs"])
+    plan = tt.SamplePlan.build(1600, "sobol", 0)
+    b = tt.assemble_load_mc(tgt, tt.MeshBackedField(fs), plan)
+    assert _rel(b, golden["b_c1_mesh_smooth"]) <= REL_B
+    b2 = tt.assemble_load_mc(tgt, tt.MeshBackedField(fs), plan, deterministic=False)
+    assert _rel(b2, golden["b_c1_mesh_smooth"]) <= REL_B
+
+
+def test_load_snap_path(tt, golden):
+    curved = tt.TriMesh.from_arrays(golden["curv_nodes"], golden["curv_elements"])
+    tsm = tt.TriMesh.from_arrays(golden["curvt_nodes"], golden["curvt_elements"])
+    fc = tt.NodalField(curved, golden["curv_coeffs"])
+    b = tt.assemble_load_mc(tsm, tt.MeshBackedField(fc), tt.SamplePlan.build(256, "sobol", 0))
+    assert _rel(b, golden["b_curv_snap"]) <= REL_B
+    with pytest.raises(tt.SourceEvalFailed):
+        tt.assemble_load_mc(tsm, tt.MeshBackedField(fc, outside="strict"), tt.SamplePlan.build(256))
+
+
+def test_load_deterministic_bitwise(tt, golden, c1):
+    tgt, src = c1
+    fs = tt.NodalField(src, golden["c1s_coeffs"])
+    plan = tt.SamplePlan.build(300, "sobol", 0)
+    src_f = tt.MeshBackedField(fs)
+    b1 = tt.assemble_load_mc(tgt, src_f, plan, workers=1)
+    b8 = tt.assemble_load_mc(tgt, src_f, plan, workers=8)
+    assert np.array_equal(b1, b8)
+
+
+def test_error_paths(tt):
+    nodes = np.array([[0.0, 0.0], [1.0, 0.0], [1.0, 1.0], [0.0, 1.0]])
+    mesh = tt.TriMesh.from_arrays(nodes, np.array([[0, 1, 2], [0, 2, 3]]))
+    plan = tt.SamplePlan.build(8, mode="uniform", seed=0)
+    bad = tt.AnalyticField(lambda x, y: x / (x - x))   # 0/0 -> nan, traced to the device
+    with pytest.raises(tt.SourceEvalFailed):
+        tt.assemble_load_mc(mesh, bad, plan)
+    with pytest.raises(tt.InvalidDensity):
+        tt.importance_weights(plan, lambda e, p: np.full((len(e), p.shape[1]), -1.0))(
+            mesh, tt.AnalyticField(lambda x, y: x))
+    with pytest.raises(tt.InvalidParameter):
+        tt.SamplePlan.build(0)
+    with pytest.raises(tt.InvalidParameter):
+        tt.SamplePlan.build(10, mode="stratified")
+    # constant source: sum_a psi_a = 1 integrates exactly (test_montecarlo.py:92-99)
+    for mode, seed, n in (("uniform", 0, 7), ("sobol", 2, 33), ("philox", 9, 17)):
+        b = tt.assemble_load_mc(mesh, tt.AnalyticField(lambda x, y: np.full_like(x, 3.25)),
+                                tt.SamplePlan.build(n, mode=mode, seed=seed))
+        assert b.sum() == pytest.approx(3.25 * mesh.domain_area, rel=1e-14)
+
+
+def test_importance_uniform_density_bitwise(tt, golden, c1):
+    tgt, _ = c1
+    source = tt.AnalyticField(lambda x, y: x ** 2 + y)
+    plan = tt.SamplePlan.build(200, mode="sobol", seed=1)
+    inv_area = 1.0 / tgt.elem_areas
+    dens = lambda e, p: np.broadcast_to(inv_area[e][:, None], (len(e), p.shape[1]))  # noqa: E731
+    assert np.array_equal(tt.assemble_load_mc(tgt, source, plan),
+                          tt.importance_weights(plan, dens)(tgt, source))
+    # a non-uniform density still integrates constants to the domain area
+    dens2 = lambda e, p: inv_area[e][:, None] * (1.5 - p[..., 0]) / (1.5 - tgt.centroids[e, 0])[:, None]  # noqa
+    b = tt.assemble_load_mc_weighted(tgt, tt.AnalyticField(lambda x, y: np.full_like(x, 2.0)), plan, dens2)
+    assert abs(b.sum() - 2.0) < 5e-3
+
+
+# ----------------------------------------------------------------- FEM / solve
+def test_mass_matrix(tt, golden, c1):
+    import scipy.sparse as sp
+    tgt, _ = c1
+    M = tt.assemble_mass_matrix(tgt)
+    Mr = sp.csr_matrix((golden["M_data"], golden["M_indices"], golden["M_indptr"]), shape=M.shape)
+    assert np.array_equal(M.csr.indptr, Mr.indptr) and np.array_equal(M.csr.indices, Mr.indices)
+    assert np.max(np.abs(M.csr.data - Mr.data)) <= 1e-15 * np.max(np.abs(Mr.data))
+    d = M.csr.toarray()
+    assert np.array_equal(d, d.T)
+    np.testing.assert_allclose(np.asarray(M.csr.sum(axis=1)).ravel(), tt.basis_integrals(tgt), atol=1e-15)
+
+
+def test_cg_solve(tt, golden, c1):
+    tgt, _ = c1
+    M = tt.assemble_mass_matrix(tgt)
+    x = tt.cg_solve(M, golden["b_c1_mesh_smooth"], tol=1e-14)
+    assert np.max(np.abs(x - golden["x_c1_mesh_tol14"])) <= 1e-12
+    assert np.all(tt.cg_solve(M, np.zeros(tgt.n_nodes)) == 0.0)
+    with pytest.raises(tt.DimensionMismatch):
+        tt.cg_solve(M, np.zeros(3))
+    with pytest.raises(tt.NoConvergence) as err:
+        tt.cg_solve(M, np.ones(tgt.n_nodes), tol=1e-16, maxiter=2)
+    assert err.value.best_x.shape == (tgt.n_nodes,) and err.value.residual > 0
+
+
+def test_transfer_mc_and_conservation(tt, golden, c1):
+    tgt, src = c1
+    fs = tt.NodalField(src, golden["c1s_coeffs"])
+    out = tt.transfer_mc(tgt, tt.MeshBackedField(fs), tt.SamplePlan.build(1600, "sobol", 0), cg_tol=1e-14)
+    assert np.max(np.abs(out.coeffs - golden["transfer_c1_mesh_tol14"])) <= 1e-12
+    assert abs(tt.integrate_field(fs) - float(golden["int_c1s"])) <= 1e-14
+    assert abs(tt.integrate_field(out) - float(golden["int_transfer"])) <= 1e-13
+
+
+def test_mc_operator(tt, golden, c1):
+    tgt, src = c1
+    fs = tt.NodalField(src, golden["c1s_coeffs"])
+    op = tt.MCTransferOperator(tgt, src, tt.SamplePlan.build(400, "sobol", 0), cg_tol=1e-14)
+    assert np.array_equal(op._src_elem[:50], golden["op_src_elem_first50"])
+    assert np.max(np.abs(op.apply(fs).coeffs - golden["op_apply_tol14"])) <= 1e-12
+    assert np.max(np.abs(op.apply_sampled(tt.MeshBackedField(fs)).coeffs
+                         - golden["op_apply_sampled_tol14"])) <= 1e-12
+
+
+# ----------------------------------------------------------------- 3-D vs oracle
+@pytest.mark.parametrize("mode", ["sobol", "philox"])
+def test_3d_mesh_backed_load_matches_oracle(tt, mode):
+    tgt = tt.generate_cube_mesh(6, 0.2, seed=20, split="kuhn")
+    src = tt.generate_cube_mesh(7, 0.2, seed=10, split="kuhn_mirror")
+    field = tt.get_field("smooth", dim=3)
+    fs = tt.NodalField.from_function(src, field.fn)
+    plan = tt.SamplePlan.build(48, mode, 5, dim=3)
+    b = tt.assemble_load_mc(tgt, tt.MeshBackedField(fs), plan)
+    g = O.Grid(src.nodes, src.elements)
+    srcf = lambda P: O.mesh_backed_eval(g, fs.coeffs, P)  # noqa: E731
+    area = np.abs(O.signed_measure(tgt.nodes, tgt.elements))
+    if mode == "sobol":
+        contrib = O.accumulate(tgt.nodes, tgt.elements, area, O.bary_map(O.sobol(48, 3, skip=5 * 48)), srcf)
+    else:
+        contrib = O.accumulate_philox(tgt.nodes, tgt.elements, area, 48, 5, srcf)
+    ref = O.reduce_to_nodes(tgt.n_nodes, tgt.elements, contrib)
+    assert _rel(b, ref) <= 1e-12
+    # the projection conserves the sampled mass exactly (sum_a psi_a = 1)
+    lin = tt.NodalField.from_function(src, lambda x, y, z: 2 * x - y + 0.5 * z + 1)
+    p64 = tt.SamplePlan.build(64, "sobol", 0, dim=3)
+    b = tt.assemble_load_mc(tgt, tt.MeshBackedField(lin), p64)
+    out = tt.transfer_mc(tgt, tt.MeshBackedField(lin), p64, cg_tol=1e-14)
+    assert tt.integrate_field(out) == pytest.approx(b.sum(), rel=1e-12)
+    assert abs(tt.integrate_field(out) - tt.integrate_field(lin)) < 5e-3 * tt.integrate_field(lin)
+
+
+def test_3d_analytic_constant_and_mass(tt):
+    tgt = tt.generate_cube_mesh(5, 0.2, seed=1)
+    b = tt.assemble_load_mc(tgt, tt.get_field("1.5 + 0*x"), tt.SamplePlan.build(16, "philox", 3, dim=3))
+    assert b.sum() == pytest.approx(1.5, rel=1e-13)
+    M = tt.assemble_mass_matrix(tgt)
+    Mo = O.mass_matrix(tgt.n_nodes, tgt.elements, tgt.elem_areas, 3)
+    assert abs(M.csr - Mo).max() <= 1e-17
+    assert M.csr.sum() == pytest.approx(1.0, abs=1e-13)
+
+
+# ----------------------------------------------------------------- full-size properties
+def test_c2_scale_properties(tt):
+    """C2-sized pair: constant source integrates exactly, b sums to the sampled
+    mass, the solve conserves it, and the deterministic path is bitwise stable."""
+    tgt = tt.generate_cube_mesh(40, 0.2, seed=20, split="kuhn")
+    src = tt.generate_cube_mesh(40, 0.2, seed=10, split="kuhn_mirror")
+    ones = tt.NodalField(src, np.ones(src.n_nodes))
+    plan = tt.SamplePlan.build(32, "sobol", 0, dim=3)
+    b = tt.assemble_load_mc(tgt, tt.MeshBackedField(ones), plan, device=True)
+    assert float(b.sum()) == pytest.approx(1.0, rel=1e-12)
+    fs = tt.NodalField.from_function(src, tt.get_field("smooth", dim=3).fn)
+    b1 = tt.assemble_load_mc(tgt, tt.MeshBackedField(fs), plan, device=True)
+    b2 = tt.assemble_load_mc(tgt, tt.MeshBackedField(fs), plan, device=True)
+    assert bool((b1 == b2).all())
+    x = tt.cg_solve(tgt.device.mass, b1, tol=1e-13)
+    out = tt.NodalField(tgt, x)
+    assert tt.integrate_field(out) == pytest.approx(float(b1.sum()), rel=1e-11)
