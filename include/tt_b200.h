@@ -53,6 +53,7 @@ extern "C" {
 #define TT_FLAG_OUTSIDE_STRICT   2  /* SourceEvalFailed: strict policy montecarlo.py:55-57 */
 #define TT_FLAG_CAPACITY         4  /* row/list capacity exceeded in assembly            */
 #define TT_FLAG_INVALID_DENSITY  8  /* InvalidDensity: p <= 0          montecarlo.py:129-130 */
+#define TT_FLAG_NONMANIFOLD     16  /* a facet shared by > 2 elements (mesh.py:50-53)      */
 
 /* ---- enums ---- */
 #define TT_PLAN_SHARED  0   /* one (N, k) barycentric table shared by all elements (reference) */
@@ -100,13 +101,22 @@ typedef struct tt_mesh {
     const double*  measure;   /* (n_elems,) |area| / |volume| (may be NULL where unused) */
 } tt_mesh_t;
 
-/* Packed per-element locate record: binv (dim x dim, row-major) then origin (dim);
- * stride TT_REC_STRIDE(dim) doubles (64 B in 2-D, 128 B in 3-D: one aligned line). */
+/* Packed per-element locate record, stride TT_REC_STRIDE(dim) doubles (64 B in 2-D,
+ * 128 B in 3-D: one aligned line per candidate test):
+ *   [0, d*d)        binv, row-major          (mesh.py:148-159)
+ *   [d*d, d*d+d)    origin = last vertex
+ *   next 16 bytes   float tau (certification margin), int32 nbr[0..2]
+ *   (3-D) next 4 B  int32 nbr[3]
+ * nbr[i] = element across the facet opposite vertex i (-1 on the boundary); tau and
+ * nbr are written by tt_grid_walk_prep (zero until then). */
 #define TT_REC_STRIDE(dim) ((dim) == 2 ? 8 : 16)
 
 typedef struct tt_grid {
     int32_t dim;
     int32_t n[3];             /* cells per axis; n[2] = 1 in 2-D; cell = (ix*n1 + iy)*n2 + iz */
+    int32_t walk;             /* 1: certified facet walk before the reference scan (needs
+                                 tt_grid_walk_prep on rec); 0: reference scan only */
+    int32_t reserved;
     double  lo[3];            /* mesh bbox (min corner) */
     double  hi[3];            /* mesh bbox (max corner) */
     int64_t n_elems;
@@ -141,6 +151,8 @@ typedef struct tt_source {
     const double*  coeffs;    /* TT_SRC_MESH (n_s,) nodal coefficients */
     const double*  values;    /* TT_SRC_VALUES (e_hi - e_lo, N) */
     const int32_t* cached_ids;/* TT_SRC_CACHED (e_hi - e_lo, N) source element per sample */
+    const int32_t* seeds;     /* TT_SRC_MESH optional (E_target,) walk start element per
+                                 target element (tt_seed_elements), or NULL */
 } tt_source_t;
 
 typedef struct tt_pcg_result {
@@ -187,6 +199,14 @@ int tt_locate_many(const double* points, int64_t count, int nx, int ny,
                    const int64_t* cell_start, const int32_t* cell_elems,
                    const double* binv /* (E,2,2) */, const double* origin /* (E,2) */,
                    double eps, int32_t* elem, double* lam /* (count,3) */, void* stream);
+/* Certified facet walk: fills tau and nbr of every record from
+ * the node incidence; sets TT_FLAG_NONMANIFOLD in *status for a non-manifold mesh. */
+int tt_grid_walk_prep(const tt_mesh_t* mesh, const int64_t* inc_start, const int32_t* inc,
+                      double eps, double* rec, int32_t* status, void* stream);
+/* seeds[e - e_lo] = source element containing the target element's centroid (reference
+ * scan, snapped when outside) -- the walk start for that element's samples. */
+int tt_seed_elements(const tt_grid_t* grid, const tt_mesh_t* target, int64_t e_lo,
+                     int64_t e_hi, int32_t* seeds, void* stream);
 int tt_nearest(const tt_grid_t* grid, const double* points, int64_t count,
                int32_t* elem /* out */, void* stream);
 int tt_snap(const tt_grid_t* grid, const double* points, int64_t count,
@@ -205,8 +225,8 @@ int tt_mc_load(const tt_mesh_t* target, int64_t e_lo, int64_t e_hi, const tt_pla
                int32_t* status, void* stream);
 
 int tt_mc_cache_ids(const tt_mesh_t* target, int64_t e_lo, int64_t e_hi, const tt_plan_t* plan,
-                    const tt_grid_t* grid, int32_t* ids /* (e_hi-e_lo, N): located or snapped */,
-                    void* stream);
+                    const tt_grid_t* grid, const int32_t* seeds /* (E_target,) or NULL */,
+                    int32_t* ids /* (e_hi-e_lo, N): located or snapped */, void* stream);
 
 /* ---- node reduction / incidence (deterministic np.add.at order) ---- */
 int tt_incidence_count(const tt_mesh_t* mesh, int64_t* inc_start /* (n_nodes+1) */,

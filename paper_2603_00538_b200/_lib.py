@@ -20,6 +20,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libtt_b200.so"
 
 TT_OK, TT_ERR_INVALID_PARAMETER, TT_ERR_DIMENSION_MISMATCH, TT_ERR_CUDA, TT_ERR_CAPACITY = 0, 1, 2, 3, 4
 TT_FLAG_NONFINITE, TT_FLAG_OUTSIDE_STRICT, TT_FLAG_CAPACITY, TT_FLAG_INVALID_DENSITY = 1, 2, 4, 8
+TT_FLAG_NONMANIFOLD = 16
 TT_PLAN_SHARED, TT_PLAN_PHILOX = 0, 1
 TT_SRC_EXPR, TT_SRC_MESH, TT_SRC_VALUES, TT_SRC_CACHED = 0, 1, 2, 3
 TT_OUTSIDE_SNAP, TT_OUTSIDE_STRICT = 0, 1
@@ -41,7 +42,8 @@ class tt_mesh_t(C.Structure):
 
 
 class tt_grid_t(C.Structure):
-    _fields_ = [("dim", C.c_int32), ("n", C.c_int32 * 3), ("lo", C.c_double * 3),
+    _fields_ = [("dim", C.c_int32), ("n", C.c_int32 * 3), ("walk", C.c_int32),
+                ("reserved", C.c_int32), ("lo", C.c_double * 3),
                 ("hi", C.c_double * 3), ("n_elems", C.c_int64), ("cell_start", C.c_void_p),
                 ("cell_elems", C.c_void_p), ("rec", C.c_void_p), ("centroids", C.c_void_p)]
 
@@ -60,7 +62,7 @@ class tt_source_t(C.Structure):
     _fields_ = [("kind", C.c_int32), ("outside", C.c_int32), ("dim", C.c_int32),
                 ("reserved", C.c_int32), ("expr", tt_expr_t), ("grid", tt_grid_t),
                 ("src_elems", C.c_void_p), ("coeffs", C.c_void_p), ("values", C.c_void_p),
-                ("cached_ids", C.c_void_p)]
+                ("cached_ids", C.c_void_p), ("seeds", C.c_void_p)]
 
 
 class tt_pcg_result_t(C.Structure):
@@ -89,6 +91,8 @@ _SIGNATURES = {
     "tt_grid_fill": ([C.POINTER(tt_mesh_t), C.POINTER(tt_grid_t), _P, _P, _P], _I),
     "tt_locate": ([C.POINTER(tt_grid_t), _P, _I64, _D, _P, _P, _P], _I),
     "tt_locate_many": ([_P, _I64, _I, _I, C.POINTER(_D), _P, _P, _P, _P, _D, _P, _P, _P], _I),
+    "tt_grid_walk_prep": ([C.POINTER(tt_mesh_t), _P, _P, _D, _P, _P, _P], _I),
+    "tt_seed_elements": ([C.POINTER(tt_grid_t), C.POINTER(tt_mesh_t), _I64, _I64, _P, _P], _I),
     "tt_nearest": ([C.POINTER(tt_grid_t), _P, _I64, _P, _P], _I),
     "tt_snap": ([C.POINTER(tt_grid_t), _P, _I64, _P, _P, _P], _I),
     "tt_map_points": ([C.POINTER(tt_mesh_t), _I64, _I64, C.POINTER(tt_plan_t), _P, _P], _I),
@@ -96,7 +100,7 @@ _SIGNATURES = {
     "tt_mc_load": ([C.POINTER(tt_mesh_t), _I64, _I64, C.POINTER(tt_plan_t),
                     C.POINTER(tt_source_t), _P, _P, _P, _P], _I),
     "tt_mc_cache_ids": ([C.POINTER(tt_mesh_t), _I64, _I64, C.POINTER(tt_plan_t),
-                         C.POINTER(tt_grid_t), _P, _P], _I),
+                         C.POINTER(tt_grid_t), _P, _P, _P], _I),
     "tt_incidence_count": ([C.POINTER(tt_mesh_t), _P, _P], _I),
     "tt_incidence_fill": ([C.POINTER(tt_mesh_t), _P, _P, _P, _P], _I),
     "tt_reduce_nodes": ([_I64, _I, _P, _P, _I64, _I64, _P, _P, _P], _I),

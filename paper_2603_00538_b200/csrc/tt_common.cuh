@@ -121,9 +121,27 @@ TT_D void map_point(const double* lam, const double (*v)[D], double* x) {
     }
 }
 
+// Record tail: certification margin and facet neighbours (written by walk prep).
+template <int D>
+struct RecTail {
+    float tau;
+    int nbr[D + 1];
+};
+
+template <int D>
+TT_D void load_tail(const double* __restrict__ rec, int64_t e, RecTail<D>& t) {
+    constexpr int S = (D == 2) ? 8 : 16;
+    const int4* q = reinterpret_cast<const int4*>(rec + e * S + D * D + D);
+    int4 a = __ldg(q);
+    t.tau = __int_as_float(a.x);
+    t.nbr[0] = a.y; t.nbr[1] = a.z; t.nbr[2] = a.w;
+    if constexpr (D == 3) t.nbr[3] = __ldg(reinterpret_cast<const int*>(q + 1));
+}
+
 // --------------------------------------------------------------- grid descriptor
 struct GridDev {
     int n0, n1, n2;
+    int walk;
     double lo[3], hi[3];
     const int64_t* __restrict__ cell_start;
     const int32_t* __restrict__ cell_elems;
@@ -134,6 +152,7 @@ struct GridDev {
 inline GridDev to_dev(const tt_grid_t& g) {
     GridDev d;
     d.n0 = g.n[0]; d.n1 = g.n[1]; d.n2 = g.dim == 3 ? g.n[2] : 1;
+    d.walk = g.walk;
     for (int c = 0; c < 3; ++c) { d.lo[c] = g.lo[c]; d.hi[c] = g.hi[c]; }
     d.cell_start = g.cell_start; d.cell_elems = g.cell_elems;
     d.rec = g.rec; d.centroids = g.centroids;
@@ -168,6 +187,45 @@ TT_D int locate_point(const GridDev& g, const double* x, double eps, double* lam
         }
     }
     return -1;
+}
+
+// Certified facet walk.  From `guess`, evaluate lambda in the current element A (the
+// reference formula, bit-identical); if min_i lambda_i >= tau_A the point lies at
+// distance > k*eps*diam_max from every other element of a valid tessellation, so A is
+// the ONLY element passing the reference predicate (lambda >= -eps) and therefore the
+// element the reference's ascending cell scan returns (A is in the point's cell list
+// because the cell map is monotone).  Otherwise step across the facet of the most
+// negative lambda.  Anything uncertain (near a facet, boundary, step cap) falls back to
+// the exact reference scan.  Returns the element or -1 (outside), lam filled as locate.
+template <int D>
+TT_D int locate_walk(const GridDev& g, const double* x, double eps, int guess, double* lam) {
+    int e = guess;
+#pragma unroll 1
+    for (int step = 0; step < 12 && e >= 0; ++step) {
+        Rec<D> r;
+        load_rec<D>(g.rec, e, r);
+        RecTail<D> t;
+        load_tail<D>(g.rec, e, t);
+        double l[D + 1];
+        bary_from_rec<D>(r, x, l);
+        int imin = 0;
+        double lmin = l[0];
+#pragma unroll
+        for (int i = 1; i <= D; ++i)
+            if (l[i] < lmin) { lmin = l[i]; imin = i; }
+        if (lmin >= (double)t.tau) {
+#pragma unroll
+            for (int i = 0; i <= D; ++i) lam[i] = l[i];
+            return e;
+        }
+        if (lmin >= -eps) break;  // inside within the slack but not certified: exact scan
+        int nb = t.nbr[0];
+#pragma unroll
+        for (int i = 1; i <= D; ++i)
+            if (imin == i) nb = t.nbr[i];
+        e = nb;
+    }
+    return locate_point<D>(g, x, eps, lam);
 }
 
 // Expanding-ring nearest centroid, lowest id on ties, stop one ring after the first
@@ -242,6 +300,23 @@ TT_D void snap_lambda(const GridDev& g, int e, const double* x, double* lam) {
     for (int i = 2; i <= D; ++i) s = add(s, lam[i]);
 #pragma unroll
     for (int i = 0; i <= D; ++i) lam[i] = div(lam[i], s);
+}
+
+// Out-of-line snap for OUTSIDE points (rare): keeps the ring search's registers and
+// stack out of the fused kernels' hot loops.
+template <int D>
+struct SnapOut {
+    int e;
+    double l[D + 1];
+};
+
+template <int D>
+__device__ __noinline__ SnapOut<D> snap_point(const GridDev g, double x0, double x1, double x2) {
+    const double x[3] = {x0, x1, x2};
+    SnapOut<D> o;
+    o.e = nearest_element<D>(g, x);
+    snap_lambda<D>(g, o.e, x, o.l);
+    return o;
 }
 
 }  // namespace tt

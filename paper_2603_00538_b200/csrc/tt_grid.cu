@@ -285,6 +285,124 @@ __global__ void snap_kernel(GridDev g, const double* __restrict__ pts, int64_t K
     for (int c = 0; c <= D; ++c) lam[i * (D + 1) + c] = l[c];
 }
 
+// ---------------------------------------------------------------- certified walk prep
+template <int D>
+__global__ void max_diam_kernel(int64_t E, const double* __restrict__ nodes,
+                                const int32_t* __restrict__ elems,
+                                unsigned long long* __restrict__ out) {
+    constexpr int K = D + 1;
+    double best = 0.0;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        double v[K][D];
+        for (int i = 0; i < K; ++i)
+            for (int c = 0; c < D; ++c) v[i][c] = nodes[(int64_t)elems[e * K + i] * D + c];
+        for (int i = 0; i < K; ++i)
+            for (int j = i + 1; j < K; ++j) {
+                double d2 = 0.0;
+                for (int c = 0; c < D; ++c) d2 += (v[i][c] - v[j][c]) * (v[i][c] - v[j][c]);
+                best = fmax(best, d2);
+            }
+    }
+    // positive doubles order like their bit patterns
+    atomicMax(out, (unsigned long long)__double_as_longlong(sqrt(best)));
+}
+
+template <int D>
+__global__ void walk_prep_kernel(int64_t E, const double* __restrict__ nodes,
+                                 const int32_t* __restrict__ elems,
+                                 const int64_t* __restrict__ inc_start,
+                                 const int32_t* __restrict__ inc, double eps, double dmax,
+                                 double* __restrict__ rec, int32_t* __restrict__ status) {
+    constexpr int K = D + 1;
+    constexpr int S = (D == 2) ? 8 : 16;
+    int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= E) return;
+    int vid[K];
+    double v[K][D];
+    for (int i = 0; i < K; ++i) {
+        vid[i] = elems[e * K + i];
+        for (int c = 0; c < D; ++c) v[i][c] = nodes[(int64_t)vid[i] * D + c];
+    }
+    int nbr[4] = {-1, -1, -1, -1};
+    bool nonmanifold = false;
+    for (int i = 0; i < K; ++i) {          // facet opposite vertex i
+        int f[D];
+        for (int t = 0, q = 0; t < K; ++t)
+            if (t != i) f[q++] = vid[t];
+        int found = -1, matches = 0;
+        for (int64_t q = inc_start[f[0]]; q < inc_start[f[0] + 1]; ++q) {
+            int64_t e2 = inc[q] / K;
+            if (e2 == e) continue;
+            bool all = true;
+            for (int a = 1; a < D && all; ++a) {
+                bool has = false;
+                for (int b = 0; b < K; ++b) has |= (elems[e2 * K + b] == f[a]);
+                all = has;
+            }
+            if (all) { found = (int)e2; ++matches; }
+        }
+        if (matches > 1) nonmanifold = true;
+        nbr[i] = found;
+    }
+    // smallest height: 2A / max edge (2-D), 3V / max face area (3-D)
+    double hmin;
+    if constexpr (D == 2) {
+        double a2 = fabs((v[1][0] - v[0][0]) * (v[2][1] - v[0][1]) - (v[2][0] - v[0][0]) * (v[1][1] - v[0][1]));
+        double lmax = 0.0;
+        for (int i = 0; i < 3; ++i) {
+            int j = (i + 1) % 3;
+            lmax = fmax(lmax, hypot(v[i][0] - v[j][0], v[i][1] - v[j][1]));
+        }
+        hmin = a2 / lmax;
+    } else {
+        double u[3], w[3], t3[3];
+        for (int c = 0; c < 3; ++c) { u[c] = v[1][c] - v[0][c]; w[c] = v[2][c] - v[0][c]; t3[c] = v[3][c] - v[0][c]; }
+        double vol6 = fabs(u[0] * (w[1] * t3[2] - w[2] * t3[1]) + u[1] * (w[2] * t3[0] - w[0] * t3[2]) +
+                           u[2] * (w[0] * t3[1] - w[1] * t3[0]));
+        double amax2 = 0.0;  // (2 * face area)^2
+        for (int i = 0; i < 4; ++i) {
+            int a = (i + 1) % 4, b = (i + 2) % 4, c = (i + 3) % 4;
+            double p[3], q[3];
+            for (int k = 0; k < 3; ++k) { p[k] = v[b][k] - v[a][k]; q[k] = v[c][k] - v[a][k]; }
+            double cx = p[1] * q[2] - p[2] * q[1], cy = p[2] * q[0] - p[0] * q[2], cz = p[0] * q[1] - p[1] * q[0];
+            amax2 = fmax(amax2, cx * cx + cy * cy + cz * cz);
+        }
+        hmin = vol6 / sqrt(amax2);  // 3V / A = (6V) / (2A)
+    }
+    // margin: distance > k * (eps + rounding) * diam_max from every other element,
+    // doubled, plus an absolute slack far above the lambda rounding error
+    double tau = 2.0 * K * (eps + 1e-13) * dmax / hmin + 1e-12;
+    if (!(tau < 0.25)) tau = 2.0;  // degenerate/pathological: never certify
+    int4 tail;
+    tail.x = __float_as_int(__double2float_ru(tau));
+    tail.y = nbr[0]; tail.z = nbr[1]; tail.w = nbr[2];
+    int4* q = reinterpret_cast<int4*>(rec + e * S + D * D + D);
+    *q = tail;
+    if constexpr (D == 3) reinterpret_cast<int*>(q + 1)[0] = nbr[3];
+    if (nonmanifold) atomicOr(status, TT_FLAG_NONMANIFOLD);
+}
+
+template <int D>
+__global__ void seed_kernel(GridDev g, const double* __restrict__ nodes,
+                            const int32_t* __restrict__ elems, int64_t e_lo, int64_t n_el,
+                            int32_t* __restrict__ seeds) {
+    constexpr int K = D + 1;
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n_el) return;
+    int64_t e = e_lo + i;
+    double x[D];
+    for (int c = 0; c < D; ++c) {
+        double s = add(nodes[(int64_t)elems[e * K] * D + c], nodes[(int64_t)elems[e * K + 1] * D + c]);
+        for (int a = 2; a < K; ++a) s = add(s, nodes[(int64_t)elems[e * K + a] * D + c]);
+        x[c] = div(s, (double)K);
+    }
+    double l[D + 1];
+    int es = locate_point<D>(g, x, 1e-12, l);
+    if (es < 0) es = nearest_element<D>(g, x);
+    seeds[i] = es;
+}
+
 static int64_t ncells_of(const tt_grid_t* g) {
     return (int64_t)g->n[0] * g->n[1] * (g->dim == 3 ? g->n[2] : 1);
 }
@@ -456,4 +574,52 @@ extern "C" int tt_snap(const tt_grid_t* g, const double* pts, int64_t K, int32_t
     else
         snap_kernel<3><<<grid_for(K, 128), 128, 0, s>>>(gd, pts, K, elem, lam);
     return launch_check("snap_kernel");
+}
+
+extern "C" int tt_grid_walk_prep(const tt_mesh_t* m, const int64_t* inc_start, const int32_t* inc,
+                                 double eps, double* rec, int32_t* status, void* stream) {
+    if (!m || (m->dim != 2 && m->dim != 3) || !inc_start || !inc || !rec) {
+        set_error("tt_grid_walk_prep: bad arguments");
+        return TT_ERR_INVALID_PARAMETER;
+    }
+    if (m->n_elems == 0) return TT_OK;
+    auto s = as_stream(stream);
+    unsigned long long* dm = nullptr;
+    int st = cuda_status(cudaMallocAsync((void**)&dm, sizeof(unsigned long long), s), "walk alloc");
+    if (st) return st;
+    cudaMemsetAsync(dm, 0, sizeof(unsigned long long), s);
+    if (m->dim == 2)
+        max_diam_kernel<2><<<sm_count() * 4, 256, 0, s>>>(m->n_elems, m->nodes, m->elems, dm);
+    else
+        max_diam_kernel<3><<<sm_count() * 4, 256, 0, s>>>(m->n_elems, m->nodes, m->elems, dm);
+    unsigned long long bits = 0;
+    cudaMemcpyAsync(&bits, dm, sizeof(bits), cudaMemcpyDeviceToHost, s);
+    st = cuda_status(cudaStreamSynchronize(s), "walk prep diameter");
+    cudaFreeAsync(dm, s);
+    if (st) return st;
+    double dmax;
+    memcpy(&dmax, &bits, sizeof(dmax));
+    if (m->dim == 2)
+        walk_prep_kernel<2><<<grid_for(m->n_elems, 128), 128, 0, s>>>(m->n_elems, m->nodes, m->elems,
+                                                                      inc_start, inc, eps, dmax, rec, status);
+    else
+        walk_prep_kernel<3><<<grid_for(m->n_elems, 128), 128, 0, s>>>(m->n_elems, m->nodes, m->elems,
+                                                                      inc_start, inc, eps, dmax, rec, status);
+    return launch_check("walk_prep_kernel");
+}
+
+extern "C" int tt_seed_elements(const tt_grid_t* g, const tt_mesh_t* t, int64_t e_lo, int64_t e_hi,
+                                int32_t* seeds, void* stream) {
+    if (!grid_ok(g) || !t || t->dim != g->dim || e_lo < 0 || e_hi > t->n_elems || e_lo > e_hi) {
+        set_error("tt_seed_elements: bad arguments");
+        return TT_ERR_INVALID_PARAMETER;
+    }
+    if (e_hi == e_lo) return TT_OK;
+    GridDev gd = to_dev(*g);
+    auto s = as_stream(stream);
+    if (g->dim == 2)
+        seed_kernel<2><<<grid_for(e_hi - e_lo, 128), 128, 0, s>>>(gd, t->nodes, t->elems, e_lo, e_hi - e_lo, seeds);
+    else
+        seed_kernel<3><<<grid_for(e_hi - e_lo, 128), 128, 0, s>>>(gd, t->nodes, t->elems, e_lo, e_hi - e_lo, seeds);
+    return launch_check("seed_kernel");
 }

@@ -28,6 +28,7 @@ struct SrcDev {
     const double* __restrict__ coeffs;
     const double* __restrict__ values;
     const int32_t* __restrict__ cached;
+    const int32_t* __restrict__ seeds;
 };
 
 template <int D>
@@ -63,17 +64,21 @@ __device__ __forceinline__ double eval_expr(const tt_expr_t& p, const double* x)
 
 // MeshBackedField.__call__ (montecarlo.py:49-65) + eval_in_elements (fem.py:36-38)
 template <int D>
-__device__ __forceinline__ double eval_mesh(const SrcDev& s, const double* x, int& flags) {
+__device__ __forceinline__ double eval_mesh(const SrcDev& s, const double* x, int& flags, int& guess) {
     constexpr int K = D + 1;
     double l[K];
-    int e = locate_point<D>(s.grid, x, 1e-12, l);
+    int e = (s.grid.walk && guess >= 0) ? locate_walk<D>(s.grid, x, 1e-12, guess, l)
+                                        : locate_point<D>(s.grid, x, 1e-12, l);
+    if (e >= 0) guess = e;
     if (e < 0) {
         if (s.outside == TT_OUTSIDE_STRICT) {
             flags |= TT_FLAG_OUTSIDE_STRICT;
             return 0.0;
         }
-        e = nearest_element<D>(s.grid, x);
-        snap_lambda<D>(s.grid, e, x, l);
+        const SnapOut<D> sn = snap_point<D>(s.grid, x[0], x[1], D == 3 ? x[D - 1] : 0.0);
+        e = sn.e;
+#pragma unroll
+        for (int i = 0; i < K; ++i) l[i] = sn.l[i];
     }
     const int32_t* conn = s.src_elems + (int64_t)e * K;
     double f = mul(__ldg(s.coeffs + __ldg(conn)), l[0]);
@@ -98,9 +103,10 @@ __device__ __forceinline__ double eval_cached(const SrcDev& s, const double* x, 
 
 template <int D, int SRC>
 __device__ __forceinline__ double eval_source(const SrcDev& s, const tt_expr_t& expr,
-                                              const double* x, int64_t vidx, int& flags) {
+                                              const double* x, int64_t vidx, int& flags,
+                                              int& guess) {
     if constexpr (SRC == TT_SRC_EXPR) return eval_expr<D>(expr, x);
-    else if constexpr (SRC == TT_SRC_MESH) return eval_mesh<D>(s, x, flags);
+    else if constexpr (SRC == TT_SRC_MESH) return eval_mesh<D>(s, x, flags, guess);
     else if constexpr (SRC == TT_SRC_CACHED) return eval_cached<D>(s, x, __ldg(s.cached + vidx));
     else return __ldg(s.values + vidx);
 }
@@ -175,6 +181,9 @@ __global__ void __launch_bounds__(256) mc_load_kernel(TargetDev t, int64_t e_lo,
         if (active) {
             double v[K][D];
             load_elem<D>(t, e, v);
+            int guess = -1;
+            if constexpr (SRC == TT_SRC_MESH)
+                if (src.seeds) guess = __ldg(src.seeds + e);
             for (int64_t j = sub_lane; j < N; j += G) {
                 double lam[K];
                 if constexpr (PLAN == TT_PLAN_SHARED) {
@@ -185,7 +194,7 @@ __global__ void __launch_bounds__(256) mc_load_kernel(TargetDev t, int64_t e_lo,
                 }
                 double x[D];
                 map_point<D>(lam, v, x);
-                double f = eval_source<D, SRC>(src, expr, x, le * N + j, flags);
+                double f = eval_source<D, SRC>(src, expr, x, le * N + j, flags, guess);
                 if (!isfinite(f)) flags |= TT_FLAG_NONFINITE;
 #pragma unroll
                 for (int i = 0; i < K; ++i) acc[i] = fma(f, lam[i], acc[i]);
@@ -240,7 +249,8 @@ __global__ void eval_points_kernel(SrcDev src, const __grid_constant__ tt_expr_t
     if (i < count) {
         double x[D];
         for (int c = 0; c < D; ++c) x[c] = pts[i * D + c];
-        double f = eval_source<D, SRC>(src, expr, x, i, flags);
+        int guess = -1;
+        double f = eval_source<D, SRC>(src, expr, x, i, flags, guess);
         if (!isfinite(f)) flags |= TT_FLAG_NONFINITE;
         out[i] = f;
     }
@@ -249,7 +259,7 @@ __global__ void eval_points_kernel(SrcDev src, const __grid_constant__ tt_expr_t
 
 template <int D, int PLAN>
 __global__ void cache_ids_kernel(TargetDev t, int64_t e_lo, int64_t n_el, PlanDev plan, GridDev g,
-                                 int32_t* __restrict__ ids) {
+                                 const int32_t* __restrict__ seeds, int32_t* __restrict__ ids) {
     constexpr int K = D + 1;
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n_el * plan.n) return;
@@ -265,8 +275,9 @@ __global__ void cache_ids_kernel(TargetDev t, int64_t e_lo, int64_t n_el, PlanDe
     }
     double x[D], l[K];
     map_point<D>(lam, v, x);
-    int es = locate_point<D>(g, x, 1e-12, l);
-    if (es < 0) es = nearest_element<D>(g, x);  // transfer.py:79-81
+    int es = (g.walk && seeds) ? locate_walk<D>(g, x, 1e-12, __ldg(seeds + e), l)
+                               : locate_point<D>(g, x, 1e-12, l);
+    if (es < 0) es = snap_point<D>(g, x[0], x[1], D == 3 ? x[D - 1] : 0.0).e;  // transfer.py:79-81
     ids[i] = es;
 }
 
@@ -325,6 +336,7 @@ static SrcDev to_src(const tt_source_t& s) {
     d.coeffs = s.coeffs;
     d.values = s.values;
     d.cached = s.cached_ids;
+    d.seeds = s.seeds;
     return d;
 }
 
@@ -445,7 +457,7 @@ extern "C" int tt_mc_load(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const 
 }
 
 extern "C" int tt_mc_cache_ids(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_plan_t* p,
-                               const tt_grid_t* g, int32_t* ids, void* stream) {
+                               const tt_grid_t* g, const int32_t* seeds, int32_t* ids, void* stream) {
     if (!t || !p || !g || p->dim != t->dim || g->dim != t->dim || e_lo < 0 || e_hi > t->n_elems ||
         e_lo > e_hi) {
         set_error("tt_mc_cache_ids: bad arguments");
@@ -459,11 +471,11 @@ extern "C" int tt_mc_cache_ids(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, c
     auto s = as_stream(stream);
     const unsigned nb = grid_for(total, 256);
     if (t->dim == 2) {
-        if (p->kind == TT_PLAN_SHARED) cache_ids_kernel<2, TT_PLAN_SHARED><<<nb, 256, 0, s>>>(td, e_lo, e_hi - e_lo, pd, gd, ids);
-        else cache_ids_kernel<2, TT_PLAN_PHILOX><<<nb, 256, 0, s>>>(td, e_lo, e_hi - e_lo, pd, gd, ids);
+        if (p->kind == TT_PLAN_SHARED) cache_ids_kernel<2, TT_PLAN_SHARED><<<nb, 256, 0, s>>>(td, e_lo, e_hi - e_lo, pd, gd, seeds, ids);
+        else cache_ids_kernel<2, TT_PLAN_PHILOX><<<nb, 256, 0, s>>>(td, e_lo, e_hi - e_lo, pd, gd, seeds, ids);
     } else {
-        if (p->kind == TT_PLAN_SHARED) cache_ids_kernel<3, TT_PLAN_SHARED><<<nb, 256, 0, s>>>(td, e_lo, e_hi - e_lo, pd, gd, ids);
-        else cache_ids_kernel<3, TT_PLAN_PHILOX><<<nb, 256, 0, s>>>(td, e_lo, e_hi - e_lo, pd, gd, ids);
+        if (p->kind == TT_PLAN_SHARED) cache_ids_kernel<3, TT_PLAN_SHARED><<<nb, 256, 0, s>>>(td, e_lo, e_hi - e_lo, pd, gd, seeds, ids);
+        else cache_ids_kernel<3, TT_PLAN_PHILOX><<<nb, 256, 0, s>>>(td, e_lo, e_hi - e_lo, pd, gd, seeds, ids);
     }
     return launch_check("cache_ids_kernel");
 }

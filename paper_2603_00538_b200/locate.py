@@ -50,11 +50,13 @@ class UniformGridLocator:
     """
 
     def __init__(self, mesh: SimplexMesh, dims, cell_start: torch.Tensor,
-                 cell_elems: torch.Tensor):
+                 cell_elems: torch.Tensor, walk: bool = False):
         self.mesh = mesh
         self.dims = tuple(int(d) for d in dims)
         self.cell_start_dev = cell_start
         self.cell_elems_dev = cell_elems
+        self.walk = walk
+        self._seeds = {}
 
     @property
     def nx(self):
@@ -70,7 +72,11 @@ class UniformGridLocator:
 
     @classmethod
     def build(cls, mesh: SimplexMesh, nx: int | None = None, ny: int | None = None,
-              nz: int | None = None) -> "UniformGridLocator":
+              nz: int | None = None, walk: bool = True) -> "UniformGridLocator":
+        """``walk=True`` additionally prepares the certified facet walk:
+        queries start from a nearby element and are answered without the cell scan
+        whenever the hit is provably the unique element within the slack -- the same
+        element and barycentrics the reference scan returns (valid tessellations)."""
         d0 = default_dims(mesh.n_elems, mesh.DIM)
         nx = d0[0] if nx is None else int(nx)
         ny = nx if ny is None else int(ny)
@@ -94,6 +100,9 @@ class UniformGridLocator:
         _lib.call("tt_grid_fill", C.byref(mdesc), C.byref(desc), _lib.ptr(cell_elems),
                   _lib.ptr(cursor), s)
         loc.cell_elems_dev = cell_elems[:total] if total else cell_elems[:0]
+        if walk:
+            _walk_prep(mesh)
+            loc.walk = True
         return loc
 
     def desc(self) -> _lib.tt_grid_t:
@@ -103,6 +112,7 @@ class UniformGridLocator:
         g = _lib.tt_grid_t()
         g.dim = d
         g.n[0], g.n[1], g.n[2] = self.dims
+        g.walk = 1 if self.walk else 0
         for c in range(3):
             g.lo[c] = m.lo[c] if c < d else 0.0
             g.hi[c] = m.hi[c] if c < d else 1.0
@@ -112,6 +122,20 @@ class UniformGridLocator:
         g.rec = _lib.ptr(dm.rec).value
         g.centroids = _lib.ptr(dm.centroids).value
         return g
+
+    def seeds_for(self, target) -> torch.Tensor:
+        """Walk start per target element: the source element containing the target
+        element's centroid (cached per target mesh; meshes are immutable)."""
+        key = id(target)
+        hit = self._seeds.get(key)
+        if hit is not None and hit[0] is target:
+            return hit[1]
+        seeds = torch.empty(target.n_elems, dtype=torch.int32, device=self.cell_start_dev.device)
+        g, t = self.desc(), target.device.desc()
+        _lib.call("tt_seed_elements", C.byref(g), C.byref(t), 0, target.n_elems, _lib.ptr(seeds),
+                  _lib.stream_handle())
+        self._seeds[key] = (target, seeds)
+        return seeds
 
     @cached_property
     def cell_start(self) -> np.ndarray:
@@ -175,6 +199,22 @@ class UniformGridLocator:
         if was_np:
             return elem.cpu().numpy(), lam.cpu().numpy()
         return elem, lam
+
+
+def _walk_prep(mesh):
+    """Facet neighbours + certification margins into the mesh's locate records."""
+    dm = mesh.device
+    if getattr(dm, "walk_ready", False):
+        return
+    from .errors import NonManifold
+    inc_start, inc = dm.incidence
+    status = _lib.status_word()
+    desc = dm.desc()
+    _lib.call("tt_grid_walk_prep", C.byref(desc), _lib.ptr(inc_start), _lib.ptr(inc), EPS_LOC,
+              _lib.ptr(dm.rec), _lib.ptr(status), _lib.stream_handle())
+    if int(status.item()) & _lib.TT_FLAG_NONMANIFOLD:
+        raise NonManifold("a facet is shared by more than two elements")
+    dm.walk_ready = True
 
 
 def locate_many(points, nx, ny, bbox, cell_start, cell_elems, binv, origin, eps):

@@ -91,7 +91,7 @@ class MeshBackedField:
     def dim(self):
         return self.field.mesh.DIM
 
-    def desc(self, dim: int):
+    def desc(self, dim: int, target=None):
         if dim != self.dim:
             raise DimensionMismatch(f"{self.dim}-D source queried with {dim}-D points")
         s = _lib.tt_source_t()
@@ -101,6 +101,8 @@ class MeshBackedField:
         s.grid = self.locator.desc()
         s.src_elems = _lib.ptr(self.field.mesh.device.elems).value
         s.coeffs = _lib.ptr(self.field.coeffs_dev).value
+        if target is not None and self.locator.walk:
+            s.seeds = _lib.ptr(self.locator.seeds_for(target)).value
         return s
 
     def __call__(self, points):
@@ -252,10 +254,10 @@ class SamplePlan:
 
 
 # -------------------------------------------------------------------- assembly
-def _source_desc(source, dim):
+def _source_desc(source, dim, target=None):
     """(tt_source_t or None for a host black box, tensors to keep alive)."""
     if isinstance(source, MeshBackedField):
-        return source.desc(dim), (source.field.coeffs_dev,)
+        return source.desc(dim, target), (source.field.coeffs_dev,)
     if isinstance(source, AnalyticField):
         if source.dim is not None and source.dim != dim:
             raise DimensionMismatch(f"{source.dim}-D field on a {dim}-D mesh")
@@ -290,7 +292,7 @@ def element_contributions(target, source, plan: SamplePlan, e_lo: int = 0,
     contrib = out if out is not None else torch.empty((e_hi - e_lo, k), dtype=torch.float64,
                                                       device=dm.nodes.device)
     status = status if status is not None else _lib.status_word()
-    sdesc, keep = _source_desc(source, target.DIM)
+    sdesc, keep = _source_desc(source, target.DIM, target)
     mdesc, pdesc = dm.desc(), plan.desc()
     s = _lib.stream_handle()
     if sdesc is not None:
@@ -328,7 +330,7 @@ def load_vector(target, source, plan: SamplePlan, e_lo: int = 0, e_hi: int | Non
     e_hi = target.n_elems if e_hi is None else e_hi
     dm = target.device
     status = status if status is not None else _lib.status_word()
-    sdesc, keep = _source_desc(source, target.DIM)
+    sdesc, keep = _source_desc(source, target.DIM, target)
     if deterministic or sdesc is None:
         contrib = element_contributions(target, source, plan, e_lo, e_hi, status=status)
         b = dm.reduce_nodes(contrib, e_lo, e_hi)

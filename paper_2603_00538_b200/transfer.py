@@ -48,8 +48,9 @@ class MCTransferOperator:
         self.src_elem_dev = torch.empty((target.n_elems, plan.n_samples), dtype=torch.int32,
                                         device=dm.nodes.device)
         mdesc, pdesc, gdesc = dm.desc(), plan.desc(), self.locator.desc()
+        seeds = self.locator.seeds_for(target) if self.locator.walk else None
         _lib.call("tt_mc_cache_ids", C.byref(mdesc), 0, target.n_elems, C.byref(pdesc),
-                  C.byref(gdesc), _lib.ptr(self.src_elem_dev), _lib.stream_handle())
+                  C.byref(gdesc), _lib.ptr(seeds), _lib.ptr(self.src_elem_dev), _lib.stream_handle())
 
     @property
     def _src_elem(self):

@@ -375,3 +375,37 @@ def test_c2_scale_properties(tt):
     x = tt.cg_solve(tgt.device.mass, b1, tol=1e-13)
     out = tt.NodalField(tgt, x)
     assert tt.integrate_field(out) == pytest.approx(float(b1.sum()), rel=1e-11)
+
+
+# ----------------------------------------------------------------- certified walk
+def _walk_vs_scan(tt, tgt, src, n, dim, mode="sobol"):
+    fs = tt.NodalField.from_function(src, tt.get_field("smooth", dim=dim).fn)
+    plan = tt.SamplePlan.build(n, mode, 1, dim=dim)
+    lw = tt.UniformGridLocator.build(src, walk=True)
+    ls = tt.UniformGridLocator.build(src, walk=False)
+    bw = tt.assemble_load_mc(tgt, tt.MeshBackedField(fs, lw), plan)
+    bs = tt.assemble_load_mc(tgt, tt.MeshBackedField(fs, ls), plan)
+    assert np.array_equal(bw, bs)          # same ids + same lambdas -> bitwise b
+    ow = tt.MCTransferOperator(tgt, src, plan, source_locator=lw)
+    os_ = tt.MCTransferOperator(tgt, src, plan, source_locator=ls)
+    assert np.array_equal(ow.src_elem_dev.cpu().numpy(), os_.src_elem_dev.cpu().numpy())
+
+
+def test_walk_equals_reference_scan_2d(tt, golden, c1):
+    tgt, src = c1
+    _walk_vs_scan(tt, tgt, src, 400, 2)
+    curved = tt.TriMesh.from_arrays(golden["curv_nodes"], golden["curv_elements"])
+    tsm = tt.TriMesh.from_arrays(golden["curvt_nodes"], golden["curvt_elements"])
+    _walk_vs_scan(tt, tsm, curved, 256, 2)
+    # coincident meshes: many samples on shared edges/vertices of the source
+    m = tt.generate_square_mesh(10, 0.0, diagonal="left")
+    _walk_vs_scan(tt, m, m, 64, 2)
+
+
+@pytest.mark.parametrize("mode", ["sobol", "philox"])
+def test_walk_equals_reference_scan_3d(tt, mode):
+    tgt = tt.generate_cube_mesh(12, 0.2, seed=20, split="kuhn")
+    src = tt.generate_cube_mesh(13, 0.25, seed=10, split="kuhn_mirror")
+    _walk_vs_scan(tt, tgt, src, 64, 3, mode)
+    flat = tt.generate_cube_mesh(6, 0.0)
+    _walk_vs_scan(tt, flat, flat, 32, 3, mode)
