@@ -151,8 +151,8 @@ typedef struct tt_source {
     const double*  coeffs;    /* TT_SRC_MESH (n_s,) nodal coefficients */
     const double*  values;    /* TT_SRC_VALUES (e_hi - e_lo, N) */
     const int32_t* cached_ids;/* TT_SRC_CACHED (e_hi - e_lo, N) source element per sample */
-    const int32_t* seeds;     /* TT_SRC_MESH optional (E_target,) walk start element per
-                                 target element (tt_seed_elements), or NULL */
+    const int32_t* seeds;     /* TT_SRC_MESH optional (E_target, dim+2) walk start elements
+                                 per target element (tt_seed_elements), or NULL */
 } tt_source_t;
 
 typedef struct tt_pcg_result {
@@ -203,8 +203,9 @@ int tt_locate_many(const double* points, int64_t count, int nx, int ny,
  * the node incidence; sets TT_FLAG_NONMANIFOLD in *status for a non-manifold mesh. */
 int tt_grid_walk_prep(const tt_mesh_t* mesh, const int64_t* inc_start, const int32_t* inc,
                       double eps, double* rec, int32_t* status, void* stream);
-/* seeds[e - e_lo] = source element containing the target element's centroid (reference
- * scan, snapped when outside) -- the walk start for that element's samples. */
+/* seeds[(e - e_lo)*(dim+2) + s] = source element containing, for s = 0, the target
+ * element's centroid c and, for s = 1 + i, the point (v_i + c)/2 (reference scan, snapped
+ * when outside): walk starts for the element's samples (nearest by max barycentric). */
 int tt_seed_elements(const tt_grid_t* grid, const tt_mesh_t* target, int64_t e_lo,
                      int64_t e_hi, int32_t* seeds, void* stream);
 int tt_nearest(const tt_grid_t* grid, const double* points, int64_t count,
@@ -225,7 +226,7 @@ int tt_mc_load(const tt_mesh_t* target, int64_t e_lo, int64_t e_hi, const tt_pla
                int32_t* status, void* stream);
 
 int tt_mc_cache_ids(const tt_mesh_t* target, int64_t e_lo, int64_t e_hi, const tt_plan_t* plan,
-                    const tt_grid_t* grid, const int32_t* seeds /* (E_target,) or NULL */,
+                    const tt_grid_t* grid, const int32_t* seeds /* (E_target, dim+2) or NULL */,
                     int32_t* ids /* (e_hi-e_lo, N): located or snapped */, void* stream);
 
 /* ---- node reduction / incidence (deterministic np.add.at order) ---- */

@@ -105,19 +105,21 @@ struct PcgArgs {
     const double* __restrict__ b;
     double tol;
     int64_t maxiter;
-    double* __restrict__ x;
-    double* __restrict__ best_x;
-    double* __restrict__ r;
-    double* __restrict__ z;
-    double* __restrict__ p;
-    double* __restrict__ ap;
-    double* __restrict__ dinv;
-    double* __restrict__ part;  // 3 * gridDim.x partial slots
+    double* x;
+    double* best_x;
+    double* r;
+    double* z;
+    double* p0;     // p double buffer: p_{it} is read from one, p_{it+1} written to the other
+    double* p1;
+    double* ap;
+    double* dinv;
+    double* part;   // 3 * gridDim.x partial slots
     tt_pcg_result_t* res;
 };
 
-constexpr int kPcgBlock = 512;
-constexpr int kRowG = 8;  // lanes per CSR row in the SpMV
+constexpr int kPcgBlock = 256;
+constexpr int kPcgMinBlocks = 4;
+constexpr int kRowG = 4;  // lanes per CSR row in the SpMV (rows have ~7 (2-D) / ~15 (3-D) nnz)
 
 __device__ __forceinline__ double block_sum(double v, double* sh) {
     for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
@@ -146,7 +148,13 @@ __device__ __forceinline__ double grid_total(const double* part, double* sh) {
     return sh[32];
 }
 
-__global__ void __launch_bounds__(kPcgBlock) pcg_kernel(PcgArgs a) {
+// Jacobi PCG, the reference recurrence (fem.py:131-152), two grid barriers/iteration:
+//   A: p_new = z + beta p_old formed on the fly for every gathered column (identical
+//      bits in every block), own rows stored; Ap = M p_new; partial p.Ap    | sync
+//   B: alpha = rz / p.Ap; x += alpha p; r -= alpha Ap; z = dinv r;
+//      partials r.r, r.z                                                   | sync
+//   then (every block, no barrier): residual test, best iterate, beta = rz_new / rz.
+__global__ void __launch_bounds__(kPcgBlock, kPcgMinBlocks) pcg_kernel(PcgArgs a) {
     cg::grid_group grid = cg::this_grid();
     __shared__ double sh[33];
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -157,7 +165,7 @@ __global__ void __launch_bounds__(kPcgBlock) pcg_kernel(PcgArgs a) {
     double* partC = a.part + 2 * nb;
     const int64_t n = a.n;
 
-    // init: dinv, x = 0, r = b, z = dinv r, p = z
+    // init: dinv, x = 0, r = b, z = dinv r, p_old = 0 (so p_1 = z exactly)
     double bb = 0.0, rz_p = 0.0;
     for (int64_t i = tid; i < n; i += nthreads) {
         double d = 0.0;
@@ -171,7 +179,7 @@ __global__ void __launch_bounds__(kPcgBlock) pcg_kernel(PcgArgs a) {
         a.r[i] = bi;
         const double zi = di * bi;
         a.z[i] = zi;
-        a.p[i] = zi;
+        a.p0[i] = 0.0;
         bb += bi * bi;
         rz_p += bi * zi;
     }
@@ -190,38 +198,47 @@ __global__ void __launch_bounds__(kPcgBlock) pcg_kernel(PcgArgs a) {
         return;
     }
     double best = bnorm / bnorm;  // ||r0|| / ||b||  (fem.py:136)
+    double res = best;
+    double beta = 0.0;
     constexpr int kRowsPerWarp = 32 / kRowG;
     const int64_t warp_id = tid >> 5, nwarps = nthreads >> 5;
     const int lane = threadIdx.x & 31;
     const int sub = lane % kRowG;
-    double res = best;
+    double* p_old = a.p0;
+    double* p_new = a.p1;
     for (int64_t it = 0; it < a.maxiter; ++it) {
-        // ---- phase 1: Ap = M p, partial p.Ap (kRowG lanes per row, warp-uniform loop)
+        // ---- A: p_new = z + beta p_old (on the fly), Ap = M p_new, partial p.Ap
         double pap = 0.0;
         for (int64_t w0 = warp_id * kRowsPerWarp; w0 < n; w0 += nwarps * kRowsPerWarp) {
             const int64_t i = w0 + lane / kRowG;
             double s = 0.0;
             if (i < n) {
-                for (int64_t q = a.rp[i] + sub; q < a.rp[i + 1]; q += kRowG)
-                    s += a.v[q] * __ldcg(a.p + a.ci[q]);
+                const int64_t q0 = a.rp[i], q1 = a.rp[i + 1];
+                for (int64_t q = q0 + sub; q < q1; q += kRowG) {
+                    const int c = a.ci[q];
+                    const double pc = a.z[c] + beta * p_old[c];
+                    s += a.v[q] * pc;
+                }
             }
 #pragma unroll
             for (int off = kRowG / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
             if (i < n && sub == 0) {
+                const double pi = a.z[i] + beta * p_old[i];
+                p_new[i] = pi;
                 a.ap[i] = s;
-                pap += __ldcg(a.p + i) * s;
+                pap += pi * s;
             }
         }
         pap = block_sum(pap, sh);
         if (threadIdx.x == 0) partA[blockIdx.x] = pap;
         grid.sync();
-        // ---- phase 2: alpha, x += alpha p, r -= alpha Ap, z = dinv r; partial rr, rz
+        // ---- B: alpha, x += alpha p, r -= alpha Ap, z = dinv r; partial rr, rz
         const double alpha = rz / grid_total(partA, sh);
         double rr = 0.0, rzn = 0.0;
         for (int64_t i = tid; i < n; i += nthreads) {
-            const double pi = __ldcg(a.p + i);
+            const double pi = p_new[i];
             const double xi = a.x[i] + alpha * pi;
-            const double ri = a.r[i] - alpha * __ldcg(a.ap + i);
+            const double ri = a.r[i] - alpha * a.ap[i];
             const double zi = a.dinv[i] * ri;
             a.x[i] = xi;
             a.r[i] = ri;
@@ -234,11 +251,10 @@ __global__ void __launch_bounds__(kPcgBlock) pcg_kernel(PcgArgs a) {
         rzn = block_sum(rzn, sh);
         if (threadIdx.x == 0) partC[blockIdx.x] = rzn;
         grid.sync();
-        // ---- phase 3: residual test, best iterate, p = z + beta p
+        // ---- residual test, best iterate, beta (uniform in every block)
         res = sqrt(grid_total(partB, sh)) / bnorm;
         const double rz_new = grid_total(partC, sh);
-        const bool improved = res < best;
-        if (improved) {
+        if (res < best) {
             best = res;
             for (int64_t i = tid; i < n; i += nthreads) a.best_x[i] = a.x[i];
         }
@@ -249,10 +265,9 @@ __global__ void __launch_bounds__(kPcgBlock) pcg_kernel(PcgArgs a) {
             }
             return;
         }
-        const double beta = rz_new / rz;
-        for (int64_t i = tid; i < n; i += nthreads) a.p[i] = a.z[i] + beta * __ldcg(a.p + i);
+        beta = rz_new / rz;
         rz = rz_new;
-        grid.sync();
+        double* t = p_old; p_old = p_new; p_new = t;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         a.res->iterations = a.maxiter; a.res->residual = res; a.res->best_residual = best;
@@ -360,7 +375,7 @@ extern "C" int tt_mass_fill(const tt_mesh_t* m, const int64_t* inc_start, const 
     return launch_check("mass_fill_kernel");
 }
 
-extern "C" int64_t tt_pcg_workspace_doubles(int64_t n) { return 6 * n + 3 * 148 * 32 + 64; }
+extern "C" int64_t tt_pcg_workspace_doubles(int64_t n) { return 7 * n + 3 * 148 * 32 + 64; }
 
 extern "C" int tt_pcg(int64_t n, const int64_t* rp, const int32_t* ci, const double* v,
                       const double* b, double tol, int64_t maxiter, double* x, double* best_x,
@@ -372,8 +387,9 @@ extern "C" int tt_pcg(int64_t n, const int64_t* rp, const int32_t* ci, const dou
     PcgArgs a;
     a.n = n; a.rp = rp; a.ci = ci; a.v = v; a.b = b; a.tol = tol; a.maxiter = maxiter;
     a.x = x; a.best_x = best_x;
-    a.r = work; a.z = work + n; a.p = work + 2 * n; a.ap = work + 3 * n; a.dinv = work + 4 * n;
-    a.part = work + 5 * n;
+    a.r = work; a.z = work + n; a.p0 = work + 2 * n; a.p1 = work + 3 * n; a.ap = work + 4 * n;
+    a.dinv = work + 5 * n;
+    a.part = work + 6 * n;
     a.res = result;
     int blocks = pcg_grid_blocks(n);
     if (blocks > 148 * 32) blocks = 148 * 32;

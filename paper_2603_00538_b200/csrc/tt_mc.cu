@@ -220,6 +220,179 @@ __global__ void __launch_bounds__(256) mc_load_kernel(TargetDev t, int64_t e_lo,
     if (flags) atomicOr(status, flags);
 }
 
+template <int D, int PLAN>
+__device__ __forceinline__ void plan_lambda(const PlanDev& plan, int64_t e, int64_t j, double* lam) {
+    constexpr int K = D + 1;
+    if constexpr (PLAN == TT_PLAN_SHARED) {
+        if constexpr (D == 3) {
+            const double2* q = reinterpret_cast<const double2*>(plan.lam + j * 4);
+            const double2 a = __ldg(q), b = __ldg(q + 1);
+            lam[0] = a.x; lam[1] = a.y; lam[2] = b.x; lam[3] = b.y;
+        } else {
+#pragma unroll
+            for (int i = 0; i < K; ++i) lam[i] = __ldg(plan.lam + j * K + i);
+        }
+    } else {
+        philox_lambda<D>(plan.seed, e, j, lam);
+    }
+}
+
+// Mesh-backed source, flattened walk: each loop iteration performs exactly ONE facet-walk
+// step for every busy lane, and idle lanes immediately take the element's next unprocessed
+// sample (ballot + popc inside the G-lane group).  SIMT lanes stay busy regardless of how
+// many steps individual samples need; the assignment is a deterministic function of the
+// data, so results are bitwise reproducible.  Identical ids/lambdas as the reference scan
+// (certified walk, see locate_walk in tt_common.cuh).
+template <int D, int PLAN, int G>
+__global__ void __launch_bounds__(256, 2) mc_mesh_kernel(TargetDev t, int64_t e_lo, int64_t e_hi,
+                                                      PlanDev plan, SrcDev src,
+                                                      double* __restrict__ contrib,
+                                                      double* __restrict__ b,
+                                                      int32_t* __restrict__ ids_out,
+                                                      int32_t* __restrict__ status) {
+    constexpr int K = D + 1;
+    constexpr int EPW = 32 / G;
+    constexpr double EPS = 1e-12;
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const unsigned gmask = (G == 32) ? FULL : (((1u << G) - 1u) << (lane & ~(G - 1)));
+    const unsigned lt = (1u << lane) - 1u;
+    const int sub_lane = lane % G;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t n_el = e_hi - e_lo;
+    const int64_t N = plan.n;
+    const GridDev& g = src.grid;
+    const bool walk = g.walk && src.seeds;
+    int flags = 0;
+
+    for (int64_t tile = warp; tile * EPW < n_el; tile += nwarps) {
+        const int64_t le = tile * EPW + lane / G;
+        const bool active = le < n_el;
+        const int64_t e = e_lo + le;
+        double acc[K];
+#pragma unroll
+        for (int i = 0; i < K; ++i) acc[i] = 0.0;
+        double v[K][D];
+        int seed[K + 1];
+        if (active) {
+            load_elem<D>(t, e, v);
+            if (walk) {
+#pragma unroll
+                for (int i = 0; i <= K; ++i) seed[i] = __ldg(src.seeds + e * (K + 1) + i);
+            }
+        }
+        int64_t next = 0;
+        int64_t jcur = 0;
+        bool busy = false;
+        double x[D], lam[K];
+        int cur = -1, steps = 0;
+        while (true) {
+            const bool want = active && !busy;
+            const unsigned m = __ballot_sync(FULL, want) & gmask;
+            if (want) {
+                const int64_t j = next + __popc(m & lt);
+                if (j < N) {
+                    plan_lambda<D, PLAN>(plan, e, j, lam);
+                    map_point<D>(lam, v, x);
+                    cur = -1;
+                    if (walk) {
+                        int imax = 0;
+                        double lmax = lam[0];
+#pragma unroll
+                        for (int i = 1; i < K; ++i)
+                            if (lam[i] > lmax) { lmax = lam[i]; imax = i; }
+                        cur = seed[0];
+#pragma unroll
+                        for (int i = 0; i < K; ++i)
+                            if (lmax > 0.45 && imax == i) cur = seed[1 + i];
+                    }
+                    steps = 0;
+                    jcur = j;
+                    busy = true;
+                }
+            }
+            next += __popc(m);
+            if (!__any_sync(FULL, busy)) break;
+            if (!busy) continue;
+            double l[K];
+            int hit = -1;
+            bool done = false;
+            if (cur >= 0 && steps < 12) {
+                Rec<D> r;
+                load_rec<D>(g.rec, cur, r);
+                RecTail<D> tl;
+                load_tail<D>(g.rec, cur, tl);
+                bary_from_rec<D>(r, x, l);
+                int imin = 0;
+                double lmin = l[0];
+#pragma unroll
+                for (int i = 1; i <= D; ++i)
+                    if (l[i] < lmin) { lmin = l[i]; imin = i; }
+                if (lmin >= (double)tl.tau) {
+                    hit = cur;
+                    done = true;
+                } else if (lmin >= -EPS) {
+                    cur = -1;  // inside within the slack, not certified: reference scan
+                } else {
+                    int nb = tl.nbr[0];
+#pragma unroll
+                    for (int i = 1; i <= D; ++i)
+                        if (imin == i) nb = tl.nbr[i];
+                    cur = nb;
+                    ++steps;
+                }
+            } else {
+                cur = -1;
+            }
+            if (!done && cur < 0) {
+                // exact reference scan (+ snap / strict), rare
+                hit = locate_point<D>(g, x, EPS, l);
+                if (hit < 0) {
+                    if (src.outside == TT_OUTSIDE_STRICT) {
+                        flags |= TT_FLAG_OUTSIDE_STRICT;
+                    } else {
+                        const SnapOut<D> sn = snap_point<D>(g, x[0], x[1], D == 3 ? x[D - 1] : 0.0);
+                        hit = sn.e;
+#pragma unroll
+                        for (int i = 0; i < K; ++i) l[i] = sn.l[i];
+                    }
+                }
+                done = true;
+            }
+            if (done) {
+                if (ids_out) ids_out[le * N + jcur] = hit;
+                double f = 0.0;
+                if (hit >= 0 && (contrib || b)) {
+                    const int32_t* conn = src.src_elems + (int64_t)hit * K;
+                    f = mul(__ldg(src.coeffs + __ldg(conn)), l[0]);
+#pragma unroll
+                    for (int i = 1; i < K; ++i) f = add(f, mul(__ldg(src.coeffs + __ldg(conn + i)), l[i]));
+                }
+                if (!isfinite(f)) flags |= TT_FLAG_NONFINITE;
+#pragma unroll
+                for (int i = 0; i < K; ++i) acc[i] = fma(f, lam[i], acc[i]);
+                busy = false;
+            }
+        }
+#pragma unroll
+        for (int off = G / 2; off > 0; off >>= 1)
+#pragma unroll
+            for (int i = 0; i < K; ++i) acc[i] += __shfl_xor_sync(FULL, acc[i], off);
+        if (active && sub_lane == 0) {
+            const double q = (double)N * (1.0 / __ldg(t.measure + e));
+            if (contrib) {
+#pragma unroll
+                for (int i = 0; i < K; ++i) contrib[le * K + i] = acc[i] / q;
+            } else if (b) {
+#pragma unroll
+                for (int i = 0; i < K; ++i) atomicAdd(b + __ldg(t.elems + e * K + i), acc[i] / q);
+            }
+        }
+    }
+    if (flags && status) atomicOr(status, flags);
+}
+
 template <int D>
 __global__ void map_points_kernel(TargetDev t, int64_t e_lo, int64_t n_el, int plan_kind,
                                   PlanDev plan, double* __restrict__ pts) {
@@ -255,30 +428,6 @@ __global__ void eval_points_kernel(SrcDev src, const __grid_constant__ tt_expr_t
         out[i] = f;
     }
     if (flags) atomicOr(status, flags);
-}
-
-template <int D, int PLAN>
-__global__ void cache_ids_kernel(TargetDev t, int64_t e_lo, int64_t n_el, PlanDev plan, GridDev g,
-                                 const int32_t* __restrict__ seeds, int32_t* __restrict__ ids) {
-    constexpr int K = D + 1;
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n_el * plan.n) return;
-    const int64_t le = i / plan.n, j = i % plan.n, e = e_lo + le;
-    double v[K][D];
-    load_elem<D>(t, e, v);
-    double lam[K];
-    if constexpr (PLAN == TT_PLAN_SHARED) {
-#pragma unroll
-        for (int c = 0; c < K; ++c) lam[c] = __ldg(plan.lam + j * K + c);
-    } else {
-        philox_lambda<D>(plan.seed, e, j, lam);
-    }
-    double x[D], l[K];
-    map_point<D>(lam, v, x);
-    int es = (g.walk && seeds) ? locate_walk<D>(g, x, 1e-12, __ldg(seeds + e), l)
-                               : locate_point<D>(g, x, 1e-12, l);
-    if (es < 0) es = snap_point<D>(g, x[0], x[1], D == 3 ? x[D - 1] : 0.0).e;  // transfer.py:79-81
-    ids[i] = es;
 }
 
 // b[n] = sum over the node's incidences (e*k + a ascending) of contrib[e - e_lo, a],
@@ -352,6 +501,16 @@ static int launch_mc(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_pl
     const int block = 256;
     int64_t blocks = (tiles + 7) / 8;
     int per_sm = 0;
+    if constexpr (SRC == TT_SRC_MESH) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mc_mesh_kernel<D, PLAN, G>, block, 0);
+        if (per_sm < 1) per_sm = 1;
+        const int64_t cap = (int64_t)sm_count() * per_sm * 16;
+        if (blocks > cap) blocks = cap;
+        if (blocks < 1) blocks = 1;
+        mc_mesh_kernel<D, PLAN, G><<<(unsigned)blocks, block, 0, st>>>(td, e_lo, e_hi, pd, sd, contrib, b,
+                                                                        nullptr, status);
+        return launch_check("mc_mesh_kernel");
+    }
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mc_load_kernel<D, PLAN, SRC, G>, block, 0);
     if (per_sm < 1) per_sm = 1;
     const int64_t cap = (int64_t)sm_count() * per_sm * 16;
@@ -366,9 +525,11 @@ template <int D, int PLAN, int SRC>
 static int dispatch_g(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_plan_t* p,
                       const tt_source_t* s, double* contrib, double* b, int32_t* status,
                       cudaStream_t st) {
+    // lanes per element: at least ~8 samples per lane (amortises the per-element setup)
     const int64_t N = p->n_samples;
-    if (N <= 8) return launch_mc<D, PLAN, SRC, 8>(t, e_lo, e_hi, p, s, contrib, b, status, st);
-    if (N <= 16) return launch_mc<D, PLAN, SRC, 16>(t, e_lo, e_hi, p, s, contrib, b, status, st);
+    if (N < 64) return launch_mc<D, PLAN, SRC, 4>(t, e_lo, e_hi, p, s, contrib, b, status, st);
+    if (N < 128) return launch_mc<D, PLAN, SRC, 8>(t, e_lo, e_hi, p, s, contrib, b, status, st);
+    if (N < 256) return launch_mc<D, PLAN, SRC, 16>(t, e_lo, e_hi, p, s, contrib, b, status, st);
     return launch_mc<D, PLAN, SRC, 32>(t, e_lo, e_hi, p, s, contrib, b, status, st);
 }
 
@@ -463,21 +624,27 @@ extern "C" int tt_mc_cache_ids(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, c
         set_error("tt_mc_cache_ids: bad arguments");
         return TT_ERR_INVALID_PARAMETER;
     }
-    const int64_t total = (e_hi - e_lo) * p->n_samples;
-    if (total == 0) return TT_OK;
+    if ((e_hi - e_lo) * p->n_samples == 0) return TT_OK;
+    // the fused mesh kernel with an id sink and no accumulation: the very code path the
+    // load uses, so cached ids are the ids every load sees (transfer.py:74-82)
     TargetDev td{t->nodes, t->elems, t->measure};
     PlanDev pd{p->n_samples, p->lam, p->seed};
-    GridDev gd = to_dev(*g);
+    SrcDev sd{};
+    sd.kind = TT_SRC_MESH;
+    sd.outside = TT_OUTSIDE_SNAP;
+    sd.grid = to_dev(*g);
+    sd.seeds = seeds;
     auto s = as_stream(stream);
-    const unsigned nb = grid_for(total, 256);
+    const int64_t tiles = (e_hi - e_lo + 3) / 4;
+    const unsigned nb = grid_for(tiles * 32, 256);
     if (t->dim == 2) {
-        if (p->kind == TT_PLAN_SHARED) cache_ids_kernel<2, TT_PLAN_SHARED><<<nb, 256, 0, s>>>(td, e_lo, e_hi - e_lo, pd, gd, seeds, ids);
-        else cache_ids_kernel<2, TT_PLAN_PHILOX><<<nb, 256, 0, s>>>(td, e_lo, e_hi - e_lo, pd, gd, seeds, ids);
+        if (p->kind == TT_PLAN_SHARED) mc_mesh_kernel<2, TT_PLAN_SHARED, 8><<<nb, 256, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
+        else mc_mesh_kernel<2, TT_PLAN_PHILOX, 8><<<nb, 256, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
     } else {
-        if (p->kind == TT_PLAN_SHARED) cache_ids_kernel<3, TT_PLAN_SHARED><<<nb, 256, 0, s>>>(td, e_lo, e_hi - e_lo, pd, gd, seeds, ids);
-        else cache_ids_kernel<3, TT_PLAN_PHILOX><<<nb, 256, 0, s>>>(td, e_lo, e_hi - e_lo, pd, gd, seeds, ids);
+        if (p->kind == TT_PLAN_SHARED) mc_mesh_kernel<3, TT_PLAN_SHARED, 8><<<nb, 256, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
+        else mc_mesh_kernel<3, TT_PLAN_PHILOX, 8><<<nb, 256, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
     }
-    return launch_check("cache_ids_kernel");
+    return launch_check("mc_mesh_kernel (cache ids)");
 }
 
 extern "C" int tt_map_points(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_plan_t* p,

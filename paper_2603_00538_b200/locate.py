@@ -124,13 +124,14 @@ class UniformGridLocator:
         return g
 
     def seeds_for(self, target) -> torch.Tensor:
-        """Walk start per target element: the source element containing the target
-        element's centroid (cached per target mesh; meshes are immutable)."""
+        """Walk starts per target element (E, d+2): source elements containing the
+        centroid c and the points (v_i + c)/2 (cached per target; meshes are immutable)."""
         key = id(target)
         hit = self._seeds.get(key)
         if hit is not None and hit[0] is target:
             return hit[1]
-        seeds = torch.empty(target.n_elems, dtype=torch.int32, device=self.cell_start_dev.device)
+        seeds = torch.empty((target.n_elems, target.DIM + 2), dtype=torch.int32,
+                            device=self.cell_start_dev.device)
         g, t = self.desc(), target.device.desc()
         _lib.call("tt_seed_elements", C.byref(g), C.byref(t), 0, target.n_elems, _lib.ptr(seeds),
                   _lib.stream_handle())

@@ -385,10 +385,22 @@ def _walk_vs_scan(tt, tgt, src, n, dim, mode="sobol"):
     ls = tt.UniformGridLocator.build(src, walk=False)
     bw = tt.assemble_load_mc(tgt, tt.MeshBackedField(fs, lw), plan)
     bs = tt.assemble_load_mc(tgt, tt.MeshBackedField(fs, ls), plan)
-    assert np.array_equal(bw, bs)          # same ids + same lambdas -> bitwise b
+    # same ids and lambdas; only the per-lane summation order may differ
+    assert _rel(bw, bs) <= 1e-14
+    # ids through the fused kernel's own code path (walk) vs the reference scan
     ow = tt.MCTransferOperator(tgt, src, plan, source_locator=lw)
     os_ = tt.MCTransferOperator(tgt, src, plan, source_locator=ls)
-    assert np.array_equal(ow.src_elem_dev.cpu().numpy(), os_.src_elem_dev.cpu().numpy())
+    iw, is_ = ow.src_elem_dev.cpu().numpy(), os_.src_elem_dev.cpu().numpy()
+    assert np.array_equal(iw, is_)
+    # and vs the oracle scan on the materialised sample points
+    from paper_2603_00538_b200.montecarlo import map_points
+    g = O.Grid(src.nodes, src.elements)
+    pts = map_points(tgt, plan, 0, min(tgt.n_elems, 300)).cpu().numpy().reshape(-1, dim)
+    eo, _ = g.locate_many(pts)
+    out = np.flatnonzero(eo < 0)
+    for i in out[:200]:
+        eo[i] = g.nearest_element(pts[i])
+    assert np.array_equal(iw[:min(tgt.n_elems, 300)].ravel()[:len(eo)][eo >= 0], eo[eo >= 0])
 
 
 def test_walk_equals_reference_scan_2d(tt, golden, c1):
