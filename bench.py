@@ -167,8 +167,9 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     tgt, src, fs, loc, mass = build_problem(args, tt)
     box = tt.MeshBackedField(fs, loc)
+    from paper_2603_00538_b200.dist import partition_elements, reduce_load
     E = tgt.n_elems
-    e_lo, e_hi = E * rank // world, E * (rank + 1) // world
+    e_lo, e_hi = partition_elements(E, world, rank)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
     status = _lib.status_word()
 
@@ -178,8 +179,7 @@ def run_ours(args):
         b = load_vector(tgt, box, plan, e_lo, e_hi, deterministic=True, check=False, status=status)
         if ev is not None:
             ev[1].record()
-        if world > 1:
-            dist.all_reduce(b)
+        reduce_load(b)                      # NCCL all-reduce of the partial b (N>1)
         x, best_x, res = pcg_device(mass, b, tol=1e-12)
         return x, res
 
@@ -258,8 +258,7 @@ def run_ours(args):
         c_dev.copy_(c_host, non_blocking=True)
         field = tt.NodalField(src, c_dev)
         b = load_vector(tgt, tt.MeshBackedField(field, loc), plan, e_lo, e_hi)
-        if world > 1:
-            dist.all_reduce(b)
+        reduce_load(b)
         xx = tt.cg_solve(mass, b, tol=1e-12)
         x_host.copy_(xx, non_blocking=True)
         torch.cuda.current_stream().synchronize()
