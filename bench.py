@@ -297,7 +297,7 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args, tgt, src, fs, seconds=args.cpu_seconds)
+        cpu = cpu_baseline(args, tgt, src, fs.coeffs, seconds=args.cpu_seconds)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
@@ -327,40 +327,36 @@ def run_ours(args):
 
 
 # --------------------------------------------------------------------- CPU
-def cpu_baseline(args, tgt, src, fs, seconds=12.0):
-    """The oracle restatement (numpy, 3-D) on a bounded sample of the same workload."""
+def cpu_baseline(args, tgt, src, coeffs, seconds=12.0):
+    """The reference MC load restated in C/OpenMP (oracle/c, all host cores) on a bounded
+    sample of the same workload: grid built by the oracle (untimed setup), then as many
+    512-element chunks as fit in ``seconds``."""
     import numpy as np
     sys.path.insert(0, str(ROOT / "oracle"))
     import tt_oracle as O
+    import tt_oracle_c as OC
     t0 = time.perf_counter()
     g = O.Grid(src.nodes, src.elements)
     setup_s = time.perf_counter() - t0
     lam = O.bary_map(O.sobol(args.samples, 3))
-    coeffs = np.asarray(fs.coeffs)
-    srcf = lambda P: O.mesh_backed_eval(g, coeffs, P)  # noqa: E731
-    area = tgt.elem_areas
+    coeffs = np.asarray(coeffs)
     threads = os.cpu_count() or 1
-    n_el, done, t_used = 256, 0, 0.0
+    OC.mc_load_mesh(g, coeffs, tgt.nodes, tgt.elements, tgt.elem_areas, lam, 0, 512, threads)  # warm
+    n_el, done, t_used = 4096, 0, 0.0
     while t_used < seconds and done < tgt.n_elems:
         lo, hi = done, min(done + n_el, tgt.n_elems)
         t = time.perf_counter()
-        sub = tgt.elements[lo:hi]
-        bounds = [(a, min(a + O.CHUNK, hi - lo)) for a in range(0, hi - lo, O.CHUNK)]
-        from concurrent.futures import ThreadPoolExecutor
-
-        def run(b):
-            return O.accumulate(tgt.nodes, sub, area[lo:hi], lam, srcf, b)
-        with ThreadPoolExecutor(max_workers=threads) as ex:
-            list(ex.map(run, bounds))
+        OC.mc_load_mesh(g, coeffs, tgt.nodes, tgt.elements, tgt.elem_areas, lam, lo, hi, threads)
         t_used += time.perf_counter() - t
         done = hi
-        n_el = min(n_el * 2, 65536)
+        n_el = min(n_el * 2, 262144)
     sps = done * args.samples / t_used
     return {"value": sps, "unit": "samples/s", "cores": threads, "kind": "port",
-            "sample": f"oracle 3-D MC load on the first {done} of {tgt.n_elems} target elements, "
-                      f"N={args.samples} ({done * args.samples} samples, {t_used:.1f} s); "
+            "sample": f"MC load (locate+snap+P1 eval+accumulate) on target elements [0, {done}) of "
+                      f"{tgt.n_elems}, N={args.samples}: {done * args.samples} samples in {t_used:.1f} s; "
                       f"grid setup {setup_s:.1f} s untimed",
-            "impl": "oracle/tt_oracle.py (numpy restatement; reference is 2-D only)"}
+            "impl": "oracle/c/tt_oracle_c.c: C/OpenMP restatement of the reference MC path "
+                    "(the reference itself is 2-D only); -O2, no FMA, 512-element chunks"}
 
 
 def run_reference(args):
@@ -375,9 +371,8 @@ def run_reference(args):
     tgt = M.generate_cube_mesh(args.n, 0.2, seed=20, split="kuhn")
     src = M.generate_cube_mesh(args.n, 0.2, seed=10, split="kuhn_mirror")
 
-    class _F:
-        coeffs = np.sin(src.nodes[:, 0]) * np.cos(src.nodes[:, 1]) * np.cos(src.nodes[:, 2]) + 2
-    cpu = cpu_baseline(args, tgt, src, _F, seconds=args.cpu_seconds)
+    coeffs = np.sin(src.nodes[:, 0]) * np.cos(src.nodes[:, 1]) * np.cos(src.nodes[:, 2]) + 2
+    cpu = cpu_baseline(args, tgt, src, coeffs, seconds=args.cpu_seconds)
     # the PCG on the full target mesh (scipy CSR, the reference's solver) once
     t = time.perf_counter()
     Mm = O.mass_matrix(tgt.n_nodes, tgt.elements, tgt.elem_areas, 3)

@@ -1,0 +1,70 @@
+"""ctypes wrapper of oracle/c/tt_oracle_c.c -- TEST / BASELINE INFRASTRUCTURE ONLY.
+
+The C/OpenMP port of the reference MC load is the CPU baseline of bench.py (it is
+faster than the numpy restatement, so the reported GPU/CPU ratio is conservative).
+Built on first use with gcc into oracle/_build/ (git-ignored; travels with gpurun).
+"""
+
+import ctypes as C
+import os
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+SRC = HERE / "c" / "tt_oracle_c.c"
+LIB = HERE / "_build" / "libtt_oracle_c.so"
+_lib = None
+
+
+def build(force=False):
+    if force or not LIB.exists() or LIB.stat().st_mtime < SRC.stat().st_mtime:
+        LIB.parent.mkdir(exist_ok=True)
+        tmp = LIB.with_suffix(f".{os.getpid()}.tmp")
+        subprocess.run(["gcc", "-O2", "-fopenmp", "-ffp-contract=off", "-fPIC", "-shared",
+                        str(SRC), "-o", str(tmp), "-lm"], check=True)
+        os.replace(tmp, LIB)
+    return LIB
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = C.CDLL(str(build()))
+        _lib.tto_mc_load_mesh.restype = C.c_int64
+        _lib.tto_mc_load_mesh.argtypes = [C.c_int] + [C.c_void_p] * 3 + [C.c_int64] * 3 + \
+            [C.c_void_p] * 11 + [C.c_double, C.c_void_p, C.c_int]
+    return _lib
+
+
+def _p(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def mc_load_mesh(grid, coeffs, t_nodes, t_elems, t_measure, lam, e_lo=0, e_hi=None,
+                 threads=None, eps=1e-12):
+    """Element contributions (e_hi-e_lo, k) of a mesh-backed source; ``grid`` is an
+    oracle ``tt_oracle.Grid``.  Returns (contrib, n_outside)."""
+    d = grid.dim
+    k = d + 1
+    e_hi = len(t_elems) if e_hi is None else e_hi
+    arrs = dict(
+        t_nodes=np.ascontiguousarray(t_nodes, np.float64), t_elems=np.ascontiguousarray(t_elems, np.int32),
+        t_measure=np.ascontiguousarray(t_measure, np.float64), lam=np.ascontiguousarray(lam, np.float64),
+        s_elems=np.ascontiguousarray(grid.elems, np.int32), coeffs=np.ascontiguousarray(coeffs, np.float64),
+        dims=np.array(grid.dims, np.int32), lo=np.zeros(3), hi=np.ones(3),
+        cs=np.ascontiguousarray(grid.cell_start, np.int64), ce=np.ascontiguousarray(grid.cell_elems, np.int32),
+        binv=np.ascontiguousarray(grid.binv, np.float64), origin=np.ascontiguousarray(grid.origin, np.float64),
+        cent=np.ascontiguousarray(grid.centroids, np.float64))
+    arrs["lo"][:d], arrs["hi"][:d] = grid.lo, grid.hi
+    out = np.empty((e_hi - e_lo, k))
+    a = arrs
+    n_out = lib().tto_mc_load_mesh(d, _p(a["t_nodes"]), _p(a["t_elems"]), _p(a["t_measure"]), e_lo, e_hi,
+                                   len(lam), _p(a["lam"]), _p(a["s_elems"]), _p(a["coeffs"]),
+                                   _p(a["dims"]), _p(a["lo"]), _p(a["hi"]), _p(a["cs"]), _p(a["ce"]),
+                                   _p(a["binv"]), _p(a["origin"]), _p(a["cent"]), eps, _p(out),
+                                   int(threads or os.cpu_count() or 1))
+    if n_out < 0:
+        raise FloatingPointError("SourceEvalFailed: non-finite source value")
+    return out, int(n_out)

@@ -169,3 +169,22 @@ def test_3d_oracle_properties():
     M = O.mass_matrix(len(nodes), elems, vol, 3)
     assert np.allclose(M.sum(), 1.0, atol=1e-14)
     assert abs(M - M.T).max() == 0.0
+
+
+def test_c_port_matches_reference_golden(golden):
+    """The C/OpenMP port (bench.py's CPU baseline) reproduces the reference load."""
+    import tt_oracle_c as OC
+    g = O.Grid(golden["c1s_nodes"], golden["c1s_elements"])
+    tn, te = golden["c1t_nodes"], golden["c1t_elements"]
+    c, n_out = OC.mc_load_mesh(g, golden["c1s_coeffs"], tn, te, np.abs(O.signed_measure(tn, te)),
+                               golden["plan_sobol1600_bary"], threads=4)
+    b = O.reduce_to_nodes(len(tn), te, c)
+    ref = golden["b_c1_mesh_smooth"]
+    assert n_out == 0 and np.max(np.abs(b - ref)) <= 1e-14 * np.max(np.abs(ref))
+    g2 = O.Grid(golden["curv_nodes"], golden["curv_elements"])
+    tn2, te2 = golden["curvt_nodes"], golden["curvt_elements"]
+    c2, n2 = OC.mc_load_mesh(g2, golden["curv_coeffs"], tn2, te2, np.abs(O.signed_measure(tn2, te2)),
+                             O.bary_map(O.sobol(256, 2)), threads=2)
+    assert n2 == int(golden["curv_n_outside"])
+    b2 = O.reduce_to_nodes(len(tn2), te2, c2)
+    assert np.max(np.abs(b2 - golden["b_curv_snap"])) <= 1e-14 * np.max(np.abs(golden["b_curv_snap"]))
