@@ -176,6 +176,7 @@ def run_ours(args):
     def step(plan, ev=None):
         if ev is not None:
             ev[0].record()
+        fs._packed = None   # a coupling step brings new coefficients: repack them (timed)
         b = load_vector(tgt, box, plan, e_lo, e_hi, deterministic=True, check=False, status=status)
         if ev is not None:
             ev[1].record()
@@ -319,7 +320,7 @@ def run_ours(args):
             "sweep": sweep,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
-            "gpu_launches": 3 * args.steps,
+            "gpu_launches": 4 * args.steps,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

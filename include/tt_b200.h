@@ -153,6 +153,8 @@ typedef struct tt_source {
     const int32_t* cached_ids;/* TT_SRC_CACHED (e_hi - e_lo, N) source element per sample */
     const int32_t* seeds;     /* TT_SRC_MESH optional (E_target, dim+2) walk start elements
                                  per target element (tt_seed_elements), or NULL */
+    const double*  elem_coeffs;/* TT_SRC_MESH/CACHED optional (E_s, 4) per-element vertex
+                                 coefficients (tt_pack_coeffs); replaces src_elems+coeffs */
 } tt_source_t;
 
 typedef struct tt_pcg_result {
@@ -228,6 +230,10 @@ int tt_mc_load(const tt_mesh_t* target, int64_t e_lo, int64_t e_hi, const tt_pla
 int tt_mc_cache_ids(const tt_mesh_t* target, int64_t e_lo, int64_t e_hi, const tt_plan_t* plan,
                     const tt_grid_t* grid, const int32_t* seeds /* (E_target, dim+2) or NULL */,
                     int32_t* ids /* (e_hi-e_lo, N): located or snapped */, void* stream);
+
+/* out[e*4 + i] = coeffs[elems[e*k + i]] (i < k, zero padded): one aligned 32-byte record
+ * per source element, gathered once per coefficient update. */
+int tt_pack_coeffs(const tt_mesh_t* src, const double* coeffs, double* out, void* stream);
 
 /* ---- node reduction / incidence (deterministic np.add.at order) ---- */
 int tt_incidence_count(const tt_mesh_t* mesh, int64_t* inc_start /* (n_nodes+1) */,

@@ -62,7 +62,7 @@ class tt_source_t(C.Structure):
     _fields_ = [("kind", C.c_int32), ("outside", C.c_int32), ("dim", C.c_int32),
                 ("reserved", C.c_int32), ("expr", tt_expr_t), ("grid", tt_grid_t),
                 ("src_elems", C.c_void_p), ("coeffs", C.c_void_p), ("values", C.c_void_p),
-                ("cached_ids", C.c_void_p), ("seeds", C.c_void_p)]
+                ("cached_ids", C.c_void_p), ("seeds", C.c_void_p), ("elem_coeffs", C.c_void_p)]
 
 
 class tt_pcg_result_t(C.Structure):
@@ -101,6 +101,7 @@ _SIGNATURES = {
                     C.POINTER(tt_source_t), _P, _P, _P, _P], _I),
     "tt_mc_cache_ids": ([C.POINTER(tt_mesh_t), _I64, _I64, C.POINTER(tt_plan_t),
                          C.POINTER(tt_grid_t), _P, _P, _P], _I),
+    "tt_pack_coeffs": ([C.POINTER(tt_mesh_t), _P, _P, _P], _I),
     "tt_incidence_count": ([C.POINTER(tt_mesh_t), _P, _P], _I),
     "tt_incidence_fill": ([C.POINTER(tt_mesh_t), _P, _P, _P, _P], _I),
     "tt_reduce_nodes": ([_I64, _I, _P, _P, _I64, _I64, _P, _P, _P], _I),

@@ -11,6 +11,7 @@
 #include <stdint.h>
 #include <stdio.h>
 #include <string.h>
+#include <stdlib.h>
 #include "../../include/tt_b200.h"
 
 #define TT_HD __host__ __device__ __forceinline__

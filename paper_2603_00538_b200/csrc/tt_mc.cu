@@ -29,6 +29,7 @@ struct SrcDev {
     const double* __restrict__ values;
     const int32_t* __restrict__ cached;
     const int32_t* __restrict__ seeds;
+    const double* __restrict__ ecoef;
 };
 
 template <int D>
@@ -62,6 +63,28 @@ __device__ __forceinline__ double eval_expr(const tt_expr_t& p, const double* x)
     return sp > 0 ? st[0] : 0.0;
 }
 
+// P1 evaluation sum_i c_i lambda_i at source element e: from the packed per-element
+// coefficient record when present (one aligned 32 B load), else conn + coeff gathers.
+template <int D>
+__device__ __forceinline__ double p1_eval(const SrcDev& s, int e, const double* l) {
+    constexpr int K = D + 1;
+    double c[K];
+    if (s.ecoef) {
+        const double2* q = reinterpret_cast<const double2*>(s.ecoef + (int64_t)e * 4);
+        const double2 a = __ldg(q), b = __ldg(q + 1);
+        c[0] = a.x; c[1] = a.y; c[2] = b.x;
+        if constexpr (D == 3) c[3] = b.y;
+    } else {
+        const int32_t* conn = s.src_elems + (int64_t)e * K;
+#pragma unroll
+        for (int i = 0; i < K; ++i) c[i] = __ldg(s.coeffs + __ldg(conn + i));
+    }
+    double f = mul(c[0], l[0]);
+#pragma unroll
+    for (int i = 1; i < K; ++i) f = add(f, mul(c[i], l[i]));
+    return f;
+}
+
 // MeshBackedField.__call__ (montecarlo.py:49-65) + eval_in_elements (fem.py:36-38)
 template <int D>
 __device__ __forceinline__ double eval_mesh(const SrcDev& s, const double* x, int& flags, int& guess) {
@@ -80,11 +103,7 @@ __device__ __forceinline__ double eval_mesh(const SrcDev& s, const double* x, in
 #pragma unroll
         for (int i = 0; i < K; ++i) l[i] = sn.l[i];
     }
-    const int32_t* conn = s.src_elems + (int64_t)e * K;
-    double f = mul(__ldg(s.coeffs + __ldg(conn)), l[0]);
-#pragma unroll
-    for (int i = 1; i < K; ++i) f = add(f, mul(__ldg(s.coeffs + __ldg(conn + i)), l[i]));
-    return f;
+    return p1_eval<D>(s, e, l);
 }
 
 // cached source element: lambda_s for ALL samples clipped >= 0 and renormalised
@@ -94,11 +113,7 @@ __device__ __forceinline__ double eval_cached(const SrcDev& s, const double* x, 
     constexpr int K = D + 1;
     double l[K];
     snap_lambda<D>(s.grid, e, x, l);
-    const int32_t* conn = s.src_elems + (int64_t)e * K;
-    double f = mul(__ldg(s.coeffs + __ldg(conn)), l[0]);
-#pragma unroll
-    for (int i = 1; i < K; ++i) f = add(f, mul(__ldg(s.coeffs + __ldg(conn + i)), l[i]));
-    return f;
+    return p1_eval<D>(s, e, l);
 }
 
 template <int D, int SRC>
@@ -243,8 +258,8 @@ __device__ __forceinline__ void plan_lambda(const PlanDev& plan, int64_t e, int6
 // many steps individual samples need; the assignment is a deterministic function of the
 // data, so results are bitwise reproducible.  Identical ids/lambdas as the reference scan
 // (certified walk, see locate_walk in tt_common.cuh).
-template <int D, int PLAN, int G>
-__global__ void __launch_bounds__(256, 2) mc_mesh_kernel(TargetDev t, int64_t e_lo, int64_t e_hi,
+template <int D, int PLAN, int G, bool SPEC, int MINB>
+__global__ void __launch_bounds__(256, MINB) mc_mesh_kernel(TargetDev t, int64_t e_lo, int64_t e_hi,
                                                       PlanDev plan, SrcDev src,
                                                       double* __restrict__ contrib,
                                                       double* __restrict__ b,
@@ -318,11 +333,20 @@ __global__ void __launch_bounds__(256, 2) mc_mesh_kernel(TargetDev t, int64_t e_
             double l[K];
             int hit = -1;
             bool done = false;
+            double2 pc0 = make_double2(0.0, 0.0), pc1 = make_double2(0.0, 0.0);
             if (cur >= 0 && steps < 12) {
                 Rec<D> r;
                 load_rec<D>(g.rec, cur, r);
                 RecTail<D> tl;
                 load_tail<D>(g.rec, cur, tl);
+                if constexpr (SPEC) {
+                    // speculative: the coefficient record of the element being tested
+                    if (src.ecoef) {
+                        const double2* q = reinterpret_cast<const double2*>(src.ecoef + (int64_t)cur * 4);
+                        pc0 = __ldg(q);
+                        pc1 = __ldg(q + 1);
+                    }
+                }
                 bary_from_rec<D>(r, x, l);
                 int imin = 0;
                 double lmin = l[0];
@@ -364,10 +388,14 @@ __global__ void __launch_bounds__(256, 2) mc_mesh_kernel(TargetDev t, int64_t e_
                 if (ids_out) ids_out[le * N + jcur] = hit;
                 double f = 0.0;
                 if (hit >= 0 && (contrib || b)) {
-                    const int32_t* conn = src.src_elems + (int64_t)hit * K;
-                    f = mul(__ldg(src.coeffs + __ldg(conn)), l[0]);
+                    if (SPEC && src.ecoef && hit == cur) {
+                        const double c[4] = {pc0.x, pc0.y, pc1.x, pc1.y};
+                        f = mul(c[0], l[0]);
 #pragma unroll
-                    for (int i = 1; i < K; ++i) f = add(f, mul(__ldg(src.coeffs + __ldg(conn + i)), l[i]));
+                        for (int i = 1; i < K; ++i) f = add(f, mul(c[i], l[i]));
+                    } else {
+                        f = p1_eval<D>(src, hit, l);
+                    }
                 }
                 if (!isfinite(f)) flags |= TT_FLAG_NONFINITE;
 #pragma unroll
@@ -430,6 +458,17 @@ __global__ void eval_points_kernel(SrcDev src, const __grid_constant__ tt_expr_t
     if (flags) atomicOr(status, flags);
 }
 
+__global__ void pack_coeffs_kernel(int64_t E, int k, const int32_t* __restrict__ elems,
+                                   const double* __restrict__ coeffs, double* __restrict__ out) {
+    int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= E) return;
+    double c[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int i = 0; i < k; ++i) c[i] = coeffs[elems[e * k + i]];
+    double2* o = reinterpret_cast<double2*>(out + e * 4);
+    o[0] = make_double2(c[0], c[1]);
+    o[1] = make_double2(c[2], c[3]);
+}
+
 // b[n] = sum over the node's incidences (e*k + a ascending) of contrib[e - e_lo, a],
 // starting from 0.0 -- exactly np.add.at's accumulation order (montecarlo.py:146).
 __global__ void reduce_nodes_kernel(int64_t n_nodes, int k, const int64_t* __restrict__ inc_start,
@@ -486,6 +525,7 @@ static SrcDev to_src(const tt_source_t& s) {
     d.values = s.values;
     d.cached = s.cached_ids;
     d.seeds = s.seeds;
+    d.ecoef = s.elem_coeffs;
     return d;
 }
 
@@ -502,13 +542,22 @@ static int launch_mc(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_pl
     int64_t blocks = (tiles + 7) / 8;
     int per_sm = 0;
     if constexpr (SRC == TT_SRC_MESH) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mc_mesh_kernel<D, PLAN, G>, block, 0);
-        if (per_sm < 1) per_sm = 1;
-        const int64_t cap = (int64_t)sm_count() * per_sm * 16;
-        if (blocks > cap) blocks = cap;
-        if (blocks < 1) blocks = 1;
-        mc_mesh_kernel<D, PLAN, G><<<(unsigned)blocks, block, 0, st>>>(td, e_lo, e_hi, pd, sd, contrib, b,
-                                                                        nullptr, status);
+        // variant: bit0 = speculative coefficient prefetch, bit1 = 3 blocks/SM register target
+        static int variant = [] { const char* v = getenv("TT_MC_VARIANT"); return v ? atoi(v) : 1; }();
+        auto launch = [&](auto kernel) {
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, 0);
+            if (per_sm < 1) per_sm = 1;
+            const int64_t cap = (int64_t)sm_count() * per_sm * 16;
+            if (blocks > cap) blocks = cap;
+            if (blocks < 1) blocks = 1;
+            kernel<<<(unsigned)blocks, block, 0, st>>>(td, e_lo, e_hi, pd, sd, contrib, b, nullptr, status);
+        };
+        switch (variant & 3) {
+            case 0: launch(mc_mesh_kernel<D, PLAN, G, false, 2>); break;
+            case 1: launch(mc_mesh_kernel<D, PLAN, G, true, 2>); break;
+            case 2: launch(mc_mesh_kernel<D, PLAN, G, false, 3>); break;
+            default: launch(mc_mesh_kernel<D, PLAN, G, true, 3>); break;
+        }
         return launch_check("mc_mesh_kernel");
     }
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mc_load_kernel<D, PLAN, SRC, G>, block, 0);
@@ -638,11 +687,11 @@ extern "C" int tt_mc_cache_ids(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, c
     const int64_t tiles = (e_hi - e_lo + 3) / 4;
     const unsigned nb = grid_for(tiles * 32, 256);
     if (t->dim == 2) {
-        if (p->kind == TT_PLAN_SHARED) mc_mesh_kernel<2, TT_PLAN_SHARED, 8><<<nb, 256, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
-        else mc_mesh_kernel<2, TT_PLAN_PHILOX, 8><<<nb, 256, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
+        if (p->kind == TT_PLAN_SHARED) mc_mesh_kernel<2, TT_PLAN_SHARED, 8, false, 2><<<nb, 256, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
+        else mc_mesh_kernel<2, TT_PLAN_PHILOX, 8, false, 2><<<nb, 256, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
     } else {
-        if (p->kind == TT_PLAN_SHARED) mc_mesh_kernel<3, TT_PLAN_SHARED, 8><<<nb, 256, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
-        else mc_mesh_kernel<3, TT_PLAN_PHILOX, 8><<<nb, 256, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
+        if (p->kind == TT_PLAN_SHARED) mc_mesh_kernel<3, TT_PLAN_SHARED, 8, false, 2><<<nb, 256, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
+        else mc_mesh_kernel<3, TT_PLAN_PHILOX, 8, false, 2><<<nb, 256, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
     }
     return launch_check("mc_mesh_kernel (cache ids)");
 }
@@ -744,4 +793,15 @@ extern "C" int tt_reduce_nodes(int64_t n_nodes, int k, const int64_t* inc_start,
     reduce_nodes_kernel<<<grid_for(n_nodes, 256), 256, 0, as_stream(stream)>>>(
         n_nodes, k, inc_start, inc, e_lo, e_hi, contrib, b);
     return launch_check("reduce_nodes_kernel");
+}
+
+extern "C" int tt_pack_coeffs(const tt_mesh_t* m, const double* coeffs, double* out, void* stream) {
+    if (!m || (m->dim != 2 && m->dim != 3) || !coeffs || !out) {
+        set_error("tt_pack_coeffs: bad arguments");
+        return TT_ERR_INVALID_PARAMETER;
+    }
+    if (m->n_elems == 0) return TT_OK;
+    pack_coeffs_kernel<<<grid_for(m->n_elems, 256), 256, 0, as_stream(stream)>>>(
+        m->n_elems, m->dim + 1, m->elems, coeffs, out);
+    return launch_check("pack_coeffs_kernel");
 }

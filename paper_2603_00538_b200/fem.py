@@ -51,6 +51,21 @@ class NodalField:
             self._host = self.coeffs_dev.cpu().numpy()
         return self._host
 
+    def elem_coeffs(self) -> torch.Tensor:
+        """(E, 4) per-element vertex coefficients (one aligned 32 B record per element,
+        tt_pack_coeffs), rebuilt when the coefficient tensor changes."""
+        key = (self.coeffs_dev.data_ptr(), self.coeffs_dev._version)
+        cached = getattr(self, "_packed", None)
+        if cached is not None and cached[0] == key:
+            return cached[1]
+        dm = self.mesh.device
+        out = torch.empty((self.mesh.n_elems, 4), dtype=torch.float64, device=self.coeffs_dev.device)
+        desc = dm.desc()
+        _lib.call("tt_pack_coeffs", C.byref(desc), _lib.ptr(self.coeffs_dev), _lib.ptr(out),
+                  _lib.stream_handle())
+        self._packed = (key, out)
+        return out
+
     @classmethod
     def from_function(cls, mesh, fn) -> "NodalField":
         """Nodal interpolant of ``fn(x, y[, z])`` (fem.py:30-34)."""

@@ -101,6 +101,7 @@ class MeshBackedField:
         s.grid = self.locator.desc()
         s.src_elems = _lib.ptr(self.field.mesh.device.elems).value
         s.coeffs = _lib.ptr(self.field.coeffs_dev).value
+        s.elem_coeffs = _lib.ptr(self.field.elem_coeffs()).value
         if target is not None and self.locator.walk:
             s.seeds = _lib.ptr(self.locator.seeds_for(target)).value
         return s

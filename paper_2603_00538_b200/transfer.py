@@ -70,6 +70,7 @@ class MCTransferOperator:
         s.src_elems = _lib.ptr(self.source_mesh.device.elems).value
         s.coeffs = _lib.ptr(source_field.coeffs_dev).value
         s.cached_ids = _lib.ptr(self.src_elem_dev).value
+        s.elem_coeffs = _lib.ptr(source_field.elem_coeffs()).value
         contrib = torch.empty((self.target.n_elems, k), dtype=torch.float64, device=dm.nodes.device)
         status = _lib.status_word()
         mdesc, pdesc = dm.desc(), self.plan.desc()
