@@ -117,8 +117,6 @@ struct PcgArgs {
     tt_pcg_result_t* res;
 };
 
-constexpr int kPcgBlock = 256;
-constexpr int kPcgMinBlocks = 4;
 constexpr int kRowG = 4;  // lanes per CSR row in the SpMV (rows have ~7 (2-D) / ~15 (3-D) nnz)
 
 __device__ __forceinline__ double block_sum(double v, double* sh) {
@@ -154,7 +152,8 @@ __device__ __forceinline__ double grid_total(const double* part, double* sh) {
 //   B: alpha = rz / p.Ap; x += alpha p; r -= alpha Ap; z = dinv r;
 //      partials r.r, r.z                                                   | sync
 //   then (every block, no barrier): residual test, best iterate, beta = rz_new / rz.
-__global__ void __launch_bounds__(kPcgBlock, kPcgMinBlocks) pcg_kernel(PcgArgs a) {
+template <int BLOCK, int MINB>
+__global__ void __launch_bounds__(BLOCK, MINB) pcg_kernel(PcgArgs a) {
     cg::grid_group grid = cg::this_grid();
     __shared__ double sh[33];
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -314,14 +313,20 @@ __global__ void sum_parts_kernel(int nparts, const double* __restrict__ part, do
     }
 }
 
-static int pcg_grid_blocks(int64_t n) {
+template <int BLOCK, int MINB>
+static int pcg_launch(PcgArgs& a, int64_t n, cudaStream_t st) {
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg_kernel, kPcgBlock, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg_kernel<BLOCK, MINB>, BLOCK, 0);
     if (per_sm < 1) per_sm = 1;
     int64_t maxb = (int64_t)sm_count() * per_sm;
-    int64_t need = (n * kRowG + kPcgBlock - 1) / kPcgBlock;
+    int64_t need = (n * kRowG + BLOCK - 1) / BLOCK;
     if (need < 1) need = 1;
-    return (int)(need < maxb ? need : maxb);
+    int blocks = (int)(need < maxb ? need : maxb);
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    void* args[] = {&a};
+    cudaError_t e = cudaLaunchCooperativeKernel((void*)pcg_kernel<BLOCK, MINB>, dim3(blocks), dim3(BLOCK),
+                                                args, 0, st);
+    return cuda_status(e, "pcg_kernel (cooperative launch)");
 }
 
 }  // namespace tt
@@ -391,12 +396,11 @@ extern "C" int tt_pcg(int64_t n, const int64_t* rp, const int32_t* ci, const dou
     a.dinv = work + 5 * n;
     a.part = work + 6 * n;
     a.res = result;
-    int blocks = pcg_grid_blocks(n);
-    if (blocks > 148 * 32) blocks = 148 * 32;
-    void* args[] = {&a};
-    cudaError_t e = cudaLaunchCooperativeKernel((void*)pcg_kernel, dim3(blocks), dim3(kPcgBlock), args,
-                                                0, as_stream(stream));
-    return cuda_status(e, "pcg_kernel (cooperative launch)");
+    // block shape: 2 x 512 threads per SM by default (measured best of 256x4 / 512x2 / 1024x1)
+    static int variant = [] { const char* v = getenv("TT_PCG_VARIANT"); return v ? atoi(v) : 1; }();
+    if (variant == 0) return pcg_launch<256, 4>(a, n, as_stream(stream));
+    if (variant == 1) return pcg_launch<512, 2>(a, n, as_stream(stream));
+    return pcg_launch<1024, 1>(a, n, as_stream(stream));
 }
 
 extern "C" int tt_spmv(int64_t n, const int64_t* rp, const int32_t* ci, const double* v,
