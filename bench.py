@@ -47,8 +47,11 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--samples", type=int, default=64)
+    ap.add_argument("--samples", type=int, default=None, help="N per element (64; c5: 50)")
     ap.add_argument("--n", type=int, default=55, help="cubes per axis (C2: 55)")
+    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5"],
+                    help="c2 (default): 1M-tet cube; c3: ~5M-tet torus pair (snap); c4: 10M-tet "
+                         "cube; c5: repeated coupling with cached localisation (C2 mesh)")
     ap.add_argument("--mode", default="sobol", choices=["sobol", "uniform", "philox"])
     ap.add_argument("--sweep", default="16,32,64,128,256")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -63,10 +66,26 @@ def dist_env():
     return rank, world, local
 
 
+WORKLOADS = {
+    "c2": "C2: 3-D unit-cube tet transfer (998,250 tets), mesh-backed source, 1 coupling step",
+    "c3": "C3: LTX-like swept-annulus torus pair (4,992,000 / 4,561,920 tets), snap on the "
+          "non-matching faceted boundary, 1 coupling step",
+    "c4": "C4: 3-D unit-cube tet transfer (10,368,000 tets), mesh-backed source, 1 coupling step",
+    "c5": "C5: repeated coupling step with cached localisation (MCTransferOperator.apply, C2 mesh)",
+}
+
+
+def mesh_names(args):
+    if args.config == "c3":
+        return "torus 40x80x260 kuhn jitter0.2 seed20", "torus 36x88x240 kuhn_mirror jitter0.2 seed10"
+    n = 120 if args.config == "c4" else args.n
+    return f"cube n={n} kuhn jitter0.2 seed20", f"cube n={n} kuhn_mirror jitter0.2 seed10"
+
+
 def workload_config(args, world):
-    return {"workload": "C2: 3-D unit-cube tet transfer, mesh-backed source, 1 coupling step",
-            "target": f"cube n={args.n} kuhn jitter0.2 seed20",
-            "source": f"cube n={args.n} kuhn_mirror jitter0.2 seed10",
+    tname, sname = mesh_names(args)
+    return {"workload": WORKLOADS[args.config],
+            "target": tname, "source": sname,
             "field": "sin(x)cos(y)cos(z)+2 (P1 interpolant on source)",
             "samples_per_elem": args.samples, "plan": args.mode, "cg_tol": 1e-12,
             "partition": f"contiguous target-element ranges x{world}", "l2": "flushed between timed steps",
@@ -120,9 +139,17 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------- ours
+def build_meshes(args, M):
+    if args.config == "c3":
+        return (M.generate_torus_mesh(40, 80, 260, perturbation=0.2, seed=20),
+                M.generate_torus_mesh(36, 88, 240, perturbation=0.2, seed=10, split="kuhn_mirror"))
+    n = 120 if args.config == "c4" else args.n
+    return (M.generate_cube_mesh(n, 0.2, seed=20, split="kuhn"),
+            M.generate_cube_mesh(n, 0.2, seed=10, split="kuhn_mirror"))
+
+
 def build_problem(args, tt):
-    tgt = tt.generate_cube_mesh(args.n, 0.2, seed=20, split="kuhn")
-    src = tt.generate_cube_mesh(args.n, 0.2, seed=10, split="kuhn_mirror")
+    tgt, src = build_meshes(args, tt)
     field = tt.get_field("smooth", dim=3)
     fs = tt.NodalField.from_function(src, field.fn)
     loc = tt.UniformGridLocator.build(src)
@@ -173,11 +200,19 @@ def run_ours(args):
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
     status = _lib.status_word()
 
+    ops = {}
+
     def step(plan, ev=None):
         if ev is not None:
             ev[0].record()
         fs._packed = None   # a coupling step brings new coefficients: repack them (timed)
-        b = load_vector(tgt, box, plan, e_lo, e_hi, deterministic=True, check=False, status=status)
+        if args.config == "c5":
+            if plan.n_samples not in ops:   # localisation cached once per plan (untimed init)
+                ops[plan.n_samples] = tt.MCTransferOperator(tgt, src, plan, source_locator=loc)
+                torch.cuda.synchronize()
+            b = ops[plan.n_samples].load(fs, check=False)
+        else:
+            b = load_vector(tgt, box, plan, e_lo, e_hi, deterministic=True, check=False, status=status)
         if ev is not None:
             ev[1].record()
         reduce_load(b)                      # NCCL all-reduce of the partial b (N>1)
@@ -230,7 +265,10 @@ def run_ours(args):
         flush.zero_()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
-        element_contributions(tgt, box, plan, e_lo, e_hi, out=contrib, status=status)
+        if args.config == "c5":
+            ops[plan.n_samples].load(fs, check=False)
+        else:
+            element_contributions(tgt, box, plan, e_lo, e_hi, out=contrib, status=status)
         e.record()
         if i >= args.warmup:
             kt.append((s, e))
@@ -258,7 +296,10 @@ def run_ours(args):
     def e2e_step():
         c_dev.copy_(c_host, non_blocking=True)
         field = tt.NodalField(src, c_dev)
-        b = load_vector(tgt, tt.MeshBackedField(field, loc), plan, e_lo, e_hi)
+        if args.config == "c5":
+            b = ops[plan.n_samples].load(field)
+        else:
+            b = load_vector(tgt, tt.MeshBackedField(field, loc), plan, e_lo, e_hi)
         reduce_load(b)
         xx = tt.cg_solve(mass, b, tol=1e-12)
         x_host.copy_(xx, non_blocking=True)
@@ -310,7 +351,7 @@ def run_ours(args):
             "e2e": {"value": S / (e2e_ms * 1e-3), "unit": "samples/s", "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": src.n_nodes * 8, "d2h_bytes_per_step": tgt.n_nodes * 8,
                     "api": "NodalField(pinned->device) + MeshBackedField + load_vector + cg_solve"},
-            "roofline": {"bound": "hbm", "kernel": "mc_load_kernel<3,SHARED,MESH,32>",
+            "roofline": {"bound": "hbm", "kernel": "mc_load_kernel<3,SHARED,CACHED>" if args.config == "c5" else "mc_mesh_kernel<3,SHARED,G,spec>",
                          "achieved": achieved, "peak": peak_hbm, "unit": "GB/s",
                          "frac": achieved / peak_hbm, "peak_source": peak_src,
                          "traffic": None, "kernel_ms": k_ms, "algorithmic_bytes": alg_bytes,
@@ -369,8 +410,7 @@ def run_reference(args):
     import paper_2603_00538_b200.mesh as M   # host-only mesh generators (no GPU use)
     sys.path.insert(0, str(ROOT / "oracle"))
     import tt_oracle as O
-    tgt = M.generate_cube_mesh(args.n, 0.2, seed=20, split="kuhn")
-    src = M.generate_cube_mesh(args.n, 0.2, seed=10, split="kuhn_mirror")
+    tgt, src = build_meshes(args, M)
 
     coeffs = np.sin(src.nodes[:, 0]) * np.cos(src.nodes[:, 1]) * np.cos(src.nodes[:, 2]) + 2
     cpu = cpu_baseline(args, tgt, src, coeffs, seconds=args.cpu_seconds)
@@ -398,6 +438,8 @@ def run_reference(args):
 
 def main():
     args = parse_args()
+    if args.samples is None:
+        args.samples = 50 if args.config == "c5" else 64
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -12,7 +12,7 @@ from .errors import (DegenerateElement, DeviceUnavailable, DimensionMismatch, Em
                      NonManifold, ParseError, SourceEvalFailed, TransferError,
                      ZeroDenominator)
 from .mesh import (SimplexMesh, TetMesh, TriMesh, build_adjacency, generate_cube_mesh,
-                   generate_square_mesh, load_msh, save_msh)
+                   generate_square_mesh, generate_torus_mesh, load_msh, save_msh)
 from .fem import (NodalField, SparseSymMatrix, assemble_mass_matrix, basis_integrals,
                   cg_solve, integrate_field)
 from .locate import EPS_LOC, OUTSIDE, UniformGridLocator
@@ -26,7 +26,7 @@ kernel_backend = "cuda-sm_100a"
 
 __all__ = [
     "TriMesh", "TetMesh", "SimplexMesh", "NodalField", "SparseSymMatrix",
-    "generate_square_mesh", "generate_cube_mesh", "load_msh", "save_msh", "build_adjacency",
+    "generate_square_mesh", "generate_cube_mesh", "generate_torus_mesh", "load_msh", "save_msh", "build_adjacency",
     "assemble_mass_matrix", "cg_solve", "integrate_field", "basis_integrals",
     "UniformGridLocator", "EPS_LOC", "OUTSIDE",
     "AnalyticField", "MeshBackedField", "SamplePlan", "assemble_load_mc",

@@ -421,3 +421,24 @@ def test_walk_equals_reference_scan_3d(tt, mode):
     _walk_vs_scan(tt, tgt, src, 64, 3, mode)
     flat = tt.generate_cube_mesh(6, 0.0)
     _walk_vs_scan(tt, flat, flat, 32, 3, mode)
+
+
+def test_torus_pair_snap_heavy_3d(tt):
+    """C3 stand-in at small size: non-matching faceted tori -> OUTSIDE samples snapped."""
+    tgt = tt.generate_torus_mesh(3, 14, 20, perturbation=0.2, seed=20)
+    src = tt.generate_torus_mesh(3, 12, 17, perturbation=0.2, seed=10, split="kuhn_mirror")
+    fs = tt.NodalField.from_function(src, tt.get_field("smooth", dim=3).fn)
+    plan = tt.SamplePlan.build(40, "sobol", 0, dim=3)
+    b = tt.assemble_load_mc(tgt, tt.MeshBackedField(fs), plan)
+    g = O.Grid(src.nodes, src.elements)
+    from paper_2603_00538_b200.montecarlo import map_points
+    pts = map_points(tgt, plan).cpu().numpy().reshape(-1, 3)
+    eo, _ = g.locate_many(pts)
+    assert (eo < 0).mean() > 0.005                     # the snap path really runs
+    ref = O.reduce_to_nodes(tgt.n_nodes, tgt.elements,
+                            O.accumulate(tgt.nodes, tgt.elements, tgt.elem_areas, plan.barycentric,
+                                         lambda P: O.mesh_backed_eval(g, fs.coeffs, P)))
+    assert _rel(b, ref) <= 1e-12
+    with pytest.raises(tt.SourceEvalFailed):
+        tt.assemble_load_mc(tgt, tt.MeshBackedField(fs, outside="strict"), plan)
+    _walk_vs_scan(tt, tgt, src, 40, 3)

@@ -147,3 +147,16 @@ def test_quadrature_local_mass():
         r = triangle_rule(deg)
         assert r.weights.sum() == pytest.approx(1.0, abs=1e-12)
     assert math.isclose(triangle_rule(3).degree, 4)
+
+
+def test_torus_generator_is_a_closed_tessellation():
+    m = tt.generate_torus_mesh(3, 10, 14, perturbation=0.2, seed=2)
+    assert m.n_elems == 6 * 3 * 10 * 14
+    adj = tt.build_adjacency(m.elements)
+    assert int((adj < 0).sum()) == 2 * 2 * 10 * 14       # inner + outer annulus surfaces
+    assert m.domain_volume == pytest.approx(m.elem_areas.sum(), rel=1e-12)
+    fine = tt.generate_torus_mesh(6, 48, 64)
+    exact = 2 * np.pi ** 2 * 1.0 * (0.45 ** 2 - 0.15 ** 2)
+    assert fine.elem_areas.sum() == pytest.approx(exact, rel=5e-3)
+    with pytest.raises(tt.InvalidParameter):
+        tt.generate_torus_mesh(2, 2, 8)
