@@ -205,7 +205,7 @@ def run_ours(args):
     def step(plan, ev=None):
         if ev is not None:
             ev[0].record()
-        fs._packed = None   # a coupling step brings new coefficients: repack them (timed)
+        fs._packed = fs._grad = None   # new coefficients each coupling step: repack (timed)
         if args.config == "c5":
             if plan.n_samples not in ops:   # localisation cached once per plan (untimed init)
                 ops[plan.n_samples] = tt.MCTransferOperator(tgt, src, plan, source_locator=loc)
@@ -361,7 +361,7 @@ def run_ours(args):
             "sweep": sweep,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
-            "gpu_launches": 4 * args.steps,
+            "gpu_launches": 5 * args.steps,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -124,7 +124,13 @@ typedef struct tt_grid {
     const int32_t* cell_elems;  /* ascending element ids per cell */
     const double*  rec;         /* (n_elems, TT_REC_STRIDE(dim)) packed binv/origin */
     const double*  centroids;   /* (n_elems, dim) */
+    const double*  wrec;        /* optional compact walk records (n_elems, TT_WREC_STRIDE(dim)):
+                                   origin (dim doubles), binv as float (dim*dim), float tau_f,
+                                   int32 nbr[dim+1]; written by tt_grid_walk_prep */
 } tt_grid_t;
+
+/* compact walk record stride in doubles: 48 B (2-D), 80 B (3-D) */
+#define TT_WREC_STRIDE(dim) ((dim) == 2 ? 6 : 10)
 
 typedef struct tt_plan {
     int32_t  kind;            /* TT_PLAN_SHARED | TT_PLAN_PHILOX */
@@ -155,6 +161,8 @@ typedef struct tt_source {
                                  per target element (tt_seed_elements), or NULL */
     const double*  elem_coeffs;/* TT_SRC_MESH/CACHED optional (E_s, 4) per-element vertex
                                  coefficients (tt_pack_coeffs); replaces src_elems+coeffs */
+    const double*  elem_grad;  /* TT_SRC_MESH optional (E_s, 4): gradient g (dim) and the value at
+                                 the origin vertex (tt_pack_grad): f = c_last + g.(x - o) */
 } tt_source_t;
 
 typedef struct tt_pcg_result {
@@ -204,7 +212,8 @@ int tt_locate_many(const double* points, int64_t count, int nx, int ny,
 /* Certified facet walk: fills tau and nbr of every record from
  * the node incidence; sets TT_FLAG_NONMANIFOLD in *status for a non-manifold mesh. */
 int tt_grid_walk_prep(const tt_mesh_t* mesh, const int64_t* inc_start, const int32_t* inc,
-                      double eps, double* rec, int32_t* status, void* stream);
+                      double eps, double* rec, double* wrec /* or NULL */, int32_t* status,
+                      void* stream);
 /* seeds[(e - e_lo)*(dim+2) + s] = source element containing, for s = 0, the target
  * element's centroid c and, for s = 1 + i, the point (v_i + c)/2 (reference scan, snapped
  * when outside): walk starts for the element's samples (nearest by max barycentric). */
@@ -234,6 +243,11 @@ int tt_mc_cache_ids(const tt_mesh_t* target, int64_t e_lo, int64_t e_hi, const t
 /* out[e*4 + i] = coeffs[elems[e*k + i]] (i < k, zero padded): one aligned 32-byte record
  * per source element, gathered once per coefficient update. */
 int tt_pack_coeffs(const tt_mesh_t* src, const double* coeffs, double* out, void* stream);
+
+/* out[e*4 ..] = (g, c_last): the P1 field's gradient on element e and its value at the
+ * last vertex (the record origin), from the packed binv: g_j = sum_i binv_ij (c_i - c_last). */
+int tt_pack_grad(const tt_mesh_t* src, const double* rec, const double* coeffs, double* out,
+                 void* stream);
 
 /* ---- node reduction / incidence (deterministic np.add.at order) ---- */
 int tt_incidence_count(const tt_mesh_t* mesh, int64_t* inc_start /* (n_nodes+1) */,

@@ -35,6 +35,10 @@ def rec_stride(dim: int) -> int:
     return 8 if dim == 2 else 16
 
 
+def wrec_stride(dim: int) -> int:
+    return 6 if dim == 2 else 10
+
+
 class tt_mesh_t(C.Structure):
     _fields_ = [("dim", C.c_int32), ("reserved", C.c_int32), ("n_nodes", C.c_int64),
                 ("n_elems", C.c_int64), ("nodes", C.c_void_p), ("elems", C.c_void_p),
@@ -45,7 +49,8 @@ class tt_grid_t(C.Structure):
     _fields_ = [("dim", C.c_int32), ("n", C.c_int32 * 3), ("walk", C.c_int32),
                 ("reserved", C.c_int32), ("lo", C.c_double * 3),
                 ("hi", C.c_double * 3), ("n_elems", C.c_int64), ("cell_start", C.c_void_p),
-                ("cell_elems", C.c_void_p), ("rec", C.c_void_p), ("centroids", C.c_void_p)]
+                ("cell_elems", C.c_void_p), ("rec", C.c_void_p), ("centroids", C.c_void_p),
+                ("wrec", C.c_void_p)]
 
 
 class tt_plan_t(C.Structure):
@@ -62,7 +67,8 @@ class tt_source_t(C.Structure):
     _fields_ = [("kind", C.c_int32), ("outside", C.c_int32), ("dim", C.c_int32),
                 ("reserved", C.c_int32), ("expr", tt_expr_t), ("grid", tt_grid_t),
                 ("src_elems", C.c_void_p), ("coeffs", C.c_void_p), ("values", C.c_void_p),
-                ("cached_ids", C.c_void_p), ("seeds", C.c_void_p), ("elem_coeffs", C.c_void_p)]
+                ("cached_ids", C.c_void_p), ("seeds", C.c_void_p), ("elem_coeffs", C.c_void_p),
+                ("elem_grad", C.c_void_p)]
 
 
 class tt_pcg_result_t(C.Structure):
@@ -91,7 +97,7 @@ _SIGNATURES = {
     "tt_grid_fill": ([C.POINTER(tt_mesh_t), C.POINTER(tt_grid_t), _P, _P, _P], _I),
     "tt_locate": ([C.POINTER(tt_grid_t), _P, _I64, _D, _P, _P, _P], _I),
     "tt_locate_many": ([_P, _I64, _I, _I, C.POINTER(_D), _P, _P, _P, _P, _D, _P, _P, _P], _I),
-    "tt_grid_walk_prep": ([C.POINTER(tt_mesh_t), _P, _P, _D, _P, _P, _P], _I),
+    "tt_grid_walk_prep": ([C.POINTER(tt_mesh_t), _P, _P, _D, _P, _P, _P, _P], _I),
     "tt_seed_elements": ([C.POINTER(tt_grid_t), C.POINTER(tt_mesh_t), _I64, _I64, _P, _P], _I),
     "tt_nearest": ([C.POINTER(tt_grid_t), _P, _I64, _P, _P], _I),
     "tt_snap": ([C.POINTER(tt_grid_t), _P, _I64, _P, _P, _P], _I),
@@ -102,6 +108,7 @@ _SIGNATURES = {
     "tt_mc_cache_ids": ([C.POINTER(tt_mesh_t), _I64, _I64, C.POINTER(tt_plan_t),
                          C.POINTER(tt_grid_t), _P, _P, _P], _I),
     "tt_pack_coeffs": ([C.POINTER(tt_mesh_t), _P, _P, _P], _I),
+    "tt_pack_grad": ([C.POINTER(tt_mesh_t), _P, _P, _P, _P], _I),
     "tt_incidence_count": ([C.POINTER(tt_mesh_t), _P, _P], _I),
     "tt_incidence_fill": ([C.POINTER(tt_mesh_t), _P, _P, _P, _P], _I),
     "tt_reduce_nodes": ([_I64, _I, _P, _P, _I64, _I64, _P, _P, _P], _I),

@@ -139,6 +139,39 @@ TT_D void load_tail(const double* __restrict__ rec, int64_t e, RecTail<D>& t) {
     if constexpr (D == 3) t.nbr[3] = __ldg(reinterpret_cast<const int*>(q + 1));
 }
 
+// Compact walk record: origin (double), binv (float), tau_f (float), nbr (int32).
+template <int D>
+struct WRec {
+    double o[D];
+    float b[D][D];
+    float tau;
+    int nbr[D + 1];
+};
+
+template <int D>
+TT_D void load_wrec(const double* __restrict__ wrec, int64_t e, WRec<D>& w) {
+    if constexpr (D == 2) {
+        const int4* q = reinterpret_cast<const int4*>(wrec + e * 6);
+        const int4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
+        w.o[0] = __hiloint2double(a.y, a.x); w.o[1] = __hiloint2double(a.w, a.z);
+        w.b[0][0] = __int_as_float(b.x); w.b[0][1] = __int_as_float(b.y);
+        w.b[1][0] = __int_as_float(b.z); w.b[1][1] = __int_as_float(b.w);
+        w.tau = __int_as_float(c.x);
+        w.nbr[0] = c.y; w.nbr[1] = c.z; w.nbr[2] = c.w;
+    } else {
+        const int4* q = reinterpret_cast<const int4*>(wrec + e * 10);
+        const int4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2), d = __ldg(q + 3), f = __ldg(q + 4);
+        w.o[0] = __hiloint2double(a.y, a.x); w.o[1] = __hiloint2double(a.w, a.z);
+        w.o[2] = __hiloint2double(b.y, b.x);
+        w.b[0][0] = __int_as_float(b.z); w.b[0][1] = __int_as_float(b.w);
+        w.b[0][2] = __int_as_float(c.x); w.b[1][0] = __int_as_float(c.y);
+        w.b[1][1] = __int_as_float(c.z); w.b[1][2] = __int_as_float(c.w);
+        w.b[2][0] = __int_as_float(d.x); w.b[2][1] = __int_as_float(d.y);
+        w.b[2][2] = __int_as_float(d.z); w.tau = __int_as_float(d.w);
+        w.nbr[0] = f.x; w.nbr[1] = f.y; w.nbr[2] = f.z; w.nbr[3] = f.w;
+    }
+}
+
 // --------------------------------------------------------------- grid descriptor
 struct GridDev {
     int n0, n1, n2;
@@ -148,6 +181,7 @@ struct GridDev {
     const int32_t* __restrict__ cell_elems;
     const double* __restrict__ rec;
     const double* __restrict__ centroids;
+    const double* __restrict__ wrec;
 };
 
 inline GridDev to_dev(const tt_grid_t& g) {
@@ -157,6 +191,7 @@ inline GridDev to_dev(const tt_grid_t& g) {
     for (int c = 0; c < 3; ++c) { d.lo[c] = g.lo[c]; d.hi[c] = g.hi[c]; }
     d.cell_start = g.cell_start; d.cell_elems = g.cell_elems;
     d.rec = g.rec; d.centroids = g.centroids;
+    d.wrec = g.wrec;
     return d;
 }
 

@@ -313,7 +313,8 @@ __global__ void walk_prep_kernel(int64_t E, const double* __restrict__ nodes,
                                  const int32_t* __restrict__ elems,
                                  const int64_t* __restrict__ inc_start,
                                  const int32_t* __restrict__ inc, double eps, double dmax,
-                                 double* __restrict__ rec, int32_t* __restrict__ status) {
+                                 double* __restrict__ rec, double* __restrict__ wrec,
+                                 int32_t* __restrict__ status) {
     constexpr int K = D + 1;
     constexpr int S = (D == 2) ? 8 : 16;
     int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -381,6 +382,32 @@ __global__ void walk_prep_kernel(int64_t E, const double* __restrict__ nodes,
     *q = tail;
     if constexpr (D == 3) reinterpret_cast<int*>(q + 1)[0] = nbr[3];
     if (nonmanifold) atomicOr(status, TT_FLAG_NONMANIFOLD);
+    if (wrec) {
+        // compact float walk record; its margin adds a rigorous bound on the float
+        // evaluation error of lambda for points within the element:
+        //   |lambda_f - lambda| <= 2^-24 * (~6 * sum|b_ij| * |r| + 3),  |r| <= diam(A)
+        // taken with a 16x safety factor (2^-20 and 4x/8x terms)
+        const double* rb = rec + e * S;
+        double babs = 0.0;
+        for (int i = 0; i < D * D; ++i) babs += fabs(rb[i]);
+        double diam = 0.0;
+        for (int a = 0; a < K; ++a)
+            for (int b2 = a + 1; b2 < K; ++b2) {
+                double d2 = 0.0;
+                for (int c = 0; c < D; ++c) d2 += (v[a][c] - v[b2][c]) * (v[a][c] - v[b2][c]);
+                diam = fmax(diam, sqrt(d2));
+            }
+        double tau_f = tau + 9.5367431640625e-07 * (4.0 * babs * diam * 1.0001 + 8.0);
+        if (!(tau_f < 0.25)) tau_f = 2.0;
+        constexpr int WS = (D == 2) ? 6 : 10;
+        double* w = wrec + e * WS;
+        for (int c = 0; c < D; ++c) w[c] = rb[D * D + c];           // origin (double)
+        float* wf = reinterpret_cast<float*>(w + D);
+        for (int i = 0; i < D * D; ++i) wf[i] = __double2float_rn(rb[i]);
+        wf[D * D] = __double2float_ru(tau_f);
+        int* wn = reinterpret_cast<int*>(wf + D * D + 1);
+        for (int i = 0; i < K; ++i) wn[i] = nbr[i];
+    }
 }
 
 // Walk seeds per target element: the source elements containing its centroid and the
@@ -583,7 +610,7 @@ extern "C" int tt_snap(const tt_grid_t* g, const double* pts, int64_t K, int32_t
 }
 
 extern "C" int tt_grid_walk_prep(const tt_mesh_t* m, const int64_t* inc_start, const int32_t* inc,
-                                 double eps, double* rec, int32_t* status, void* stream) {
+                                 double eps, double* rec, double* wrec, int32_t* status, void* stream) {
     if (!m || (m->dim != 2 && m->dim != 3) || !inc_start || !inc || !rec) {
         set_error("tt_grid_walk_prep: bad arguments");
         return TT_ERR_INVALID_PARAMETER;
@@ -607,10 +634,10 @@ extern "C" int tt_grid_walk_prep(const tt_mesh_t* m, const int64_t* inc_start, c
     memcpy(&dmax, &bits, sizeof(dmax));
     if (m->dim == 2)
         walk_prep_kernel<2><<<grid_for(m->n_elems, 128), 128, 0, s>>>(m->n_elems, m->nodes, m->elems,
-                                                                      inc_start, inc, eps, dmax, rec, status);
+                                                                      inc_start, inc, eps, dmax, rec, wrec, status);
     else
         walk_prep_kernel<3><<<grid_for(m->n_elems, 128), 128, 0, s>>>(m->n_elems, m->nodes, m->elems,
-                                                                      inc_start, inc, eps, dmax, rec, status);
+                                                                      inc_start, inc, eps, dmax, rec, wrec, status);
     return launch_check("walk_prep_kernel");
 }
 

@@ -30,6 +30,7 @@ struct SrcDev {
     const int32_t* __restrict__ cached;
     const int32_t* __restrict__ seeds;
     const double* __restrict__ ecoef;
+    const double* __restrict__ egrad;
 };
 
 template <int D>
@@ -258,7 +259,7 @@ __device__ __forceinline__ void plan_lambda(const PlanDev& plan, int64_t e, int6
 // many steps individual samples need; the assignment is a deterministic function of the
 // data, so results are bitwise reproducible.  Identical ids/lambdas as the reference scan
 // (certified walk, see locate_walk in tt_common.cuh).
-template <int D, int PLAN, int G, bool SPEC, int MINB>
+template <int D, int PLAN, int G, bool SPEC, int MINB, bool FW = false>
 __global__ void __launch_bounds__(256, MINB) mc_mesh_kernel(TargetDev t, int64_t e_lo, int64_t e_hi,
                                                       PlanDev plan, SrcDev src,
                                                       double* __restrict__ contrib,
@@ -333,8 +334,64 @@ __global__ void __launch_bounds__(256, MINB) mc_mesh_kernel(TargetDev t, int64_t
             double l[K];
             int hit = -1;
             bool done = false;
+            bool fw_hit = false;
+            double fw_f = 0.0;
             double2 pc0 = make_double2(0.0, 0.0), pc1 = make_double2(0.0, 0.0);
-            if (cur >= 0 && steps < 12) {
+            if constexpr (FW) {
+                if (cur >= 0 && steps < 12) {
+                    // compact float walk step: exact ids via a margin that bounds the float
+                    // evaluation error (tt_grid.cu walk_prep_kernel); f from the element's
+                    // gradient record: f = c_last + g . (x - o), accurate to a few ulps
+                    WRec<D> w;
+                    load_wrec<D>(g.wrec, cur, w);
+                    if (src.egrad) {
+                        const double2* q = reinterpret_cast<const double2*>(src.egrad + (int64_t)cur * 4);
+                        pc0 = __ldg(q);
+                        pc1 = __ldg(q + 1);
+                    }
+                    double r[D];
+                    float rf[D];
+#pragma unroll
+                    for (int c = 0; c < D; ++c) { r[c] = x[c] - w.o[c]; rf[c] = __double2float_rn(r[c]); }
+                    float lf[K];
+#pragma unroll
+                    for (int i = 0; i < D; ++i) {
+                        float a = w.b[i][0] * rf[0];
+#pragma unroll
+                        for (int c = 1; c < D; ++c) a = fmaf(w.b[i][c], rf[c], a);
+                        lf[i] = a;
+                    }
+                    float last = 1.0f - lf[0] - lf[1];
+                    if constexpr (D == 3) last -= lf[2];
+                    lf[D] = last;
+                    int imin = 0;
+                    float lmin = lf[0];
+#pragma unroll
+                    for (int i = 1; i <= D; ++i)
+                        if (lf[i] < lmin) { lmin = lf[i]; imin = i; }
+                    if (lmin >= w.tau) {
+                        hit = cur;
+                        done = true;
+                        fw_hit = true;
+                        const double gv[4] = {pc0.x, pc0.y, pc1.x, pc1.y};
+                        double f = gv[D];
+#pragma unroll
+                        for (int c = 0; c < D; ++c) f = fma(gv[c], r[c], f);
+                        fw_f = f;
+                    } else if (lmin > -w.tau) {
+                        cur = -1;  // within the uncertainty band of a facet: exact scan
+                    } else {
+                        int nb = w.nbr[0];
+#pragma unroll
+                        for (int i = 1; i <= D; ++i)
+                            if (imin == i) nb = w.nbr[i];
+                        cur = nb;
+                        ++steps;
+                    }
+                } else {
+                    cur = -1;
+                }
+            } else if (cur >= 0 && steps < 12) {
                 Rec<D> r;
                 load_rec<D>(g.rec, cur, r);
                 RecTail<D> tl;
@@ -387,8 +444,10 @@ __global__ void __launch_bounds__(256, MINB) mc_mesh_kernel(TargetDev t, int64_t
             if (done) {
                 if (ids_out) ids_out[le * N + jcur] = hit;
                 double f = 0.0;
-                if (hit >= 0 && (contrib || b)) {
-                    if (SPEC && src.ecoef && hit == cur) {
+                if (FW && fw_hit) {
+                    f = fw_f;
+                } else if (hit >= 0 && (contrib || b)) {
+                    if (SPEC && !FW && src.ecoef && hit == cur) {
                         const double c[4] = {pc0.x, pc0.y, pc1.x, pc1.y};
                         f = mul(c[0], l[0]);
 #pragma unroll
@@ -469,6 +528,30 @@ __global__ void pack_coeffs_kernel(int64_t E, int k, const int32_t* __restrict__
     o[1] = make_double2(c[2], c[3]);
 }
 
+template <int D>
+__global__ void pack_grad_kernel(int64_t E, const int32_t* __restrict__ elems,
+                                 const double* __restrict__ rec, const double* __restrict__ coeffs,
+                                 double* __restrict__ out) {
+    constexpr int K = D + 1;
+    constexpr int S = (D == 2) ? 8 : 16;
+    int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= E) return;
+    double c[K];
+    for (int i = 0; i < K; ++i) c[i] = coeffs[elems[e * K + i]];
+    const double* b = rec + e * S;
+    double o[4] = {0.0, 0.0, 0.0, 0.0};
+    // g_j = sum_i binv_ij (c_i - c_last); lambda_i = sum_j binv_ij r_j, lambda_last = 1 - sum
+    for (int j = 0; j < D; ++j) {
+        double gj = 0.0;
+        for (int i = 0; i < D; ++i) gj = fma(b[i * D + j], c[i] - c[D], gj);
+        o[j] = gj;
+    }
+    o[D] = c[D];
+    double2* q = reinterpret_cast<double2*>(out + e * 4);
+    q[0] = make_double2(o[0], o[1]);
+    q[1] = make_double2(o[2], o[3]);
+}
+
 // b[n] = sum over the node's incidences (e*k + a ascending) of contrib[e - e_lo, a],
 // starting from 0.0 -- exactly np.add.at's accumulation order (montecarlo.py:146).
 __global__ void reduce_nodes_kernel(int64_t n_nodes, int k, const int64_t* __restrict__ inc_start,
@@ -526,6 +609,7 @@ static SrcDev to_src(const tt_source_t& s) {
     d.cached = s.cached_ids;
     d.seeds = s.seeds;
     d.ecoef = s.elem_coeffs;
+    d.egrad = s.elem_grad;
     return d;
 }
 
@@ -542,8 +626,9 @@ static int launch_mc(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_pl
     int64_t blocks = (tiles + 7) / 8;
     int per_sm = 0;
     if constexpr (SRC == TT_SRC_MESH) {
-        // variant: bit0 = speculative coefficient prefetch, bit1 = 3 blocks/SM register target
-        static int variant = [] { const char* v = getenv("TT_MC_VARIANT"); return v ? atoi(v) : 1; }();
+        // variant: bit0 = speculative coefficient prefetch, bit1 = 3 blocks/SM register target,
+        // bit2 = compact float walk + gradient evaluation (needs grid.wrec and elem_grad)
+        static int variant = [] { const char* v = getenv("TT_MC_VARIANT"); return v ? atoi(v) : 5; }();
         auto launch = [&](auto kernel) {
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, 0);
             if (per_sm < 1) per_sm = 1;
@@ -552,6 +637,10 @@ static int launch_mc(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_pl
             if (blocks < 1) blocks = 1;
             kernel<<<(unsigned)blocks, block, 0, st>>>(td, e_lo, e_hi, pd, sd, contrib, b, nullptr, status);
         };
+        if ((variant & 4) && sd.grid.wrec && sd.egrad && sd.grid.walk && sd.seeds) {
+            launch(mc_mesh_kernel<D, PLAN, G, true, 2, true>);
+            return launch_check("mc_mesh_kernel (float walk)");
+        }
         switch (variant & 3) {
             case 0: launch(mc_mesh_kernel<D, PLAN, G, false, 2>); break;
             case 1: launch(mc_mesh_kernel<D, PLAN, G, true, 2>); break;
@@ -576,6 +665,12 @@ static int dispatch_g(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_p
                       cudaStream_t st) {
     // lanes per element: at least ~8 samples per lane (amortises the per-element setup)
     const int64_t N = p->n_samples;
+    static int spl = [] { const char* v = getenv("TT_MC_SPL"); return v ? atoi(v) : 8; }();
+    const int64_t gsel = N / spl;  // lanes so that each lane gets ~spl samples
+    if (gsel < 8) return launch_mc<D, PLAN, SRC, 4>(t, e_lo, e_hi, p, s, contrib, b, status, st);
+    if (gsel < 16) return launch_mc<D, PLAN, SRC, 8>(t, e_lo, e_hi, p, s, contrib, b, status, st);
+    if (gsel < 32) return launch_mc<D, PLAN, SRC, 16>(t, e_lo, e_hi, p, s, contrib, b, status, st);
+    return launch_mc<D, PLAN, SRC, 32>(t, e_lo, e_hi, p, s, contrib, b, status, st);
     if (N < 64) return launch_mc<D, PLAN, SRC, 4>(t, e_lo, e_hi, p, s, contrib, b, status, st);
     if (N < 128) return launch_mc<D, PLAN, SRC, 8>(t, e_lo, e_hi, p, s, contrib, b, status, st);
     if (N < 256) return launch_mc<D, PLAN, SRC, 16>(t, e_lo, e_hi, p, s, contrib, b, status, st);
@@ -686,12 +781,25 @@ extern "C" int tt_mc_cache_ids(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, c
     auto s = as_stream(stream);
     const int64_t tiles = (e_hi - e_lo + 3) / 4;
     const unsigned nb = grid_for(tiles * 32, 256);
+    // the float-walk kernel when the grid carries compact walk records (the default load
+    // path), else the double walk; either way the ids are the reference scan's
+    const bool fw = g->wrec && g->walk && seeds;
     if (t->dim == 2) {
-        if (p->kind == TT_PLAN_SHARED) mc_mesh_kernel<2, TT_PLAN_SHARED, 8, false, 2><<<nb, 256, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
-        else mc_mesh_kernel<2, TT_PLAN_PHILOX, 8, false, 2><<<nb, 256, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
+        if (p->kind == TT_PLAN_SHARED) {
+            if (fw) mc_mesh_kernel<2, TT_PLAN_SHARED, 8, true, 2, true><<<nb, 256, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
+            else mc_mesh_kernel<2, TT_PLAN_SHARED, 8, false, 2><<<nb, 256, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
+        } else {
+            if (fw) mc_mesh_kernel<2, TT_PLAN_PHILOX, 8, true, 2, true><<<nb, 256, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
+            else mc_mesh_kernel<2, TT_PLAN_PHILOX, 8, false, 2><<<nb, 256, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
+        }
     } else {
-        if (p->kind == TT_PLAN_SHARED) mc_mesh_kernel<3, TT_PLAN_SHARED, 8, false, 2><<<nb, 256, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
-        else mc_mesh_kernel<3, TT_PLAN_PHILOX, 8, false, 2><<<nb, 256, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
+        if (p->kind == TT_PLAN_SHARED) {
+            if (fw) mc_mesh_kernel<3, TT_PLAN_SHARED, 8, true, 2, true><<<nb, 256, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
+            else mc_mesh_kernel<3, TT_PLAN_SHARED, 8, false, 2><<<nb, 256, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
+        } else {
+            if (fw) mc_mesh_kernel<3, TT_PLAN_PHILOX, 8, true, 2, true><<<nb, 256, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
+            else mc_mesh_kernel<3, TT_PLAN_PHILOX, 8, false, 2><<<nb, 256, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
+        }
     }
     return launch_check("mc_mesh_kernel (cache ids)");
 }
@@ -804,4 +912,18 @@ extern "C" int tt_pack_coeffs(const tt_mesh_t* m, const double* coeffs, double* 
     pack_coeffs_kernel<<<grid_for(m->n_elems, 256), 256, 0, as_stream(stream)>>>(
         m->n_elems, m->dim + 1, m->elems, coeffs, out);
     return launch_check("pack_coeffs_kernel");
+}
+
+extern "C" int tt_pack_grad(const tt_mesh_t* m, const double* rec, const double* coeffs, double* out,
+                            void* stream) {
+    if (!m || (m->dim != 2 && m->dim != 3) || !rec || !coeffs || !out) {
+        set_error("tt_pack_grad: bad arguments");
+        return TT_ERR_INVALID_PARAMETER;
+    }
+    if (m->n_elems == 0) return TT_OK;
+    if (m->dim == 2)
+        pack_grad_kernel<2><<<grid_for(m->n_elems, 256), 256, 0, as_stream(stream)>>>(m->n_elems, m->elems, rec, coeffs, out);
+    else
+        pack_grad_kernel<3><<<grid_for(m->n_elems, 256), 256, 0, as_stream(stream)>>>(m->n_elems, m->elems, rec, coeffs, out);
+    return launch_check("pack_grad_kernel");
 }

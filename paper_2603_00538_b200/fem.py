@@ -66,6 +66,21 @@ class NodalField:
         self._packed = (key, out)
         return out
 
+    def elem_grad(self) -> torch.Tensor:
+        """(E, 4) per-element (gradient, value at the last vertex) of the P1 field
+        (tt_pack_grad): the fused kernel evaluates f = c_last + g.(x - o)."""
+        key = (self.coeffs_dev.data_ptr(), self.coeffs_dev._version)
+        cached = getattr(self, "_grad", None)
+        if cached is not None and cached[0] == key:
+            return cached[1]
+        dm = self.mesh.device
+        out = torch.empty((self.mesh.n_elems, 4), dtype=torch.float64, device=self.coeffs_dev.device)
+        desc = dm.desc()
+        _lib.call("tt_pack_grad", C.byref(desc), _lib.ptr(dm.rec), _lib.ptr(self.coeffs_dev),
+                  _lib.ptr(out), _lib.stream_handle())
+        self._grad = (key, out)
+        return out
+
     @classmethod
     def from_function(cls, mesh, fn) -> "NodalField":
         """Nodal interpolant of ``fn(x, y[, z])`` (fem.py:30-34)."""

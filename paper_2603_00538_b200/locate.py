@@ -121,6 +121,8 @@ class UniformGridLocator:
         g.cell_elems = _lib.ptr(self.cell_elems_dev).value if self.cell_elems_dev is not None else None
         g.rec = _lib.ptr(dm.rec).value
         g.centroids = _lib.ptr(dm.centroids).value
+        if self.walk and getattr(dm, "wrec", None) is not None:
+            g.wrec = _lib.ptr(dm.wrec).value
         return g
 
     def seeds_for(self, target) -> torch.Tensor:
@@ -211,8 +213,10 @@ def _walk_prep(mesh):
     inc_start, inc = dm.incidence
     status = _lib.status_word()
     desc = dm.desc()
+    dm.wrec = torch.empty((mesh.n_elems, _lib.wrec_stride(mesh.DIM)), dtype=torch.float64,
+                          device=dm.nodes.device)
     _lib.call("tt_grid_walk_prep", C.byref(desc), _lib.ptr(inc_start), _lib.ptr(inc), EPS_LOC,
-              _lib.ptr(dm.rec), _lib.ptr(status), _lib.stream_handle())
+              _lib.ptr(dm.rec), _lib.ptr(dm.wrec), _lib.ptr(status), _lib.stream_handle())
     if int(status.item()) & _lib.TT_FLAG_NONMANIFOLD:
         raise NonManifold("a facet is shared by more than two elements")
     dm.walk_ready = True

@@ -104,6 +104,7 @@ class MeshBackedField:
         s.elem_coeffs = _lib.ptr(self.field.elem_coeffs()).value
         if target is not None and self.locator.walk:
             s.seeds = _lib.ptr(self.locator.seeds_for(target)).value
+            s.elem_grad = _lib.ptr(self.field.elem_grad()).value
         return s
 
     def __call__(self, points):
