@@ -119,6 +119,42 @@ struct PcgArgs {
 
 constexpr int kRowG = 4;  // lanes per CSR row in the SpMV (rows have ~7 (2-D) / ~15 (3-D) nnz)
 
+// Row dot product sum_q v[q] * col(ci[q]) for kRowG lanes per row: each lane first
+// issues all of its (up to 4) column-index and value loads, then all gathers, so the
+// dependent ci -> x[ci] chains of a row overlap (memory-level parallelism).
+template <class Col>
+__device__ __forceinline__ double row_dot(const int64_t q0, const int64_t q1, const int sub,
+                                          const int32_t* __restrict__ ci,
+                                          const double* __restrict__ v, Col col) {
+    double acc = 0.0;
+    int64_t q = q0 + sub;
+    for (; q + 3 * kRowG < q1; q += 4 * kRowG) {
+        int c[4];
+        double a[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) { c[t] = ci[q + t * kRowG]; a[t] = v[q + t * kRowG]; }
+        double x[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) x[t] = col(c[t]);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) acc = fma(a[t], x[t], acc);
+    }
+    int c[4];
+    double a[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        const bool ok = q + t * kRowG < q1;
+        c[t] = ok ? ci[q + t * kRowG] : -1;
+        a[t] = ok ? v[q + t * kRowG] : 0.0;
+    }
+    double x[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) x[t] = c[t] >= 0 ? col(c[t]) : 0.0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) acc = fma(a[t], x[t], acc);
+    return acc;
+}
+
 __device__ __forceinline__ double block_sum(double v, double* sh) {
     for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -212,12 +248,10 @@ __global__ void __launch_bounds__(BLOCK, MINB) pcg_kernel(PcgArgs a) {
             const int64_t i = w0 + lane / kRowG;
             double s = 0.0;
             if (i < n) {
-                const int64_t q0 = a.rp[i], q1 = a.rp[i + 1];
-                for (int64_t q = q0 + sub; q < q1; q += kRowG) {
-                    const int c = a.ci[q];
-                    const double pc = a.z[c] + beta * p_old[c];
-                    s += a.v[q] * pc;
-                }
+                const double* __restrict__ z = a.z;
+                const double* __restrict__ po = p_old;
+                s = row_dot(a.rp[i], a.rp[i + 1], sub, a.ci, a.v,
+                            [&](int c) { return z[c] + beta * po[c]; });
             }
 #pragma unroll
             for (int off = kRowG / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
@@ -274,6 +308,170 @@ __global__ void __launch_bounds__(BLOCK, MINB) pcg_kernel(PcgArgs a) {
     }
 }
 
+// Chronopoulos-Gear Jacobi PCG (the same Krylov iterates as fem.py:131-152 in exact
+// arithmetic; both inner products of an iteration come from ONE reduction), one grid
+// barrier per iteration.  Loop top (after the barrier): residual test / best iterate on
+// the current r, then beta = g_new/g, alpha = g_new/(delta - beta g_new/alpha_old) and
+// for own rows  s = w + beta s, p = u + beta p, x += alpha p, r -= alpha s, u = dinv r;
+// the SpMV w = A u gathers u at neighbour rows by recomputing it from the previous
+// iteration's r, s, w (double-buffered, so no block races the writers), and the block
+// partials of (r,u), (w,u), (r,r) feed the next barrier.
+struct Cg1Args {
+    int64_t n;
+    const int64_t* __restrict__ rp;
+    const int32_t* __restrict__ ci;
+    const double* __restrict__ v;
+    const double* __restrict__ b;
+    double tol;
+    int64_t maxiter;
+    double* x;
+    double* best_x;
+    double* r[2];
+    double* s[2];
+    double* w[2];
+    double* p;
+    double* dinv;
+    double* part;   // 3 * gridDim.x partial slots
+    tt_pcg_result_t* res;
+};
+
+template <int BLOCK, int MINB>
+__global__ void __launch_bounds__(BLOCK, MINB) pcg_cg1_kernel(Cg1Args a) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double sh[33];
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+    const int nb = gridDim.x;
+    double* partG = a.part;
+    double* partD = a.part + nb;
+    double* partR = a.part + 2 * nb;
+    const int64_t n = a.n;
+    constexpr int kRowsPerWarp = 32 / kRowG;
+    const int64_t warp_id = tid >> 5, nwarps = nthreads >> 5;
+    const int lane = threadIdx.x & 31;
+    const int sub = lane % kRowG;
+
+    // init: dinv, x = 0, p = 0, s_old = 0 (so iteration 0 gives p = u0, s = w0), r0 = b
+    for (int64_t i = tid; i < n; i += nthreads) {
+        double d = 0.0;
+        for (int64_t q = a.rp[i]; q < a.rp[i + 1]; ++q)
+            if (a.ci[q] == i) d = a.v[q];
+        a.dinv[i] = 1.0 / d;
+        a.x[i] = 0.0;
+        a.best_x[i] = 0.0;
+        a.p[i] = 0.0;
+        a.r[0][i] = a.b[i];
+        a.s[0][i] = 0.0;
+    }
+    grid.sync();
+    // w0 = A u0 with u0 = dinv b; partials (r0,u0), (w0,u0), (r0,r0)
+    {
+        double pg = 0.0, pd = 0.0, pr = 0.0;
+        for (int64_t w0 = warp_id * kRowsPerWarp; w0 < n; w0 += nwarps * kRowsPerWarp) {
+            const int64_t i = w0 + lane / kRowG;
+            double acc = 0.0;
+            if (i < n) {
+                const double* __restrict__ dv = a.dinv;
+                const double* __restrict__ bb = a.b;
+                acc = row_dot(a.rp[i], a.rp[i + 1], sub, a.ci, a.v, [&](int c) { return dv[c] * bb[c]; });
+            }
+#pragma unroll
+            for (int off = kRowG / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+            if (i < n && sub == 0) {
+                const double ri = a.b[i], ui = a.dinv[i] * ri;
+                a.w[0][i] = acc;
+                pg += ri * ui;
+                pd += acc * ui;
+                pr += ri * ri;
+            }
+        }
+        pg = block_sum(pg, sh); if (threadIdx.x == 0) partG[blockIdx.x] = pg;
+        pd = block_sum(pd, sh); if (threadIdx.x == 0) partD[blockIdx.x] = pd;
+        pr = block_sum(pr, sh); if (threadIdx.x == 0) partR[blockIdx.x] = pr;
+    }
+    grid.sync();
+    double gamma = grid_total(partG, sh);
+    double delta = grid_total(partD, sh);
+    const double bnorm = sqrt(grid_total(partR, sh));
+    if (bnorm == 0.0) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            a.res->iterations = 0; a.res->residual = 0.0; a.res->best_residual = 0.0;
+            a.res->converged = 1; a.res->zero_rhs = 1;
+        }
+        return;
+    }
+    double best = bnorm / bnorm;  // ||r0|| / ||b||  (fem.py:136)
+    double res = best;
+    double alpha = gamma / delta, beta = 0.0;
+    int cur = 0;
+    for (int64_t it = 0; it < a.maxiter; ++it) {
+        const int nxt = cur ^ 1;
+        const double* __restrict__ r_o = a.r[cur];
+        const double* __restrict__ s_o = a.s[cur];
+        const double* __restrict__ w_o = a.w[cur];
+        double* r_n = a.r[nxt];
+        double* s_n = a.s[nxt];
+        double* w_n = a.w[nxt];
+        double pg = 0.0, pd = 0.0, pr = 0.0;
+        for (int64_t w0 = warp_id * kRowsPerWarp; w0 < n; w0 += nwarps * kRowsPerWarp) {
+            const int64_t i = w0 + lane / kRowG;
+            double acc = 0.0;
+            if (i < n) {
+                const double* __restrict__ dv = a.dinv;
+                acc = row_dot(a.rp[i], a.rp[i + 1], sub, a.ci, a.v, [&](int c) {
+                    return dv[c] * (r_o[c] - alpha * (w_o[c] + beta * s_o[c]));
+                });
+            }
+#pragma unroll
+            for (int off = kRowG / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+            if (i < n && sub == 0) {
+                const double si = w_o[i] + beta * s_o[i];
+                const double ri = r_o[i] - alpha * si;
+                const double ui = a.dinv[i] * ri;
+                s_n[i] = si;
+                r_n[i] = ri;
+                w_n[i] = acc;
+                pg += ri * ui;
+                pd += acc * ui;
+                pr += ri * ri;
+            }
+        }
+        // x, p for own rows (p = u_old + beta p, x += alpha p): u_old = dinv r_old
+        for (int64_t i = tid; i < n; i += nthreads) {
+            const double pi = a.dinv[i] * r_o[i] + beta * a.p[i];
+            a.p[i] = pi;
+            a.x[i] += alpha * pi;
+        }
+        pg = block_sum(pg, sh); if (threadIdx.x == 0) partG[blockIdx.x] = pg;
+        pd = block_sum(pd, sh); if (threadIdx.x == 0) partD[blockIdx.x] = pd;
+        pr = block_sum(pr, sh); if (threadIdx.x == 0) partR[blockIdx.x] = pr;
+        grid.sync();
+        cur = nxt;
+        const double g_new = grid_total(partG, sh);
+        const double d_new = grid_total(partD, sh);
+        res = sqrt(grid_total(partR, sh)) / bnorm;
+        if (res < best) {
+            best = res;
+            for (int64_t i = tid; i < n; i += nthreads) a.best_x[i] = a.x[i];
+        }
+        if (res <= a.tol) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                a.res->iterations = it + 1; a.res->residual = res; a.res->best_residual = best;
+                a.res->converged = 1; a.res->zero_rhs = 0;
+            }
+            return;
+        }
+        beta = g_new / gamma;
+        alpha = g_new / (d_new - beta * g_new / alpha);
+        gamma = g_new;
+        delta = d_new;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        a.res->iterations = a.maxiter; a.res->residual = res; a.res->best_residual = best;
+        a.res->converged = 0; a.res->zero_rhs = 0;
+    }
+}
+
 __global__ void spmv_kernel(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
                             const double* __restrict__ v, const double* __restrict__ x,
                             double* __restrict__ y) {
@@ -311,6 +509,22 @@ __global__ void sum_parts_kernel(int nparts, const double* __restrict__ part, do
         for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
         if (threadIdx.x == 0) *out = t;
     }
+}
+
+template <int BLOCK, int MINB>
+static int cg1_launch(Cg1Args& a, int64_t n, cudaStream_t st) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg_cg1_kernel<BLOCK, MINB>, BLOCK, 0);
+    if (per_sm < 1) per_sm = 1;
+    int64_t maxb = (int64_t)sm_count() * per_sm;
+    int64_t need = (n * kRowG + BLOCK - 1) / BLOCK;
+    if (need < 1) need = 1;
+    int blocks = (int)(need < maxb ? need : maxb);
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    void* args[] = {&a};
+    cudaError_t e = cudaLaunchCooperativeKernel((void*)pcg_cg1_kernel<BLOCK, MINB>, dim3(blocks),
+                                                dim3(BLOCK), args, 0, st);
+    return cuda_status(e, "pcg_cg1_kernel (cooperative launch)");
 }
 
 template <int BLOCK, int MINB>
@@ -380,7 +594,7 @@ extern "C" int tt_mass_fill(const tt_mesh_t* m, const int64_t* inc_start, const 
     return launch_check("mass_fill_kernel");
 }
 
-extern "C" int64_t tt_pcg_workspace_doubles(int64_t n) { return 7 * n + 3 * 148 * 32 + 64; }
+extern "C" int64_t tt_pcg_workspace_doubles(int64_t n) { return 8 * n + 3 * 148 * 32 + 64; }
 
 extern "C" int tt_pcg(int64_t n, const int64_t* rp, const int32_t* ci, const double* v,
                       const double* b, double tol, int64_t maxiter, double* x, double* best_x,
@@ -388,6 +602,20 @@ extern "C" int tt_pcg(int64_t n, const int64_t* rp, const int32_t* ci, const dou
     if (n < 1 || maxiter < 0) {
         set_error("tt_pcg: bad size");
         return TT_ERR_INVALID_PARAMETER;
+    }
+    // algorithm: 0 (default) the textbook recurrence of fem.py:131-152, two barriers per
+    //            iteration; 1 Chronopoulos-Gear, one barrier but 4 gathers per nonzero
+    //            (measured slower on B200: a grid barrier costs ~1.2 us, the gathers more)
+    static int algo = [] { const char* v = getenv("TT_PCG_ALGO"); return v ? atoi(v) : 0; }();
+    if (algo == 1) {
+        Cg1Args c;
+        c.n = n; c.rp = rp; c.ci = ci; c.v = v; c.b = b; c.tol = tol; c.maxiter = maxiter;
+        c.x = x; c.best_x = best_x;
+        c.r[0] = work; c.r[1] = work + n; c.s[0] = work + 2 * n; c.s[1] = work + 3 * n;
+        c.w[0] = work + 4 * n; c.w[1] = work + 5 * n; c.p = work + 6 * n; c.dinv = work + 7 * n;
+        c.part = work + 8 * n;
+        c.res = result;
+        return cg1_launch<512, 2>(c, n, as_stream(stream));
     }
     PcgArgs a;
     a.n = n; a.rp = rp; a.ci = ci; a.v = v; a.b = b; a.tol = tol; a.maxiter = maxiter;

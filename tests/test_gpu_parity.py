@@ -442,3 +442,19 @@ def test_torus_pair_snap_heavy_3d(tt):
     with pytest.raises(tt.SourceEvalFailed):
         tt.assemble_load_mc(tgt, tt.MeshBackedField(fs, outside="strict"), plan)
     _walk_vs_scan(tt, tgt, src, 40, 3)
+
+
+def test_pcg_algorithms_agree(tt, golden, c1):
+    """Both device PCG recurrences (textbook, Chronopoulos-Gear) reach the reference x."""
+    import subprocess, sys, json
+    code = ("import numpy as np, json, sys; sys.path.insert(0, '.'); import paper_2603_00538_b200 as tt;"
+            "z = np.load('tests/golden/ref_2d.npz');"
+            "t = tt.TriMesh.from_arrays(z['c1t_nodes'], z['c1t_elements']);"
+            "x = tt.cg_solve(tt.assemble_mass_matrix(t), z['b_c1_mesh_smooth'], tol=1e-14);"
+            "print(json.dumps(float(np.max(np.abs(x - z['x_c1_mesh_tol14'])))))")
+    import os
+    for algo in ("0", "1"):
+        out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                             env=dict(os.environ, TT_PCG_ALGO=algo), cwd=str(__import__('pathlib').Path(__file__).resolve().parents[1]))
+        assert out.returncode == 0, out.stderr
+        assert json.loads(out.stdout.strip().splitlines()[-1]) <= 1e-12
