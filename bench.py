@@ -94,48 +94,74 @@ def workload_config(args, world):
 
 # --------------------------------------------------------------------- clocks
 class ClockSampler:
+    """SM clock + throttle reasons sampled DURING the timed region: an NVML polling
+    thread (every ~2 ms) with an nvidia-smi -lms 100 fallback."""
+
+    _REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+                "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+
     def __init__(self, index=0):
-        self.proc = None
         self.index = index
-        self.path = ROOT / "gpurun_out" / f"clocks_bench_{os.getpid()}.csv"
+        self.samples = []
+        self.max_mhz = None
+        self.proc = None
+        self.thread = None
 
     def __enter__(self):
+        import threading
         try:
-            self.path.parent.mkdir(exist_ok=True)
-            self.fh = open(self.path, "w")
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}",
-                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.fh,
-                stderr=subprocess.DEVNULL)
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            self.stop = threading.Event()
+
+            def run():
+                while not self.stop.is_set():
+                    try:
+                        mhz = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.samples.append((float(mhz), int(rs)))
+                    except Exception:
+                        pass
+                    self.stop.wait(0.002)
+            self.thread = threading.Thread(target=run, daemon=True)
+            self.thread.start()
         except Exception:
-            self.proc = None
+            try:
+                self.path = ROOT / "gpurun_out" / f"clocks_bench_{os.getpid()}.csv"
+                self.path.parent.mkdir(exist_ok=True)
+                self.fh = open(self.path, "w")
+                self.proc = subprocess.Popen(
+                    ["nvidia-smi", f"--id={self.index}", "--query-gpu=clocks.sm,clocks.max.sm,"
+                     "clocks_event_reasons.active", "--format=csv,noheader,nounits", "-lms", "100"],
+                    stdout=self.fh, stderr=subprocess.DEVNULL)
+            except Exception:
+                self.proc = None
         return self
 
     def __exit__(self, *a):
+        if self.thread is not None:
+            self.stop.set()
+            self.thread.join()
         if self.proc:
             self.proc.terminate()
             self.proc.wait()
             self.fh.close()
+            try:
+                for row in self.path.read_text().strip().splitlines():
+                    mhz, mx, act = (x.strip() for x in row.split(","))
+                    self.max_mhz = float(mx)
+                    self.samples.append((float(mhz), int(act, 16)))
+            except Exception:
+                pass
 
     def summary(self):
-        try:
-            rows = [r.split(",") for r in self.path.read_text().strip().splitlines() if r.strip()]
-        except Exception:
-            rows = []
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in rows]
-        reasons = set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in rows:
-            for nm, v in zip(names, r[3:7]):
-                if v.strip() == "Active":
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][1]),
-                "reasons": sorted(reasons), "samples": len(rows)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"]}
+        reasons = sorted({n for _, r in self.samples for n, bit in self._REASONS.items() if r & bit})
+        return {"sm_mhz": statistics.median(m for m, _ in self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.samples), "source": "nvml" if self.thread else "nvidia-smi"}
 
 
 # --------------------------------------------------------------------- ours

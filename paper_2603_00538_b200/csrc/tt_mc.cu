@@ -638,7 +638,8 @@ static int launch_mc(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_pl
             kernel<<<(unsigned)blocks, block, 0, st>>>(td, e_lo, e_hi, pd, sd, contrib, b, nullptr, status);
         };
         if ((variant & 4) && sd.grid.wrec && sd.egrad && sd.grid.walk && sd.seeds) {
-            launch(mc_mesh_kernel<D, PLAN, G, true, 2, true>);
+            if (variant & 8) launch(mc_mesh_kernel<D, PLAN, G, true, 3, true>);
+            else launch(mc_mesh_kernel<D, PLAN, G, true, 2, true>);
             return launch_check("mc_mesh_kernel (float walk)");
         }
         switch (variant & 3) {
