@@ -1,0 +1,172 @@
+"""GPU: the reference's own unit tests for the MC path, run against this framework
+(test_montecarlo.py, test_locate.py, test_fem.py, test_transfer.py, test_sobol.py of
+/root/reference/pkg/tests, restated)."""
+
+import numpy as np
+import pytest
+from scipy.stats import chi2
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def tt():
+    import paper_2603_00538_b200 as tt
+    return tt
+
+
+@pytest.fixture(scope="module")
+def small_pair(tt):
+    source = tt.generate_square_mesh(6, 0.2, seed=10, diagonal="left")
+    target = tt.generate_square_mesh(6, 0.2, seed=20, diagonal="right")
+    return target, source
+
+
+@pytest.fixture(scope="module")
+def matching_mesh(tt):
+    return tt.generate_square_mesh(5, 0.15, seed=7, diagonal="left")
+
+
+def test_bary_map_corners_and_validity(tt):                     # test_montecarlo.py:24-33
+    lam = tt.bary_map(np.array([0.0, 1.0 - 1e-16, 1.0 - 1e-16]), np.array([0.0, 0.0, 1.0 - 1e-16]))
+    np.testing.assert_allclose(lam[0], [1, 0, 0], atol=1e-8)
+    np.testing.assert_allclose(lam[1], [0, 1, 0], atol=1e-8)
+    np.testing.assert_allclose(lam[2], [0, 0, 1], atol=1e-8)
+    rng = np.random.default_rng(0)
+    lam = tt.bary_map(rng.random(10000), rng.random(10000))
+    assert np.all(lam >= 0) and np.all(lam <= 1)
+    np.testing.assert_allclose(lam.sum(axis=1), 1.0, atol=1e-14)
+    lam3 = tt.bary_map(rng.random(10000), rng.random(10000), rng.random(10000))
+    assert np.all(lam3 >= 0) and np.all(lam3 <= 1)
+    np.testing.assert_allclose(lam3.sum(axis=1), 1.0, atol=1e-14)
+
+
+def test_bary_map_is_area_uniform(tt):                          # test_montecarlo.py:36-61
+    n = 40000
+    rng = np.random.default_rng(7)
+    lam = tt.bary_map(rng.random(n), rng.random(n))
+    sigma = np.sqrt(1.0 / 18.0 / n)
+    assert np.all(np.abs(lam.mean(axis=0) - 1.0 / 3.0) < 3 * sigma)
+    x, y = lam[:, 1], lam[:, 2]
+    i = np.minimum((4 * x).astype(int), 3)
+    j = np.minimum((4 * y).astype(int), 3)
+    up = ((4 * x - i) + (4 * y - j)) > 1.0
+    counts = np.bincount((i * 4 + j) * 2 + up, minlength=32)
+    occupied = [(ii * 4 + jj) * 2 + u for ii in range(4) for jj in range(4) for u in (0, 1)
+                if ii + jj <= (3 - u)]
+    assert counts[occupied].sum() == n
+    c = counts[occupied]
+    assert float(((c - n / 16.0) ** 2 / (n / 16.0)).sum()) < chi2.ppf(0.999, df=15)
+
+
+def test_tet_bary_map_is_volume_uniform(tt):
+    """3-D extension: the corner sub-tets of the 2x refinement get 1/8 of the samples."""
+    n = 64000
+    rng = np.random.default_rng(3)
+    lam = tt.bary_map(rng.random(n), rng.random(n), rng.random(n))
+    corner = (lam >= 0.5).any(axis=1)
+    which = np.argmax(lam, axis=1)[corner]
+    counts = np.bincount(which, minlength=4)
+    expect = n / 8.0
+    assert float(((counts - expect) ** 2 / expect).sum()) < chi2.ppf(0.999, df=3)
+    assert abs(corner.mean() - 0.5) < 4 * np.sqrt(0.25 / n)
+
+
+def test_mesh_backed_field_matches_interpolant(tt, small_pair):  # test_montecarlo.py:126-132
+    _, source_mesh = small_pair
+    nodal = tt.NodalField.from_function(source_mesh, lambda x, y: 2 * x - y)
+    f = tt.MeshBackedField(nodal)
+    pts = np.random.default_rng(4).random((200, 2))
+    np.testing.assert_allclose(f(pts), 2 * pts[:, 0] - pts[:, 1], atol=1e-12)
+
+
+def test_plan_determinism(tt):                                   # test_montecarlo.py:162-170
+    a = tt.SamplePlan.build(128, mode="uniform", seed=5)
+    b = tt.SamplePlan.build(128, mode="uniform", seed=5)
+    assert np.array_equal(a.parametric, b.parametric)
+    c = tt.SamplePlan.build(128, mode="sobol", seed=3)
+    d = tt.SamplePlan.build(128, mode="sobol", seed=3)
+    assert np.array_equal(c.barycentric, d.barycentric)
+    assert not np.array_equal(a.parametric, tt.SamplePlan.build(128, "uniform", 6).parametric)
+
+
+def test_locate_single_point(tt):                                # test_locate.py:64-69
+    m = tt.generate_square_mesh(6, 0.3, seed=4, diagonal="alternating")
+    loc = tt.UniformGridLocator.build(m)
+    hit = loc.locate(np.array([0.41, 0.37]))
+    assert hit is not None
+    elem, lam = hit
+    assert lam.min() >= -1e-12 and lam.sum() == pytest.approx(1.0)
+    assert loc.locate(np.array([2.0, 2.0])) is None
+    assert np.all(loc.locate_many(np.array([[-0.5, 0.5], [1.5, 1.5]]))[0] == tt.OUTSIDE)
+
+
+def test_integrate_field_exact_for_linear(tt, matching_mesh):    # test_fem.py:71-75
+    field = tt.NodalField.from_function(matching_mesh, lambda x, y: 2 * x - y + 3)
+    assert tt.integrate_field(field) == pytest.approx(3.5, abs=1e-14)
+    assert tt.basis_integrals(matching_mesh).sum() == pytest.approx(1.0)
+
+
+def test_field_validation(tt, matching_mesh):                    # test_fem.py:78-84
+    with pytest.raises(tt.DimensionMismatch):
+        tt.NodalField(matching_mesh, np.zeros(3))
+    bad = np.zeros(matching_mesh.n_nodes)
+    bad[0] = np.nan
+    with pytest.raises(tt.DimensionMismatch):
+        tt.NodalField(matching_mesh, bad)
+
+
+def test_eval_in_elements(tt, matching_mesh):                    # test_fem.py:87-94
+    field = tt.NodalField.from_function(matching_mesh, lambda x, y: x * 2 + y)
+    rng = np.random.default_rng(1)
+    elems = rng.integers(0, matching_mesh.n_elems, 20).astype(np.int32)
+    lam = rng.dirichlet(np.ones(3), 20)
+    pts = matching_mesh.points_from_barycentric(elems, lam)
+    np.testing.assert_allclose(field.eval_in_elements(elems, lam), pts[:, 0] * 2 + pts[:, 1], atol=1e-12)
+
+
+def test_cg_matches_dense_solve(tt, matching_mesh):              # test_fem.py:47-53
+    M = tt.assemble_mass_matrix(matching_mesh)
+    b = np.random.default_rng(3).standard_normal(matching_mesh.n_nodes)
+    x = tt.cg_solve(M, b, tol=1e-13)
+    np.testing.assert_allclose(x, np.linalg.solve(M.csr.toarray(), b), rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(M @ x, b, atol=1e-12)
+
+
+def test_mc_operator_matrix_matches_sampled_path(tt, small_pair):  # test_transfer.py:48-59
+    target, source_mesh = small_pair
+    field = tt.NodalField.from_function(source_mesh, lambda x, y: np.sin(2 * x) - y)
+    op = tt.MCTransferOperator(target, source_mesh, tt.SamplePlan.build(400, mode="sobol", seed=0))
+    np.testing.assert_allclose(op.apply(field).coeffs,
+                               op.apply_sampled(tt.MeshBackedField(field)).coeffs, atol=1e-12)
+
+
+def test_mc_conserves_sampled_mass(tt, small_pair):              # test_transfer.py:71-83
+    target, _ = small_pair
+    source = tt.AnalyticField(lambda x, y: x ** 2 + 0.5)
+    plan = tt.SamplePlan.build(512, mode="sobol", seed=0)
+    out = tt.transfer_mc(target, source, plan, cg_tol=1e-13)
+    pts = np.einsum("nj,ejd->end", plan.barycentric, target.elem_coords)
+    f = source(pts.reshape(-1, 2)).reshape(target.n_elems, plan.n_samples)
+    sample_mass = float((target.elem_areas / plan.n_samples) @ f.sum(axis=1))
+    assert tt.integrate_field(out) == pytest.approx(sample_mass, rel=1e-11)
+
+
+def test_mc_accuracy_improves_with_samples(tt, small_pair):       # test_transfer.py:86-96
+    target, source_mesh = small_pair
+    field = tt.NodalField.from_function(source_mesh, lambda x, y: np.sin(4 * x) * np.cos(3 * y))
+    exact = tt.MCTransferOperator(target, source_mesh, tt.SamplePlan.build(65536, "sobol", 0)).apply(field)
+    errs = []
+    for n in (64, 4096):
+        out = tt.MCTransferOperator(target, source_mesh, tt.SamplePlan.build(n, "sobol", 0)).apply(field)
+        errs.append(np.linalg.norm(out.coeffs - exact.coeffs))
+    assert errs[1] < errs[0] / 4
+
+
+def test_msh_round_trip_through_device(tt, tmp_path):
+    m = tt.generate_cube_mesh(3, 0.2, seed=2)
+    tt.save_msh(m, tmp_path / "c.msh")
+    r = tt.load_msh(tmp_path / "c.msh")
+    f1 = tt.NodalField.from_function(m, lambda x, y, z: x + y * z)
+    f2 = tt.NodalField.from_function(r, lambda x, y, z: x + y * z)
+    assert tt.integrate_field(f1) == tt.integrate_field(f2)
