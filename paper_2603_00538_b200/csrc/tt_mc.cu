@@ -259,8 +259,9 @@ __device__ __forceinline__ void plan_lambda(const PlanDev& plan, int64_t e, int6
 // many steps individual samples need; the assignment is a deterministic function of the
 // data, so results are bitwise reproducible.  Identical ids/lambdas as the reference scan
 // (certified walk, see locate_walk in tt_common.cuh).
-template <int D, int PLAN, int G, bool SPEC, int MINB, bool FW = false>
-__global__ void __launch_bounds__(256, MINB) mc_mesh_kernel(TargetDev t, int64_t e_lo, int64_t e_hi,
+template <int D, int PLAN, int G, bool SPEC, int MINB, bool FW = false, int BLOCK = 256,
+          bool SMEMV = false>
+__global__ void __launch_bounds__(BLOCK, MINB) mc_mesh_kernel(TargetDev t, int64_t e_lo, int64_t e_hi,
                                                       PlanDev plan, SrcDev src,
                                                       double* __restrict__ contrib,
                                                       double* __restrict__ b,
@@ -289,9 +290,24 @@ __global__ void __launch_bounds__(256, MINB) mc_mesh_kernel(TargetDev t, int64_t
         double acc[K];
 #pragma unroll
         for (int i = 0; i < K; ++i) acc[i] = 0.0;
-        double v[K][D];
-        int seed[K + 1];
-        if (active) {
+        if constexpr (SMEMV) __syncwarp();
+        // SMEMV: the element's vertices and walk seeds live in shared memory (read at each
+        // sample start) instead of 24 + 5 registers -> more resident warps per SM
+        constexpr int NW = BLOCK / 32;
+        __shared__ double s_v[SMEMV ? NW : 1][SMEMV ? EPW : 1][SMEMV ? K * D : 1];
+        __shared__ int s_seed[SMEMV ? NW : 1][SMEMV ? EPW : 1][SMEMV ? K + 1 : 1];
+        const int wib = threadIdx.x >> 5, gib = lane / G;
+        double v[SMEMV ? 1 : K][D];
+        int seed[SMEMV ? 1 : K + 1];
+        if constexpr (SMEMV) {
+            if (active) {
+                for (int q = sub_lane; q < K * D; q += G)
+                    s_v[wib][gib][q] = __ldg(t.nodes + (int64_t)__ldg(t.elems + e * K + q / D) * D + q % D);
+                if (walk)
+                    for (int q = sub_lane; q <= K; q += G) s_seed[wib][gib][q] = __ldg(src.seeds + e * (K + 1) + q);
+            }
+            __syncwarp();
+        } else if (active) {
             load_elem<D>(t, e, v);
             if (walk) {
 #pragma unroll
@@ -310,7 +326,14 @@ __global__ void __launch_bounds__(256, MINB) mc_mesh_kernel(TargetDev t, int64_t
                 const int64_t j = next + __popc(m & lt);
                 if (j < N) {
                     plan_lambda<D, PLAN>(plan, e, j, lam);
-                    map_point<D>(lam, v, x);
+                    if constexpr (SMEMV) {
+                        double vv[K][D];
+#pragma unroll
+                        for (int q = 0; q < K * D; ++q) vv[q / D][q % D] = s_v[wib][gib][q];
+                        map_point<D>(lam, vv, x);
+                    } else {
+                        map_point<D>(lam, v, x);
+                    }
                     cur = -1;
                     if (walk) {
                         int imax = 0;
@@ -318,10 +341,14 @@ __global__ void __launch_bounds__(256, MINB) mc_mesh_kernel(TargetDev t, int64_t
 #pragma unroll
                         for (int i = 1; i < K; ++i)
                             if (lam[i] > lmax) { lmax = lam[i]; imax = i; }
-                        cur = seed[0];
+                        if constexpr (SMEMV) {
+                            cur = s_seed[wib][gib][lmax > 0.45 ? 1 + imax : 0];
+                        } else {
+                            cur = seed[0];
 #pragma unroll
-                        for (int i = 0; i < K; ++i)
-                            if (lmax > 0.45 && imax == i) cur = seed[1 + i];
+                            for (int i = 0; i < K; ++i)
+                                if (lmax > 0.45 && imax == i) cur = seed[1 + i];
+                        }
                     }
                     steps = 0;
                     jcur = j;
@@ -628,7 +655,7 @@ static int launch_mc(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_pl
     if constexpr (SRC == TT_SRC_MESH) {
         // variant: bit0 = speculative coefficient prefetch, bit1 = 3 blocks/SM register target,
         // bit2 = compact float walk + gradient evaluation (needs grid.wrec and elem_grad)
-        static int variant = [] { const char* v = getenv("TT_MC_VARIANT"); return v ? atoi(v) : 5; }();
+        static int variant = [] { const char* v = getenv("TT_MC_VARIANT"); return v ? atoi(v) : 21; }();
         auto launch = [&](auto kernel) {
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, 0);
             if (per_sm < 1) per_sm = 1;
@@ -638,6 +665,22 @@ static int launch_mc(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_pl
             kernel<<<(unsigned)blocks, block, 0, st>>>(td, e_lo, e_hi, pd, sd, contrib, b, nullptr, status);
         };
         if ((variant & 4) && sd.grid.wrec && sd.egrad && sd.grid.walk && sd.seeds) {
+            if (variant & 16) {
+                // 128-thread blocks, vertices/seeds in shared memory, 5 (or 6) blocks per SM
+                auto launch128 = [&](auto kernel) {
+                    int per = 0;
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, 128, 0);
+                    if (per < 1) per = 1;
+                    int64_t nb = (tiles + 3) / 4;
+                    const int64_t cap = (int64_t)sm_count() * per * 16;
+                    if (nb > cap) nb = cap;
+                    if (nb < 1) nb = 1;
+                    kernel<<<(unsigned)nb, 128, 0, st>>>(td, e_lo, e_hi, pd, sd, contrib, b, nullptr, status);
+                };
+                if (variant & 32) launch128(mc_mesh_kernel<D, PLAN, G, true, 6, true, 128, true>);
+                else launch128(mc_mesh_kernel<D, PLAN, G, true, 5, true, 128, true>);
+                return launch_check("mc_mesh_kernel (float walk, smem)");
+            }
             if (variant & 8) launch(mc_mesh_kernel<D, PLAN, G, true, 3, true>);
             else launch(mc_mesh_kernel<D, PLAN, G, true, 2, true>);
             return launch_check("mc_mesh_kernel (float walk)");
@@ -785,20 +828,21 @@ extern "C" int tt_mc_cache_ids(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, c
     // the float-walk kernel when the grid carries compact walk records (the default load
     // path), else the double walk; either way the ids are the reference scan's
     const bool fw = g->wrec && g->walk && seeds;
+    const unsigned nb128 = grid_for(tiles * 32, 128);  // same launch shape as the default load
     if (t->dim == 2) {
         if (p->kind == TT_PLAN_SHARED) {
-            if (fw) mc_mesh_kernel<2, TT_PLAN_SHARED, 8, true, 2, true><<<nb, 256, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
+            if (fw) mc_mesh_kernel<2, TT_PLAN_SHARED, 8, true, 5, true, 128, true><<<nb128, 128, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
             else mc_mesh_kernel<2, TT_PLAN_SHARED, 8, false, 2><<<nb, 256, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
         } else {
-            if (fw) mc_mesh_kernel<2, TT_PLAN_PHILOX, 8, true, 2, true><<<nb, 256, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
+            if (fw) mc_mesh_kernel<2, TT_PLAN_PHILOX, 8, true, 5, true, 128, true><<<nb128, 128, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
             else mc_mesh_kernel<2, TT_PLAN_PHILOX, 8, false, 2><<<nb, 256, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
         }
     } else {
         if (p->kind == TT_PLAN_SHARED) {
-            if (fw) mc_mesh_kernel<3, TT_PLAN_SHARED, 8, true, 2, true><<<nb, 256, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
+            if (fw) mc_mesh_kernel<3, TT_PLAN_SHARED, 8, true, 5, true, 128, true><<<nb128, 128, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
             else mc_mesh_kernel<3, TT_PLAN_SHARED, 8, false, 2><<<nb, 256, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
         } else {
-            if (fw) mc_mesh_kernel<3, TT_PLAN_PHILOX, 8, true, 2, true><<<nb, 256, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
+            if (fw) mc_mesh_kernel<3, TT_PLAN_PHILOX, 8, true, 5, true, 128, true><<<nb128, 128, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
             else mc_mesh_kernel<3, TT_PLAN_PHILOX, 8, false, 2><<<nb, 256, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
         }
     }
