@@ -273,6 +273,16 @@ int tt_pcg(int64_t n, const int64_t* row_ptr, const int32_t* cols, const double*
            const double* b, double tol, int64_t maxiter, double* x, double* best_x,
            double* work /* tt_pcg_workspace_doubles(n) */, tt_pcg_result_t* result /* device */,
            void* stream);
+/* ELL form of the mass matrix (width 16, padding (row, 0.0)) and the PCG over it; the
+ * same recurrence as tt_pcg with the row-pointer round trip removed from every SpMV row.
+ * TT_FLAG_CAPACITY in *status when a row has more than 16 entries (use tt_pcg then). */
+int tt_csr_to_ell(int64_t n, const int64_t* row_ptr, const int32_t* cols, const double* vals,
+                  int width, int32_t* ell_cols /* (n, 16) */, double* ell_vals /* (n, 16) */,
+                  double* diag /* (n,) */, int32_t* status, void* stream);
+int tt_pcg_ell(int64_t n, const int32_t* ell_cols, const double* ell_vals, const double* diag,
+               const double* b, double tol, int64_t maxiter, double* x, double* best_x,
+               double* work /* tt_pcg_workspace_doubles(n) */, tt_pcg_result_t* result,
+               void* stream);
 int tt_spmv(int64_t n, const int64_t* row_ptr, const int32_t* cols, const double* vals,
             const double* x, double* y, void* stream);
 

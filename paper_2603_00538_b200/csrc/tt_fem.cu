@@ -472,6 +472,171 @@ __global__ void __launch_bounds__(BLOCK, MINB) pcg_cg1_kernel(Cg1Args a) {
     }
 }
 
+// ---------------------------------------------------------------- ELL variant of the PCG
+// Fixed-width rows (width W = 16: every row of these P1 mass matrices has <= 16 entries,
+// padding = (row, 0.0)), diagonal stored separately.  4 lanes per row; lane `sub` owns
+// entries [4 sub, 4 sub + 4): one int4 column load and two double2 value loads, no row
+// pointer round trip, then 4 independent gathers.
+__global__ void csr_to_ell_kernel(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                  const double* __restrict__ v, int W, int32_t* __restrict__ ec,
+                                  double* __restrict__ ev, double* __restrict__ diag,
+                                  int32_t* __restrict__ status) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t q0 = rp[i], len = rp[i + 1] - q0;
+    if (len > W) { atomicOr(status, TT_FLAG_CAPACITY); return; }
+    double d = 0.0;
+    for (int t = 0; t < W; ++t) {
+        const bool in = t < len;
+        const int c = in ? ci[q0 + t] : (int)i;
+        const double a = in ? v[q0 + t] : 0.0;
+        if (in && c == i) d = a;
+        ec[i * W + t] = c;
+        ev[i * W + t] = a;
+    }
+    diag[i] = d;
+}
+
+struct EllArgs {
+    int64_t n;
+    const int32_t* __restrict__ ec;
+    const double* __restrict__ ev;
+    const double* __restrict__ diag;
+    const double* __restrict__ b;
+    double tol;
+    int64_t maxiter;
+    double* x;
+    double* best_x;
+    double* r;
+    double* z;
+    double* p0;
+    double* p1;
+    double* ap;
+    double* dinv;
+    double* part;
+    tt_pcg_result_t* res;
+};
+
+template <class Col>
+__device__ __forceinline__ double ell_row16(const int32_t* __restrict__ ec, const double* __restrict__ ev,
+                                           int64_t i, int sub, Col col) {
+    const int4 c = __ldg(reinterpret_cast<const int4*>(ec + i * 16) + sub);
+    const double2 a0 = __ldg(reinterpret_cast<const double2*>(ev + i * 16 + 4 * sub));
+    const double2 a1 = __ldg(reinterpret_cast<const double2*>(ev + i * 16 + 4 * sub) + 1);
+    const double x0 = col(c.x), x1 = col(c.y), x2 = col(c.z), x3 = col(c.w);
+    return fma(a1.y, x3, fma(a1.x, x2, fma(a0.y, x1, a0.x * x0)));
+}
+
+template <int BLOCK, int MINB>
+__global__ void __launch_bounds__(BLOCK, MINB) pcg_ell_kernel(EllArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double sh[33];
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+    const int nb = gridDim.x;
+    double* partA = a.part;
+    double* partB = a.part + nb;
+    double* partC = a.part + 2 * nb;
+    const int64_t n = a.n;
+    double bb = 0.0, rz_p = 0.0;
+    for (int64_t i = tid; i < n; i += nthreads) {
+        const double di = 1.0 / a.diag[i];
+        const double bi = a.b[i];
+        a.dinv[i] = di;
+        a.x[i] = 0.0;
+        a.best_x[i] = 0.0;
+        a.r[i] = bi;
+        const double zi = di * bi;
+        a.z[i] = zi;
+        a.p0[i] = 0.0;
+        bb += bi * bi;
+        rz_p += bi * zi;
+    }
+    bb = block_sum(bb, sh);
+    if (threadIdx.x == 0) partB[blockIdx.x] = bb;
+    rz_p = block_sum(rz_p, sh);
+    if (threadIdx.x == 0) partC[blockIdx.x] = rz_p;
+    grid.sync();
+    const double bnorm = sqrt(grid_total(partB, sh));
+    double rz = grid_total(partC, sh);
+    if (bnorm == 0.0) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            a.res->iterations = 0; a.res->residual = 0.0; a.res->best_residual = 0.0;
+            a.res->converged = 1; a.res->zero_rhs = 1;
+        }
+        return;
+    }
+    double best = bnorm / bnorm;
+    double res = best;
+    double beta = 0.0;
+    const int64_t group = tid >> 2, ngroups = nthreads >> 2;
+    const int sub = threadIdx.x & 3;
+    double* p_old = a.p0;
+    double* p_new = a.p1;
+    for (int64_t it = 0; it < a.maxiter; ++it) {
+        double pap = 0.0;
+        // rows are processed by 4-lane groups; the loop trip count is uniform per warp
+        for (int64_t i0 = (group & ~7LL); i0 < n; i0 += ngroups) {
+            const int64_t i = i0 + (group & 7);
+            double s = 0.0;
+            if (i < n) {
+                const double* __restrict__ z = a.z;
+                const double* __restrict__ po = p_old;
+                s = ell_row16(a.ec, a.ev, i, sub, [&](int c) { return z[c] + beta * po[c]; });
+            }
+            s += __shfl_xor_sync(0xffffffffu, s, 1);
+            s += __shfl_xor_sync(0xffffffffu, s, 2);
+            if (i < n && sub == 0) {
+                const double pi = a.z[i] + beta * p_old[i];
+                p_new[i] = pi;
+                a.ap[i] = s;
+                pap += pi * s;
+            }
+        }
+        pap = block_sum(pap, sh);
+        if (threadIdx.x == 0) partA[blockIdx.x] = pap;
+        grid.sync();
+        const double alpha = rz / grid_total(partA, sh);
+        double rr = 0.0, rzn = 0.0;
+        for (int64_t i = tid; i < n; i += nthreads) {
+            const double pi = p_new[i];
+            const double xi = a.x[i] + alpha * pi;
+            const double ri = a.r[i] - alpha * a.ap[i];
+            const double zi = a.dinv[i] * ri;
+            a.x[i] = xi;
+            a.r[i] = ri;
+            a.z[i] = zi;
+            rr += ri * ri;
+            rzn += ri * zi;
+        }
+        rr = block_sum(rr, sh);
+        if (threadIdx.x == 0) partB[blockIdx.x] = rr;
+        rzn = block_sum(rzn, sh);
+        if (threadIdx.x == 0) partC[blockIdx.x] = rzn;
+        grid.sync();
+        res = sqrt(grid_total(partB, sh)) / bnorm;
+        const double rz_new = grid_total(partC, sh);
+        if (res < best) {
+            best = res;
+            for (int64_t i = tid; i < n; i += nthreads) a.best_x[i] = a.x[i];
+        }
+        if (res <= a.tol) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                a.res->iterations = it + 1; a.res->residual = res; a.res->best_residual = best;
+                a.res->converged = 1; a.res->zero_rhs = 0;
+            }
+            return;
+        }
+        beta = rz_new / rz;
+        rz = rz_new;
+        double* t = p_old; p_old = p_new; p_new = t;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        a.res->iterations = a.maxiter; a.res->residual = res; a.res->best_residual = best;
+        a.res->converged = 0; a.res->zero_rhs = 0;
+    }
+}
+
 __global__ void spmv_kernel(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
                             const double* __restrict__ v, const double* __restrict__ x,
                             double* __restrict__ y) {
@@ -667,4 +832,44 @@ extern "C" int tt_integrate_p1(const tt_mesh_t* m, const double* coeffs, double*
     st = launch_check("integrate kernels");
     cudaFreeAsync(part, s);
     return st;
+}
+
+extern "C" int tt_csr_to_ell(int64_t n, const int64_t* rp, const int32_t* ci, const double* v, int width,
+                             int32_t* ell_cols, double* ell_vals, double* diag, int32_t* status,
+                             void* stream) {
+    if (n < 1 || width != 16) {
+        set_error("tt_csr_to_ell: width must be 16");
+        return TT_ERR_INVALID_PARAMETER;
+    }
+    csr_to_ell_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(n, rp, ci, v, width, ell_cols, ell_vals,
+                                                                        diag, status);
+    return launch_check("csr_to_ell_kernel");
+}
+
+extern "C" int tt_pcg_ell(int64_t n, const int32_t* ell_cols, const double* ell_vals, const double* diag,
+                          const double* b, double tol, int64_t maxiter, double* x, double* best_x,
+                          double* work, tt_pcg_result_t* result, void* stream) {
+    if (n < 1 || maxiter < 0) {
+        set_error("tt_pcg_ell: bad size");
+        return TT_ERR_INVALID_PARAMETER;
+    }
+    EllArgs a;
+    a.n = n; a.ec = ell_cols; a.ev = ell_vals; a.diag = diag; a.b = b; a.tol = tol; a.maxiter = maxiter;
+    a.x = x; a.best_x = best_x;
+    a.r = work; a.z = work + n; a.p0 = work + 2 * n; a.p1 = work + 3 * n; a.ap = work + 4 * n;
+    a.dinv = work + 5 * n;
+    a.part = work + 6 * n;
+    a.res = result;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg_ell_kernel<512, 2>, 512, 0);
+    if (per_sm < 1) per_sm = 1;
+    int64_t maxb = (int64_t)sm_count() * per_sm;
+    int64_t need = (n * 4 + 511) / 512;
+    if (need < 1) need = 1;
+    int blocks = (int)(need < maxb ? need : maxb);
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    void* args[] = {&a};
+    cudaError_t e = cudaLaunchCooperativeKernel((void*)pcg_ell_kernel<512, 2>, dim3(blocks), dim3(512), args,
+                                                0, as_stream(stream));
+    return cuda_status(e, "pcg_ell_kernel (cooperative launch)");
 }

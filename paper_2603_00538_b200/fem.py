@@ -157,6 +157,24 @@ class SparseSymMatrix:
 
     __matmul__ = matvec
 
+    def ell(self):
+        """(cols (n,16) i32, vals (n,16) f64, diag (n,)) when every row has <= 16 entries
+        (the P1 mass matrices of the generated meshes), else None -> CSR PCG."""
+        if not hasattr(self, "_ell"):
+            self._ell = None
+            if int((self.row_ptr_dev[1:] - self.row_ptr_dev[:-1]).max().item()) <= 16:
+                dev = self.vals_dev.device
+                ec = torch.empty((self.n, 16), dtype=torch.int32, device=dev)
+                ev = torch.empty((self.n, 16), dtype=torch.float64, device=dev)
+                dg = torch.empty(self.n, dtype=torch.float64, device=dev)
+                st = _lib.status_word()
+                _lib.call("tt_csr_to_ell", self.n, _lib.ptr(self.row_ptr_dev), _lib.ptr(self.cols_dev),
+                          _lib.ptr(self.vals_dev), 16, _lib.ptr(ec), _lib.ptr(ev), _lib.ptr(dg),
+                          _lib.ptr(st), _lib.stream_handle())
+                if int(st.item()) == 0:
+                    self._ell = (ec, ev, dg)
+        return self._ell
+
     def workspace(self):
         if self._ws is None:
             nd = int(_lib.lib().tt_pcg_workspace_doubles(self.n))
@@ -195,6 +213,10 @@ def assemble_mass_matrix(mesh, rule: QuadratureRule | None = None) -> SparseSymM
     return SparseSymMatrix(mesh.n_nodes, row_ptr, cols, vals)
 
 
+#: "ell" (default when every row has <= 16 entries) or "csr"
+_PCG_PATH = __import__("os").environ.get("TT_PCG_PATH", "ell")
+
+
 class PcgResult:
     __slots__ = ("iterations", "residual", "best_residual", "converged", "zero_rhs")
 
@@ -208,6 +230,12 @@ def pcg_device(M: SparseSymMatrix, b: torch.Tensor, tol: float = 1e-12,
     work, res = M.workspace()
     x = x if x is not None else torch.empty(n, dtype=torch.float64, device=b.device)
     best_x = best_x if best_x is not None else torch.empty(n, dtype=torch.float64, device=b.device)
+    ell = M.ell() if _PCG_PATH != "csr" else None
+    if ell is not None:
+        _lib.call("tt_pcg_ell", n, _lib.ptr(ell[0]), _lib.ptr(ell[1]), _lib.ptr(ell[2]), _lib.ptr(b),
+                  float(tol), maxiter, _lib.ptr(x), _lib.ptr(best_x), _lib.ptr(work), _lib.ptr(res),
+                  _lib.stream_handle())
+        return x, best_x, res
     _lib.call("tt_pcg", n, _lib.ptr(M.row_ptr_dev), _lib.ptr(M.cols_dev), _lib.ptr(M.vals_dev),
               _lib.ptr(b), float(tol), maxiter, _lib.ptr(x), _lib.ptr(best_x), _lib.ptr(work),
               _lib.ptr(res), _lib.stream_handle())

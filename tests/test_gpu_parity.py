@@ -458,3 +458,23 @@ def test_pcg_algorithms_agree(tt, golden, c1):
                              env=dict(os.environ, TT_PCG_ALGO=algo), cwd=str(__import__('pathlib').Path(__file__).resolve().parents[1]))
         assert out.returncode == 0, out.stderr
         assert json.loads(out.stdout.strip().splitlines()[-1]) <= 1e-12
+
+
+def test_ell_and_csr_pcg_agree(tt, golden, c1):
+    """The ELL PCG (default when rows have <= 16 entries) and the CSR PCG reach the
+    reference x at cg_tol 1e-14."""
+    from paper_2603_00538_b200 import fem
+    import torch
+    tgt, _ = c1
+    M = tt.assemble_mass_matrix(tgt)
+    assert M.ell() is not None
+    b = torch.as_tensor(golden["b_c1_mesh_smooth"], device="cuda")
+    xs = []
+    for path in ("ell", "csr"):
+        fem._PCG_PATH = path
+        try:
+            xs.append(tt.cg_solve(M, b, tol=1e-14).cpu().numpy())
+        finally:
+            fem._PCG_PATH = "ell"
+    for x in xs:
+        assert np.max(np.abs(x - golden["x_c1_mesh_tol14"])) <= 1e-12
