@@ -24,6 +24,8 @@
  *                            (+ SourceField.__call__: AnalyticField :20-29,
  *                             MeshBackedField :49-65, NodalField.eval_in_elements fem.py:36-38)
  *   tt_mc_cache_ids       <- MCTransferOperator.__init__ localisation transfer.py:74-87
+ *   tt_mc_fold(_finish)   <- MCTransferOperator load matrix fold  transfer.py:88-110
+ *   tt_spmv_rect          <- MCTransferOperator.apply R @ c      transfer.py:112-115
  *   tt_map_points         <- einsum("nj,ejd->end")             montecarlo.py:123-124
  *   tt_eval_points        <- SourceField.__call__ on given points
  *   tt_incidence_*        <- (support for np.add.at ordering)  montecarlo.py:144-147
@@ -248,6 +250,18 @@ int tt_pack_coeffs(const tt_mesh_t* src, const double* coeffs, double* out, void
  * last vertex (the record origin), from the packed binv: g_j = sum_i binv_ij (c_i - c_last). */
 int tt_pack_grad(const tt_mesh_t* src, const double* rec, const double* coeffs, double* out,
                  void* stream);
+
+/* MCTransferOperator's sparse load matrix R (n_t x n_s, transfer.py:56-110) folded on
+ * the device from the cached sample ids (shared plans): tt_mc_fold computes it into an
+ * opaque handle and returns nnz; tt_mc_fold_finish writes the CSR (row_ptr n_t+1, cols,
+ * vals) and frees the handle.  Deterministic (stable sorts, fixed reductions). */
+int tt_mc_fold(const tt_mesh_t* target, const tt_plan_t* plan, const tt_mesh_t* src,
+               const double* src_rec, const int32_t* ids /* (E_t, N) */, int64_t* nnz_out /* host */,
+               void** handle_out /* host */, void* stream);
+int tt_mc_fold_finish(void* handle, int64_t* row_ptr, int32_t* cols, double* vals, void* stream);
+/* y = A x for a rectangular CSR (one warp per row) */
+int tt_spmv_rect(int64_t n_rows, const int64_t* row_ptr, const int32_t* cols, const double* vals,
+                 const double* x, double* y, void* stream);
 
 /* ---- node reduction / incidence (deterministic np.add.at order) ---- */
 int tt_incidence_count(const tt_mesh_t* mesh, int64_t* inc_start /* (n_nodes+1) */,

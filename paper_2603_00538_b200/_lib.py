@@ -109,6 +109,10 @@ _SIGNATURES = {
                          C.POINTER(tt_grid_t), _P, _P, _P], _I),
     "tt_pack_coeffs": ([C.POINTER(tt_mesh_t), _P, _P, _P], _I),
     "tt_pack_grad": ([C.POINTER(tt_mesh_t), _P, _P, _P, _P], _I),
+    "tt_mc_fold": ([C.POINTER(tt_mesh_t), C.POINTER(tt_plan_t), C.POINTER(tt_mesh_t), _P, _P,
+                    C.POINTER(_I64), C.POINTER(_P), _P], _I),
+    "tt_mc_fold_finish": ([_P, _P, _P, _P, _P], _I),
+    "tt_spmv_rect": ([_I64, _P, _P, _P, _P, _P, _P], _I),
     "tt_incidence_count": ([C.POINTER(tt_mesh_t), _P, _P], _I),
     "tt_incidence_fill": ([C.POINTER(tt_mesh_t), _P, _P, _P, _P], _I),
     "tt_reduce_nodes": ([_I64, _I, _P, _P, _I64, _I64, _P, _P, _P], _I),

@@ -35,7 +35,10 @@ class MCTransferOperator:
     """Monte-Carlo Galerkin projection with localisation done once (transfer.py:46-129)."""
 
     def __init__(self, target, source_mesh, plan: SamplePlan, cg_tol: float = 1e-12,
-                 source_locator: UniformGridLocator | None = None):
+                 source_locator: UniformGridLocator | None = None, fold: bool | None = None):
+        """``fold`` (default: shared plans): build the reference's sparse load matrix R
+        on the device (transfer.py:88-110) so ``apply`` is one SpMV + PCG; otherwise
+        ``apply`` re-evaluates the cached per-sample source elements (4 B/sample)."""
         if target.DIM != source_mesh.DIM or plan.dim != target.DIM:
             raise DimensionMismatch("target, source mesh and plan dimensions differ")
         self.target = target
@@ -51,17 +54,51 @@ class MCTransferOperator:
         seeds = self.locator.seeds_for(target) if self.locator.walk else None
         _lib.call("tt_mc_cache_ids", C.byref(mdesc), 0, target.n_elems, C.byref(pdesc),
                   C.byref(gdesc), _lib.ptr(seeds), _lib.ptr(self.src_elem_dev), _lib.stream_handle())
+        if fold is None:
+            fold = not plan.per_element
+        self.R = self._fold() if fold else None
+
+    def _fold(self):
+        """(row_ptr, cols, vals) of R (n_t x n_s) built on the device."""
+        dm, sm = self.target.device, self.source_mesh.device
+        mdesc, pdesc, sdesc = dm.desc(), self.plan.desc(), sm.desc()
+        nnz = C.c_int64(0)
+        handle = C.c_void_p(None)
+        s = _lib.stream_handle()
+        _lib.call("tt_mc_fold", C.byref(mdesc), C.byref(pdesc), C.byref(sdesc), _lib.ptr(sm.rec),
+                  _lib.ptr(self.src_elem_dev), C.byref(nnz), C.byref(handle), s)
+        dev = dm.nodes.device
+        rp = torch.empty(self.target.n_nodes + 1, dtype=torch.int64, device=dev)
+        ci = torch.empty(max(nnz.value, 1), dtype=torch.int32, device=dev)
+        va = torch.empty(max(nnz.value, 1), dtype=torch.float64, device=dev)
+        _lib.call("tt_mc_fold_finish", handle, _lib.ptr(rp), _lib.ptr(ci), _lib.ptr(va), s)
+        return rp, ci[:nnz.value], va[:nnz.value]
+
+    @property
+    def load_matrix(self):
+        """The folded R as a scipy CSR matrix (host copy), or None when not folded."""
+        if self.R is None:
+            return None
+        import scipy.sparse as sp
+        rp, ci, va = (t.cpu().numpy() for t in self.R)
+        return sp.csr_matrix((va, ci, rp), shape=(self.target.n_nodes, self.source_mesh.n_nodes))
 
     @property
     def _src_elem(self):
         return self.src_elem_dev.cpu().numpy()
 
     def load(self, source_field: NodalField, check: bool = True) -> torch.Tensor:
-        """b = R c on the device (cached source elements, no relocalisation)."""
+        """b = R c on the device (folded R: one SpMV; else the cached source elements)."""
         if source_field.mesh is not self.source_mesh and \
                 source_field.mesh.n_nodes != self.source_mesh.n_nodes:
             raise DimensionMismatch("field is not on the operator's source mesh")
         dm = self.target.device
+        if self.R is not None:
+            rp, ci, va = self.R
+            b = torch.empty(self.target.n_nodes, dtype=torch.float64, device=dm.nodes.device)
+            _lib.call("tt_spmv_rect", self.target.n_nodes, _lib.ptr(rp), _lib.ptr(ci), _lib.ptr(va),
+                      _lib.ptr(source_field.coeffs_dev), _lib.ptr(b), _lib.stream_handle())
+            return b
         k = self.target.DIM + 1
         s = _lib.tt_source_t()
         s.kind = _lib.TT_SRC_CACHED

@@ -119,3 +119,10 @@ g["curv_n_outside"] = np.array(int((ec < 0).sum()))
 out = ROOT / "tests" / "golden" / "ref_2d.npz"
 np.savez_compressed(out, **g)
 print(out, out.stat().st_size, "bytes;", len(g), "arrays; outside samples:", int(g["curv_n_outside"]))
+
+# the folded load matrix R of MCTransferOperator (transfer.py:88-110), C1 pair N=400
+import scipy.sparse as sp  # noqa: E402
+R = op._load_matrix.tocsr()
+fold = {"R_indptr": R.indptr, "R_indices": R.indices, "R_data": R.data, "R_shape": np.array(R.shape)}
+np.savez_compressed(ROOT / "tests" / "golden" / "ref_fold.npz", **fold)
+print("fold nnz", R.nnz)

@@ -478,3 +478,43 @@ def test_ell_and_csr_pcg_agree(tt, golden, c1):
             fem._PCG_PATH = "ell"
     for x in xs:
         assert np.max(np.abs(x - golden["x_c1_mesh_tol14"])) <= 1e-12
+
+
+def test_mc_operator_folded_load_matrix(tt, golden, c1):
+    """R folded on the device == the reference's MCTransferOperator._load_matrix
+    (transfer.py:88-110), and fold / cached-id / sampled applies agree."""
+    import scipy.sparse as sp
+    from pathlib import Path
+    tgt, src = c1
+    with np.load(Path(__file__).resolve().parent / "golden" / "ref_fold.npz") as z:
+        Rref = sp.csr_matrix((z["R_data"], z["R_indices"], z["R_indptr"]), shape=tuple(z["R_shape"]))
+    plan = tt.SamplePlan.build(400, "sobol", 0)
+    op = tt.MCTransferOperator(tgt, src, plan, cg_tol=1e-14)
+    R = op.load_matrix
+    assert R.shape == Rref.shape
+    diff = abs(R - Rref)
+    assert diff.max() <= 1e-14 * abs(Rref).max()   # a few ulps: summation order differs
+    fs = tt.NodalField(src, golden["c1s_coeffs"])
+    assert np.max(np.abs(op.apply(fs).coeffs - golden["op_apply_tol14"])) <= 1e-12
+    op2 = tt.MCTransferOperator(tgt, src, plan, cg_tol=1e-14, fold=False)
+    assert op2.R is None
+    np.testing.assert_allclose(op2.apply(fs).coeffs, op.apply(fs).coeffs, atol=1e-13)
+    # deterministic: a second fold is bitwise identical
+    again = tt.MCTransferOperator(tgt, src, plan).load_matrix
+    assert np.array_equal(again.data, R.data) and np.array_equal(again.indices, R.indices)
+
+
+def test_mc_operator_fold_3d(tt):
+    tgt = tt.generate_cube_mesh(6, 0.2, seed=20)
+    src = tt.generate_cube_mesh(7, 0.2, seed=10, split="kuhn_mirror")
+    fs = tt.NodalField.from_function(src, tt.get_field("smooth", dim=3).fn)
+    plan = tt.SamplePlan.build(32, "sobol", 0, dim=3)
+    op = tt.MCTransferOperator(tgt, src, plan, cg_tol=1e-14)
+    b_fold = op.load(fs).cpu().numpy()
+    b_samp = tt.assemble_load_mc(tgt, tt.MeshBackedField(fs), plan)
+    # sampled path uses unclipped lambdas inside the mesh: equal to rounding for a cube pair
+    np.testing.assert_allclose(b_fold, b_samp, rtol=0, atol=1e-14 * np.abs(b_samp).max())
+    # R @ 1 = the MC load of the constant 1 (sum_b lambda_s,b = 1 for every sample)
+    ones = tt.NodalField(src, np.ones(src.n_nodes))
+    ref1 = tt.assemble_load_mc(tgt, tt.AnalyticField(lambda x, y, z: np.full_like(x, 1.0)), plan)
+    np.testing.assert_allclose(op.load(ones).cpu().numpy(), ref1, rtol=1e-12)
