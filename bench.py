@@ -71,7 +71,8 @@ WORKLOADS = {
     "c3": "C3: LTX-like swept-annulus torus pair (4,992,000 / 4,561,920 tets), snap on the "
           "non-matching faceted boundary, 1 coupling step",
     "c4": "C4: 3-D unit-cube tet transfer (10,368,000 tets), mesh-backed source, 1 coupling step",
-    "c5": "C5: repeated coupling step with cached localisation (MCTransferOperator.apply, C2 mesh)",
+    "c5": "C5: repeated coupling step with cached localisation: MCTransferOperator.apply = the "
+          "device-folded sparse load matrix R (E*N samples folded at init) @ c + PCG, C2 mesh",
 }
 
 
