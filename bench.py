@@ -49,7 +49,7 @@ def parse_args():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--samples", type=int, default=None, help="N per element (64; c5: 50)")
     ap.add_argument("--n", type=int, default=55, help="cubes per axis (C2: 55)")
-    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5"],
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"],
                     help="c2 (default): 1M-tet cube; c3: ~5M-tet torus pair (snap); c4: 10M-tet "
                          "cube; c5: repeated coupling with cached localisation (C2 mesh)")
     ap.add_argument("--mode", default="sobol", choices=["sobol", "uniform", "philox"])
@@ -67,6 +67,8 @@ def dist_env():
 
 
 WORKLOADS = {
+    "c1": "C1: 2-D unit-square triangle transfer, 1M-tri throughput point (n=707), mesh-backed "
+          "source, 1 coupling step (the reference itself runs this config)",
     "c2": "C2: 3-D unit-cube tet transfer (998,250 tets), mesh-backed source, 1 coupling step",
     "c3": "C3: LTX-like swept-annulus torus pair (4,992,000 / 4,561,920 tets), snap on the "
           "non-matching faceted boundary, 1 coupling step",
@@ -77,6 +79,8 @@ WORKLOADS = {
 
 
 def mesh_names(args):
+    if args.config == "c1":
+        return "square n=707 right jitter0.2 seed20", "square n=707 left jitter0.2 seed10"
     if args.config == "c3":
         return "torus 40x80x260 kuhn jitter0.2 seed20", "torus 36x88x240 kuhn_mirror jitter0.2 seed10"
     n = 120 if args.config == "c4" else args.n
@@ -87,7 +91,8 @@ def workload_config(args, world):
     tname, sname = mesh_names(args)
     return {"workload": WORKLOADS[args.config],
             "target": tname, "source": sname,
-            "field": "sin(x)cos(y)cos(z)+2 (P1 interpolant on source)",
+            "field": ("sin(x)cos(y)+2" if args.config == "c1" else "sin(x)cos(y)cos(z)+2")
+                     + " (P1 interpolant on source)",
             "samples_per_elem": args.samples, "plan": args.mode, "cg_tol": 1e-12,
             "partition": f"contiguous target-element ranges x{world}", "l2": "flushed between timed steps",
             "parallelism": f"dp{world}"}
@@ -167,6 +172,9 @@ class ClockSampler:
 
 # --------------------------------------------------------------------- ours
 def build_meshes(args, M):
+    if args.config == "c1":
+        return (M.generate_square_mesh(707, 0.2, seed=20, diagonal="right"),
+                M.generate_square_mesh(707, 0.2, seed=10, diagonal="left"))
     if args.config == "c3":
         return (M.generate_torus_mesh(40, 80, 260, perturbation=0.2, seed=20),
                 M.generate_torus_mesh(36, 88, 240, perturbation=0.2, seed=10, split="kuhn_mirror"))
@@ -177,7 +185,7 @@ def build_meshes(args, M):
 
 def build_problem(args, tt):
     tgt, src = build_meshes(args, tt)
-    field = tt.get_field("smooth", dim=3)
+    field = tt.get_field("smooth", dim=tgt.DIM)
     fs = tt.NodalField.from_function(src, field.fn)
     loc = tt.UniformGridLocator.build(src)
     _ = tgt.device.incidence
@@ -270,7 +278,8 @@ def run_ours(args):
         kms = [a.elapsed_time(b) for a, b in ker] if kernel_events else []
         return ms, kms, x, res
 
-    plan = tt.SamplePlan.build(args.samples, args.mode, 0, dim=3)
+    D = tgt.DIM
+    plan = tt.SamplePlan.build(args.samples, args.mode, 0, dim=D)
     with ClockSampler(local) as clk:
         ms, kms, x, res = timed(plan, args.steps, args.warmup)
     r = decode_result(res)
@@ -286,7 +295,7 @@ def run_ours(args):
 
     # --- dominant kernel alone (mc_load_kernel), CUDA events on the launch stream
     from paper_2603_00538_b200.montecarlo import element_contributions
-    contrib = torch.empty((e_hi - e_lo, 4), dtype=torch.float64, device="cuda")
+    contrib = torch.empty((e_hi - e_lo, D + 1), dtype=torch.float64, device="cuda")
     kt = []
     for i in range(args.warmup + args.steps):
         flush.zero_()
@@ -303,9 +312,10 @@ def run_ours(args):
     k_ms = statistics.mean(a.elapsed_time(b) for a, b in kt)
     E_loc = e_hi - e_lo
     n_cells = loc.dims[0] * loc.dims[1] * loc.dims[2]
-    alg_bytes = (E_loc * (4 * 4 + 8 * 3 * 4 + 8 + 8 * 4)       # target conn, coords, measure, contrib
+    K = D + 1
+    alg_bytes = (E_loc * (4 * K + 8 * D * K + 8 + 8 * K)       # target conn, coords, measure, contrib
                  + 8 * (n_cells + 1) + 4 * int(loc.cell_elems_dev.numel())
-                 + src.n_elems * (8 * 12 + 4 * 4) + 8 * src.n_nodes)
+                 + src.n_elems * (8 * (D * D + D) + 4 * K) + 8 * src.n_nodes)
     peak_hbm = None
     try:
         peak_hbm = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"]
@@ -366,7 +376,7 @@ def run_ours(args):
     sweep = {}
     if args.sweep:
         for n in [int(v) for v in args.sweep.split(",") if v]:
-            p = tt.SamplePlan.build(n, args.mode, 0, dim=3)
+            p = tt.SamplePlan.build(n, args.mode, 0, dim=D)
             m, km, _, rr = timed(p, max(2, args.steps // 3), 1)
             tt_ = torch.tensor([m / max(2, args.steps // 3)], dtype=torch.float64, device="cuda")
             if world > 1:
@@ -424,7 +434,7 @@ def cpu_baseline(args, tgt, src, coeffs, seconds=12.0):
     t0 = time.perf_counter()
     g = O.Grid(src.nodes, src.elements)
     setup_s = time.perf_counter() - t0
-    lam = O.bary_map(O.sobol(args.samples, 3))
+    lam = O.bary_map(O.sobol(args.samples, tgt.DIM))
     coeffs = np.asarray(coeffs)
     threads = os.cpu_count() or 1
     OC.mc_load_mesh(g, coeffs, tgt.nodes, tgt.elements, tgt.elem_areas, lam, 0, 512, threads)  # warm
@@ -454,6 +464,8 @@ def run_reference(args):
     import paper_2603_00538_b200.mesh as M   # host-only mesh generators (no GPU use)
     sys.path.insert(0, str(ROOT / "oracle"))
     import tt_oracle as O
+    if args.config == "c1" and (ROOT / "oracle" / "_ref" / "tritransfer").exists():
+        return run_reference_real(args, world)
     tgt, src = build_meshes(args, M)
 
     coeffs = np.sin(src.nodes[:, 0]) * np.cos(src.nodes[:, 1]) * np.cos(src.nodes[:, 2]) + 2
@@ -477,6 +489,45 @@ def run_reference(args):
             "config": workload_config(args, world), "cpu_baseline": cpu_line,
             "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_reference_real(args, world):
+    """C1 (2-D): the REFERENCE itself (oracle/_ref: tritransfer with its compiled Cython
+    backend) through its public API, all host cores: one online step =
+    assemble_load_mc(MeshBackedField) + cg_solve, as its own bench (cli.py:272-293)."""
+    sys.path.insert(0, str(ROOT / "oracle" / "_ref"))
+    import tritransfer as ref
+    from tritransfer.fem import NodalField, assemble_mass_matrix, cg_solve
+    from tritransfer.fields import get_field
+    from tritransfer.montecarlo import MeshBackedField, SamplePlan, assemble_load_mc
+    t0 = time.perf_counter()
+    tgt = ref.generate_square_mesh(707, 0.2, seed=20, diagonal="right")
+    src = ref.generate_square_mesh(707, 0.2, seed=10, diagonal="left")
+    fs = NodalField.from_function(src, get_field("smooth").fn)
+    box = MeshBackedField(fs)                       # grid build: untimed setup
+    mass = assemble_mass_matrix(tgt)
+    plan = SamplePlan.build(args.samples, "sobol", 0)
+    setup = time.perf_counter() - t0
+    workers = os.cpu_count() or 1
+    times = []
+    for _ in range(max(1, min(args.steps, 2))):
+        t = time.perf_counter()
+        b = assemble_load_mc(tgt, box, plan, workers=workers)
+        cg_solve(mass, b)
+        times.append(time.perf_counter() - t)
+    step_s = min(times)
+    S = tgt.n_elems * args.samples
+    value = S / step_s
+    cpu = {"value": value, "unit": "samples/s", "cores": workers, "kind": "reference",
+           "sample": f"full C1 step ({S} samples) through tritransfer.assemble_load_mc(workers={workers}) "
+                     f"+ cg_solve, best of {len(times)}; setup {setup:.1f} s untimed",
+           "impl": f"reference tritransfer {ref.__version__}, backend {ref.kernel_backend}"}
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s",
+            "n_gpus": world, "steps": len(times), "warmup": 0, "ms_per_step": step_s * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": workload_config(args, world), "cpu_baseline": cpu,
+            "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
