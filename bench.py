@@ -341,15 +341,20 @@ def run_ours(args):
     x_host = torch.empty(tgt.n_nodes, dtype=torch.float64).pin_memory()
     c_dev = torch.empty(src.n_nodes, dtype=torch.float64, device="cuda")
 
+    from paper_2603_00538_b200.dist import DistributedCoupling
+    coupling = DistributedCoupling(tgt, rank, world) if world > 1 else None
+
     def e2e_step():
+        # the calls a user makes: NodalField from host coefficients (pinned H2D), then
+        # transfer_mc / MCTransferOperator.apply / DistributedCoupling.step, x back to host
         c_dev.copy_(c_host, non_blocking=True)
         field = tt.NodalField(src, c_dev)
         if args.config == "c5":
-            b = ops[plan.n_samples].load(field)
+            xx = ops[plan.n_samples].apply(field).coeffs_dev
+        elif coupling is not None:
+            xx = coupling.step(tt.MeshBackedField(field, loc), plan, tol=1e-12)
         else:
-            b = load_vector(tgt, tt.MeshBackedField(field, loc), plan, e_lo, e_hi)
-        reduce_load(b)
-        xx = tt.cg_solve(mass, b, tol=1e-12)
+            xx = tt.transfer_mc(tgt, tt.MeshBackedField(field, loc), plan, cg_tol=1e-12).coeffs_dev
         x_host.copy_(xx, non_blocking=True)
         torch.cuda.current_stream().synchronize()
     for _ in range(args.warmup):
@@ -398,7 +403,8 @@ def run_ours(args):
             "load_ms_per_step": load_ms, "pcg_iterations": int(r.iterations),
             "e2e": {"value": S / (e2e_ms * 1e-3), "unit": "samples/s", "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": src.n_nodes * 8, "d2h_bytes_per_step": tgt.n_nodes * 8,
-                    "api": "NodalField(pinned->device) + MeshBackedField + load_vector + cg_solve"},
+                    "api": "NodalField(pinned H2D) -> transfer_mc(MeshBackedField) | "
+                           "MCTransferOperator.apply (c5) | DistributedCoupling.step (N>1) -> x D2H"},
             "roofline": {"bound": "hbm", "kernel": "mc_load_kernel<3,SHARED,CACHED>" if args.config == "c5" else "mc_mesh_kernel<3,SHARED,G,spec>",
                          "achieved": achieved, "peak": peak_hbm, "unit": "GB/s",
                          "frac": achieved / peak_hbm, "peak_source": peak_src,
