@@ -126,3 +126,12 @@ R = op._load_matrix.tocsr()
 fold = {"R_indptr": R.indptr, "R_indices": R.indices, "R_data": R.data, "R_shape": np.array(R.shape)}
 np.savez_compressed(ROOT / "tests" / "golden" / "ref_fold.npz", **fold)
 print("fold nnz", R.nnz)
+
+# CLI outputs of the reference (cli.py) for the CLI parity tests
+import subprocess  # noqa: E402
+env = dict(__import__("os").environ, PYTHONPATH=str(ROOT / "oracle" / "_ref"))
+subprocess.run([sys.executable, "-m", "tritransfer.cli", "transfer", "--method", "mc", "--gen-source",
+                "10,0.2,10,left", "--gen-target", "7,0.2,20,right", "--samples", "256", "--cg-tol", "1e-14",
+                "--out", str(ROOT / "tests" / "golden" / "ref_cli_transfer.csv")], check=True, env=env)
+subprocess.run([sys.executable, "-m", "tritransfer.cli", "integral-study", "--seeds", "0,1", "--out",
+                str(ROOT / "tests" / "golden" / "ref_cli_integral.csv")], check=True, env=env)

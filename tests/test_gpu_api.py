@@ -170,3 +170,31 @@ def test_msh_round_trip_through_device(tt, tmp_path):
     f1 = tt.NodalField.from_function(m, lambda x, y, z: x + y * z)
     f2 = tt.NodalField.from_function(r, lambda x, y, z: x + y * z)
     assert tt.integrate_field(f1) == tt.integrate_field(f2)
+
+
+def test_cli_matches_reference_cli(tt, tmp_path):
+    """`transfer --method mc` and `integral-study` reproduce the reference CLI's CSVs
+    (tests/golden/ref_cli_*.csv, made by the reference's cli.py)."""
+    from pathlib import Path
+    from paper_2603_00538_b200 import cli
+    gold = Path(__file__).resolve().parent / "golden"
+    out = tmp_path / "t.csv"
+    assert cli.main(["transfer", "--method", "mc", "--gen-source", "10,0.2,10,left", "--gen-target",
+                     "7,0.2,20,right", "--samples", "256", "--cg-tol", "1e-14", "--out", str(out)]) == 0
+    ref_lines = (gold / "ref_cli_transfer.csv").read_text().splitlines()
+    got_lines = out.read_text().splitlines()
+    assert got_lines[0] == ref_lines[0] and len(got_lines) == len(ref_lines)
+    ref = np.array([[float(v) for v in ln.split(",")] for ln in ref_lines[1:]])
+    got = np.array([[float(v) for v in ln.split(",")] for ln in got_lines[1:]])
+    assert np.array_equal(got[:, :3], ref[:, :3])                   # ids and coordinates
+    assert np.max(np.abs(got[:, 3] - ref[:, 3])) <= 1e-12
+    out2 = tmp_path / "i.csv"
+    assert cli.main(["integral-study", "--seeds", "0,1", "--out", str(out2)]) == 0
+    r2 = (gold / "ref_cli_integral.csv").read_text().splitlines()
+    g2 = out2.read_text().splitlines()
+    assert g2[:2] == r2[:2] and len(g2) == len(r2)
+    for a, b in zip(g2[2:], r2[2:]):
+        ka, va = a.rsplit(",", 1)
+        kb, vb = b.rsplit(",", 1)
+        assert ka == kb
+        assert abs(float(va) - float(vb)) <= 1e-12 * max(1.0, abs(float(vb)))

@@ -160,3 +160,19 @@ def test_torus_generator_is_a_closed_tessellation():
     assert fine.elem_areas.sum() == pytest.approx(exact, rel=5e-3)
     with pytest.raises(tt.InvalidParameter):
         tt.generate_torus_mesh(2, 2, 8)
+
+
+def test_cli_parser_and_errors(tmp_path):
+    from paper_2603_00538_b200 import cli
+    p = cli.build_parser()
+    a = p.parse_args(["transfer", "--gen-source", "4", "--gen-target", "3"])
+    assert a.method == "mc" and a.sampling == "sobol" and a.cg_tol == 1e-12
+    cfg = tmp_path / "c.json"
+    cfg.write_text('{"samples": 77, "cg-tol": 1e-9}')
+    b = cli._apply_config_file(p.parse_args(["transfer", "--config", str(cfg), "--samples", "5"]),
+                               ["transfer", "--config", str(cfg), "--samples", "5"])
+    assert b.samples == 5 and b.cg_tol == 1e-9          # explicit flags override the file
+    assert cli.main(["transfer", "--method", "mi", "--gen-source", "3", "--gen-target", "3"]) == 1
+    assert cli.main(["transfer", "--gen-source", "3"]) == 1          # missing target mesh
+    m = cli.parse_gen_spec("cube:2,0.1,3")
+    assert m.DIM == 3 and m.n_elems == 48
