@@ -421,7 +421,7 @@ def run_ours(args):
             "sweep": sweep,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
-            "gpu_launches": 5 * args.steps,
+            "gpu_launches": (3 if args.config == "c5" else 4) * args.steps,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -101,10 +101,13 @@ class MeshBackedField:
         s.grid = self.locator.desc()
         s.src_elems = _lib.ptr(self.field.mesh.device.elems).value
         s.coeffs = _lib.ptr(self.field.coeffs_dev).value
-        s.elem_coeffs = _lib.ptr(self.field.elem_coeffs()).value
         if target is not None and self.locator.walk:
+            # float-walk path: gradient records for certified hits; the rare exact-scan /
+            # snap fallbacks gather the vertex coefficients directly
             s.seeds = _lib.ptr(self.locator.seeds_for(target)).value
             s.elem_grad = _lib.ptr(self.field.elem_grad()).value
+        else:
+            s.elem_coeffs = _lib.ptr(self.field.elem_coeffs()).value
         return s
 
     def __call__(self, points):
