@@ -122,6 +122,21 @@ TT_D void map_point(const double* lam, const double (*v)[D], double* x) {
     }
 }
 
+// FMA point map for the certified walk: within 2 ulps of map_point; a certified element
+// contains both points with a margin (>= 1e-12) far above that difference, so the id is
+// the reference's; exact-scan fallbacks recompute x with map_point.
+template <int D>
+TT_D void map_point_fma(const double* lam, const double (*v)[D], double* x) {
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+        double acc = lam[0] * v[0][c];
+        acc = fma(lam[1], v[1][c], acc);
+        acc = fma(lam[2], v[2][c], acc);
+        if constexpr (D == 3) acc = fma(lam[3], v[3][c], acc);
+        x[c] = acc;
+    }
+}
+
 // Record tail: certification margin and facet neighbours (written by walk prep).
 template <int D>
 struct RecTail {

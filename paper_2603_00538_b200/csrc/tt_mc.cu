@@ -330,9 +330,11 @@ __global__ void __launch_bounds__(BLOCK, MINB) mc_mesh_kernel(TargetDev t, int64
                         double vv[K][D];
 #pragma unroll
                         for (int q = 0; q < K * D; ++q) vv[q / D][q % D] = s_v[wib][gib][q];
-                        map_point<D>(lam, vv, x);
+                        if constexpr (FW) map_point_fma<D>(lam, vv, x);
+                        else map_point<D>(lam, vv, x);
                     } else {
-                        map_point<D>(lam, v, x);
+                        if constexpr (FW) map_point_fma<D>(lam, v, x);
+                        else map_point<D>(lam, v, x);
                     }
                     cur = -1;
                     if (walk) {
@@ -454,7 +456,18 @@ __global__ void __launch_bounds__(BLOCK, MINB) mc_mesh_kernel(TargetDev t, int64
                 cur = -1;
             }
             if (!done && cur < 0) {
-                // exact reference scan (+ snap / strict), rare
+                // exact reference scan (+ snap / strict), rare; the float-walk path mapped
+                // the point with FMA, so recompute it exactly first (montecarlo.py:123-124)
+                if constexpr (FW) {
+                    if constexpr (SMEMV) {
+                        double vv[K][D];
+#pragma unroll
+                        for (int q = 0; q < K * D; ++q) vv[q / D][q % D] = s_v[wib][gib][q];
+                        map_point<D>(lam, vv, x);
+                    } else {
+                        map_point<D>(lam, v, x);
+                    }
+                }
                 hit = locate_point<D>(g, x, EPS, l);
                 if (hit < 0) {
                     if (src.outside == TT_OUTSIDE_STRICT) {
