@@ -1,0 +1,105 @@
+"""GPU edge cases of the MC path: sample counts below / not multiple of the lane group,
+very large N, single-element meshes, partial element ranges (the multi-GPU partition),
+64-bit seeds, and the reference's parameter limits."""
+
+import numpy as np
+import pytest
+
+import tt_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def tt():
+    import paper_2603_00538_b200 as tt
+    return tt
+
+
+def _oracle_b(tgt, src_mesh, coeffs, lam):
+    g = O.Grid(src_mesh.nodes, src_mesh.elements)
+    return O.reduce_to_nodes(tgt.n_nodes, tgt.elements,
+                             O.accumulate(tgt.nodes, tgt.elements, tgt.elem_areas, lam,
+                                          lambda P: O.mesh_backed_eval(g, coeffs, P)))
+
+
+@pytest.mark.parametrize("N", [1, 3, 7, 33, 1000])
+def test_sample_counts_2d_and_3d(tt, N):
+    for dim in (2, 3):
+        if dim == 2:
+            tgt = tt.generate_square_mesh(5, 0.2, seed=1, diagonal="right")
+            src = tt.generate_square_mesh(7, 0.2, seed=2)
+        else:
+            tgt = tt.generate_cube_mesh(3, 0.2, seed=1)
+            src = tt.generate_cube_mesh(4, 0.2, seed=2, split="kuhn_mirror")
+        fs = tt.NodalField.from_function(src, tt.get_field("smooth", dim=dim).fn)
+        plan = tt.SamplePlan.build(N, "sobol", 3, dim=dim)
+        b = tt.assemble_load_mc(tgt, tt.MeshBackedField(fs), plan)
+        ref = _oracle_b(tgt, src, fs.coeffs, plan.barycentric)
+        assert np.max(np.abs(b - ref)) <= 1e-12 * np.max(np.abs(ref))
+
+
+def test_single_element_meshes(tt):
+    tri = tt.TriMesh.from_arrays(np.array([[0.0, 0.0], [1.0, 0.0], [0.0, 1.0]]), np.array([[0, 1, 2]]))
+    tet = tt.TetMesh.from_arrays(np.array([[0.0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1]]), np.array([[0, 1, 2, 3]]))
+    for m in (tri, tet):
+        f = tt.NodalField(m, np.arange(m.n_nodes, dtype=float) + 1.0)
+        out = tt.transfer_mc(m, tt.MeshBackedField(f), tt.SamplePlan.build(64, "sobol", 0, dim=m.DIM),
+                             cg_tol=1e-14)
+        # a P1 field projected onto its own single element: MC load of a linear field,
+        # conservation of the sampled mass through the solve
+        b = tt.assemble_load_mc(m, tt.MeshBackedField(f), tt.SamplePlan.build(64, "sobol", 0, dim=m.DIM))
+        assert tt.integrate_field(out) == pytest.approx(b.sum(), rel=1e-12)
+        loc = tt.UniformGridLocator.build(m)
+        assert loc.dims[0] == 1
+
+
+def test_partial_ranges_sum_to_full_load(tt):
+    """The multi-GPU partition: per-range loads summed == the full load."""
+    import torch
+    from paper_2603_00538_b200.dist import partition_elements
+    from paper_2603_00538_b200.montecarlo import load_vector
+    tgt = tt.generate_cube_mesh(6, 0.2, seed=20)
+    src = tt.generate_cube_mesh(6, 0.2, seed=10, split="kuhn_mirror")
+    fs = tt.NodalField.from_function(src, tt.get_field("smooth", dim=3).fn)
+    box = tt.MeshBackedField(fs)
+    plan = tt.SamplePlan.build(40, "philox", 2**40 + 7, dim=3)
+    full = load_vector(tgt, box, plan)
+    for world in (2, 3, 8):
+        parts = torch.zeros_like(full)
+        for r in range(world):
+            lo, hi = partition_elements(tgt.n_elems, world, r)
+            parts += load_vector(tgt, box, plan, lo, hi)
+        assert float((parts - full).abs().max()) <= 1e-15 * float(full.abs().max())
+
+
+def test_large_seeds_and_skips(tt):
+    p = tt.SamplePlan.build(1000, "sobol", 123456, dim=3)      # skip = 123,456,000 points
+    assert np.array_equal(p.parametric, O.sobol(1000, 3, skip=123456 * 1000))
+    q = tt.SamplePlan.build(50, "uniform", 2**63 - 25)
+    assert np.array_equal(q.parametric, np.random.default_rng(2**63 - 25).random((50, 2)))
+
+
+def test_strict_policy_passes_when_all_inside(tt):
+    tgt = tt.generate_square_mesh(6, 0.2, seed=20, diagonal="right")
+    src = tt.generate_square_mesh(6, 0.2, seed=10)
+    fs = tt.NodalField.from_function(src, lambda x, y: x + 2 * y)
+    plan = tt.SamplePlan.build(128, "sobol", 0)
+    strict = tt.assemble_load_mc(tgt, tt.MeshBackedField(fs, outside="strict"), plan)
+    snap = tt.assemble_load_mc(tgt, tt.MeshBackedField(fs, outside="snap"), plan)
+    assert np.array_equal(strict, snap)
+
+
+def test_deterministic_reduction_matches_add_at_order(tt):
+    """tt_reduce_nodes sums each node's contributions in np.add.at order from 0.0:
+    bit-identical to np.add.at on the same contributions."""
+    import torch
+    from paper_2603_00538_b200.montecarlo import element_contributions
+    tgt = tt.generate_square_mesh(9, 0.25, seed=4)
+    f = tt.AnalyticField(lambda x, y: np.exp(x) * np.sin(3 * y))
+    plan = tt.SamplePlan.build(50, "uniform", 1)
+    contrib = element_contributions(tgt, f, plan)
+    b = tgt.device.reduce_nodes(contrib).cpu().numpy()
+    ref = np.zeros(tgt.n_nodes)
+    np.add.at(ref, tgt.elements, contrib.cpu().numpy())
+    assert np.array_equal(b, ref)
