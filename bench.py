@@ -251,6 +251,7 @@ def run_ours(args):
         if ev is not None:
             ev[1].record()
         reduce_load(b)                      # NCCL all-reduce of the partial b (N>1)
+        # (TT_DIST_REDUCE=p2p: the e2e leg uses PeerCoupling's peer-memory gather instead)
         x, best_x, res = pcg_device(mass, b, tol=1e-12)
         return x, res
 
@@ -341,8 +342,11 @@ def run_ours(args):
     x_host = torch.empty(tgt.n_nodes, dtype=torch.float64).pin_memory()
     c_dev = torch.empty(src.n_nodes, dtype=torch.float64, device="cuda")
 
-    from paper_2603_00538_b200.dist import DistributedCoupling
-    coupling = DistributedCoupling(tgt, rank, world) if world > 1 else None
+    from paper_2603_00538_b200.dist import DistributedCoupling, PeerCoupling
+    coupling = None
+    if world > 1:
+        coupling = (PeerCoupling(tgt, rank, world) if os.environ.get("TT_DIST_REDUCE") == "p2p"
+                    else DistributedCoupling(tgt, rank, world))
 
     def e2e_step():
         # the calls a user makes: NodalField from host coefficients (pinned H2D), then

@@ -273,6 +273,15 @@ int tt_reduce_nodes(int64_t n_nodes, int k, const int64_t* inc_start, const int3
                     int64_t e_lo, int64_t e_hi, const double* contrib, double* b,
                     void* stream);
 
+/* Multi-GPU node reduction over peer memory: element contributions of rank r (its
+ * contiguous range [range_lo[r], range_lo[r+1])) are read through contrib_ptrs[r] (a device
+ * array of device/peer pointers, e.g. symmetric-memory buffers over NVLink); every node sums
+ * its incidences in the single-GPU order, so b is bitwise identical for any GPU count.
+ * range_lo: device (n_ranks,) ascending element offsets. */
+int tt_reduce_nodes_peers(int64_t n_nodes, int k, const int64_t* inc_start, const int32_t* inc,
+                          int n_ranks, const int64_t* range_lo, const double* const* contrib_ptrs,
+                          double* b, void* stream);
+
 /* ---- P1 mass matrix (CSR, exactly symmetric) ---- */
 int tt_mass_pattern(const tt_mesh_t* mesh, const int64_t* inc_start, const int32_t* inc,
                     int64_t* row_ptr /* (n_nodes+1) exclusive scan of row lengths */,

@@ -116,6 +116,7 @@ _SIGNATURES = {
     "tt_incidence_count": ([C.POINTER(tt_mesh_t), _P, _P], _I),
     "tt_incidence_fill": ([C.POINTER(tt_mesh_t), _P, _P, _P, _P], _I),
     "tt_reduce_nodes": ([_I64, _I, _P, _P, _I64, _I64, _P, _P, _P], _I),
+    "tt_reduce_nodes_peers": ([_I64, _I, _P, _P, _I, _P, _P, _P, _P], _I),
     "tt_mass_pattern": ([C.POINTER(tt_mesh_t), _P, _P, _P, _P, _P], _I),
     "tt_mass_fill": ([C.POINTER(tt_mesh_t), _P, _P, C.POINTER(_D), _P, _P, _P, _P], _I),
     "tt_pcg_workspace_doubles": ([_I64], _I64),

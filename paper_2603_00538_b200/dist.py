@@ -61,3 +61,60 @@ class DistributedCoupling:
         from .fem import cg_solve
         b = self.load(source, plan)
         return cg_solve(self.target.device.mass, b, tol=tol)
+
+
+def reduce_nodes_peers(target, contrib_ptrs: torch.Tensor, range_lo: torch.Tensor,
+                       out: torch.Tensor | None = None) -> torch.Tensor:
+    """Full load vector from per-rank element contributions reached through (peer) device
+    pointers: every node sums its incidences in the single-GPU order, so the result is
+    bitwise identical to the one-GPU deterministic load for any GPU count.
+
+    ``contrib_ptrs``: device int64 tensor of per-rank contribution-buffer addresses
+    ((hi_r - lo_r, k) f64, row-major); ``range_lo``: device int64 ascending range starts.
+    """
+    from . import _lib
+    dm = target.device
+    inc_start, inc = dm.incidence
+    b = out if out is not None else torch.empty(target.n_nodes, dtype=torch.float64,
+                                                device=dm.nodes.device)
+    _lib.call("tt_reduce_nodes_peers", target.n_nodes, target.DIM + 1, _lib.ptr(inc_start),
+              _lib.ptr(inc), int(range_lo.numel()), _lib.ptr(range_lo), _lib.ptr(contrib_ptrs),
+              _lib.ptr(b), _lib.stream_handle())
+    return b
+
+
+class PeerCoupling(DistributedCoupling):
+    """Load phase with the exchange done by one peer-memory kernel instead of an NCCL
+    all-reduce: each rank writes its contributions into a symmetric-memory buffer
+    (torch.distributed._symmetric_memory, NVLink peer mappings), a device barrier makes
+    them visible, and ``tt_reduce_nodes_peers`` gathers every node's incidences over
+    NVLink in global element order -- deterministic and GPU-count invariant.
+    Opt-in (``TT_DIST_REDUCE=p2p`` in bench.py): it needs P2P-capable GPUs.
+    """
+
+    def __init__(self, target, rank: int | None = None, world: int | None = None, group=None):
+        super().__init__(target, rank, world, group)
+        import torch.distributed._symmetric_memory as symm_mem
+        k = target.DIM + 1
+        dev = target.device.nodes.device
+        spans = [partition_elements(target.n_elems, self.world, r) for r in range(self.world)]
+        self.range_lo = torch.tensor([lo for lo, _ in spans], dtype=torch.int64, device=dev)
+        max_e = max(hi - lo for lo, hi in spans)
+        self.buf = symm_mem.empty(max(max_e, 1) * k, dtype=torch.float64, device=dev)
+        self.hdl = symm_mem.rendezvous(self.buf, group if group is not None else dist.group.WORLD)
+        self.ptrs = torch.tensor(list(self.hdl.buffer_ptrs), dtype=torch.int64, device=dev)
+
+    def load(self, source, plan, check: bool = True, status=None) -> torch.Tensor:
+        from .montecarlo import _raise_status, element_contributions
+        from . import _lib
+        k = self.target.DIM + 1
+        status = status if status is not None else _lib.status_word()
+        self.hdl.barrier()                     # peers finished reading the previous step
+        contrib = self.buf[:(self.e_hi - self.e_lo) * k].view(self.e_hi - self.e_lo, k)
+        element_contributions(self.target, source, plan, self.e_lo, self.e_hi, out=contrib,
+                              status=status)
+        self.hdl.barrier()                     # every rank's contributions are visible
+        b = reduce_nodes_peers(self.target, self.ptrs, self.range_lo)
+        if check:
+            _raise_status(int(status.item()))
+        return b
