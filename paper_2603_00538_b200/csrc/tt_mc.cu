@@ -745,10 +745,13 @@ template <int D, int PLAN, int SRC>
 static int dispatch_g(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_plan_t* p,
                       const tt_source_t* s, double* contrib, double* b, int32_t* status,
                       cudaStream_t st) {
-    // lanes per element: at least ~8 samples per lane (amortises the per-element setup)
+    // lanes per element: ~16 samples per lane (measured best: amortises the per-element
+    // setup while the dynamic schedule keeps the group's lanes busy)
     const int64_t N = p->n_samples;
-    static int spl = [] { const char* v = getenv("TT_MC_SPL"); return v ? atoi(v) : 8; }();
+    static int spl = [] { const char* v = getenv("TT_MC_SPL"); return v ? atoi(v) : 16; }();
     const int64_t gsel = N / spl;  // lanes so that each lane gets ~spl samples
+    if constexpr (SRC == TT_SRC_MESH)
+        if (gsel < 4) return launch_mc<D, PLAN, SRC, 2>(t, e_lo, e_hi, p, s, contrib, b, status, st);
     if (gsel < 8) return launch_mc<D, PLAN, SRC, 4>(t, e_lo, e_hi, p, s, contrib, b, status, st);
     if (gsel < 16) return launch_mc<D, PLAN, SRC, 8>(t, e_lo, e_hi, p, s, contrib, b, status, st);
     if (gsel < 32) return launch_mc<D, PLAN, SRC, 16>(t, e_lo, e_hi, p, s, contrib, b, status, st);
