@@ -260,7 +260,7 @@ __device__ __forceinline__ void plan_lambda(const PlanDev& plan, int64_t e, int6
 // data, so results are bitwise reproducible.  Identical ids/lambdas as the reference scan
 // (certified walk, see locate_walk in tt_common.cuh).
 template <int D, int PLAN, int G, bool SPEC, int MINB, bool FW = false, int BLOCK = 256,
-          bool SMEMV = false>
+          bool SMEMV = false, bool RL = false>
 __global__ void __launch_bounds__(BLOCK, MINB) mc_mesh_kernel(TargetDev t, int64_t e_lo, int64_t e_hi,
                                                       PlanDev plan, SrcDev src,
                                                       double* __restrict__ contrib,
@@ -314,8 +314,10 @@ __global__ void __launch_bounds__(BLOCK, MINB) mc_mesh_kernel(TargetDev t, int64
                 for (int i = 0; i <= K; ++i) seed[i] = __ldg(src.seeds + e * (K + 1) + i);
             }
         }
-        int64_t next = 0;
-        int64_t jcur = 0;
+        // RL (shared plans): lambda_j is re-read from the L1-resident plan table when the
+        // sample completes instead of being held in 8 registers across the walk
+        int next = 0;
+        int jcur = 0;
         bool busy = false;
         double x[D], lam[K];
         int cur = -1, steps = 0;
@@ -323,7 +325,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) mc_mesh_kernel(TargetDev t, int64
             const bool want = active && !busy;
             const unsigned m = __ballot_sync(FULL, want) & gmask;
             if (want) {
-                const int64_t j = next + __popc(m & lt);
+                const int j = next + __popc(m & lt);
                 if (j < N) {
                     plan_lambda<D, PLAN>(plan, e, j, lam);
                     if constexpr (SMEMV) {
@@ -459,6 +461,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) mc_mesh_kernel(TargetDev t, int64
                 // exact reference scan (+ snap / strict), rare; the float-walk path mapped
                 // the point with FMA, so recompute it exactly first (montecarlo.py:123-124)
                 if constexpr (FW) {
+                    if constexpr (RL && PLAN == TT_PLAN_SHARED) plan_lambda<D, PLAN>(plan, e, jcur, lam);
                     if constexpr (SMEMV) {
                         double vv[K][D];
 #pragma unroll
@@ -497,8 +500,15 @@ __global__ void __launch_bounds__(BLOCK, MINB) mc_mesh_kernel(TargetDev t, int64
                     }
                 }
                 if (!isfinite(f)) flags |= TT_FLAG_NONFINITE;
+                if constexpr (RL && PLAN == TT_PLAN_SHARED) {
+                    double lt[K];
+                    plan_lambda<D, PLAN>(plan, e, jcur, lt);
 #pragma unroll
-                for (int i = 0; i < K; ++i) acc[i] = fma(f, lam[i], acc[i]);
+                    for (int i = 0; i < K; ++i) acc[i] = fma(f, lt[i], acc[i]);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < K; ++i) acc[i] = fma(f, lam[i], acc[i]);
+                }
                 busy = false;
             }
         }
@@ -715,7 +725,10 @@ static int launch_mc(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_pl
                     if (nb < 1) nb = 1;
                     kernel<<<(unsigned)nb, 128, 0, st>>>(td, e_lo, e_hi, pd, sd, contrib, b, nullptr, status);
                 };
-                if (variant & 32) launch128(mc_mesh_kernel<D, PLAN, G, true, 6, true, 128, true>);
+                if (variant & 64) {
+                    if (variant & 32) launch128(mc_mesh_kernel<D, PLAN, G, true, 6, true, 128, true, true>);
+                    else launch128(mc_mesh_kernel<D, PLAN, G, true, 5, true, 128, true, true>);
+                } else if (variant & 32) launch128(mc_mesh_kernel<D, PLAN, G, true, 6, true, 128, true>);
                 else launch128(mc_mesh_kernel<D, PLAN, G, true, 5, true, 128, true>);
                 return launch_check("mc_mesh_kernel (float walk, smem)");
             }
