@@ -198,3 +198,28 @@ def test_cli_matches_reference_cli(tt, tmp_path):
         kb, vb = b.rsplit(",", 1)
         assert ka == kb
         assert abs(float(va) - float(vb)) <= 1e-12 * max(1.0, abs(float(vb)))
+
+
+def test_cli_study_commands_run(tt, tmp_path):
+    """convergence / roundtrip / bench subcommands produce their versioned CSV schemas; the
+    convergence E_mass equals the reference's supermesh E_mass (tests/golden/ref_stats.npz)."""
+    from pathlib import Path
+    from paper_2603_00538_b200 import cli
+    c = tmp_path / "c.csv"
+    assert cli.main(["convergence", "--levels", "8", "--out", str(c)]) == 0
+    lines = c.read_text().splitlines()
+    assert lines[0] == "# schema: tritransfer/convergence v1"
+    assert lines[1] == "h,method,n_samples,e_l2_supermesh,e_mass_supermesh"
+    rows = {int(r.split(",")[2]): float(r.split(",")[4]) for r in lines[2:]}
+    with np.load(Path(__file__).resolve().parent / "golden" / "ref_stats.npz") as z:
+        for N in (400, 1600):
+            assert abs(rows[N] - float(z[f"emass_n8_N{N}"])) <= 1e-11
+    r = tmp_path / "r.csv"
+    assert cli.main(["roundtrip", "--gen-source", "12,0.2,1,left", "--gen-target", "6,0.2,2,right",
+                     "--samples", "64", "--seeds", "0", "--iterations", "3", "--out", str(r)]) == 0
+    rl = r.read_text().splitlines()
+    assert rl[1] == "iteration,method,n_samples,seed,e_l2_dof,e_mass_mesh" and len(rl) == 2 + 3
+    b = tmp_path / "b.csv"
+    assert cli.main(["bench", "--sizes", "2000", "--samples", "32", "--repetitions", "1", "--out", str(b)]) == 0
+    bl = b.read_text().splitlines()
+    assert bl[1] == "elements,method,init_time,online_time" and bl[2].split(",")[1] == "mc"
