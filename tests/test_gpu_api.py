@@ -223,3 +223,24 @@ def test_cli_study_commands_run(tt, tmp_path):
     assert cli.main(["bench", "--sizes", "2000", "--samples", "32", "--repetitions", "1", "--out", str(b)]) == 0
     bl = b.read_text().splitlines()
     assert bl[1] == "elements,method,init_time,online_time" and bl[2].split(",")[1] == "mc"
+
+
+def test_c_abi_example_matches_python_api(tt):
+    """examples/c_transfer.c runs a whole transfer through libtt_b200.so from C (no Python);
+    it must agree with the Python API on the same meshes, field and plan."""
+    import json
+    import subprocess
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    subprocess.run(["bash", str(root / "examples" / "build.sh")], check=True)
+    out = subprocess.run([str(root / "examples" / "c_transfer"), "12", "16", "256"], capture_output=True,
+                         text=True, check=True)
+    c = json.loads(out.stdout.strip().splitlines()[-1])
+    tgt = tt.generate_square_mesh(12, 0.0, diagonal="left")
+    src = tt.generate_square_mesh(16, 0.0, diagonal="left")
+    fs = tt.NodalField.from_function(src, tt.get_field("smooth").fn)
+    x = tt.transfer_mc(tgt, tt.MeshBackedField(fs), tt.SamplePlan.build(256, "sobol", 0), cg_tol=1e-14).coeffs
+    assert c["converged"] == 1 and c["flags"] == 0 and c["n_nodes"] == tgt.n_nodes
+    assert abs(c["x0"] - x[0]) <= 1e-12
+    assert abs(c["checksum"] - float(np.sum(x * ((np.arange(len(x)) % 7) + 1)))) <= 1e-10
+    assert abs(c["integral"] - tt.integrate_field(tt.NodalField(tgt, x))) <= 1e-13
