@@ -16,7 +16,8 @@ import torch
 from .errors import (DeviceUnavailable, DimensionMismatch, InvalidParameter,
                      TransferError)
 
-LIB_PATH = Path(__file__).resolve().parent / "libtt_b200.so"
+# TT_LIB_PATH: load another build of the library (same-box A/B measurements)
+LIB_PATH = Path(os.environ.get("TT_LIB_PATH") or Path(__file__).resolve().parent / "libtt_b200.so")
 
 TT_OK, TT_ERR_INVALID_PARAMETER, TT_ERR_DIMENSION_MISMATCH, TT_ERR_CUDA, TT_ERR_CAPACITY = 0, 1, 2, 3, 4
 TT_FLAG_NONFINITE, TT_FLAG_OUTSIDE_STRICT, TT_FLAG_CAPACITY, TT_FLAG_INVALID_DENSITY = 1, 2, 4, 8

@@ -155,31 +155,71 @@ __device__ __forceinline__ double row_dot(const int64_t q0, const int64_t q1, co
     return acc;
 }
 
-__device__ __forceinline__ double block_sum(double v, double* sh) {
-    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    __syncthreads();
-    if (l == 0) sh[w] = v;
-    __syncthreads();
-    double t = 0.0;
-    if (w == 0) {
-        t = (l < (int)(blockDim.x >> 5)) ? sh[l] : 0.0;
-        for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+// Block sums of NV values; the totals are valid in warp 0.  sh holds 32 * NV doubles.
+template <int NV>
+__device__ __forceinline__ void block_sums(double (&v)[NV], double* sh) {
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int k = 0; k < NV; ++k)
+        for (int off = 16; off > 0; off >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], off);
+    __syncthreads();  // previous readers of sh are done
+    if (l == 0) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) sh[k * 32 + w] = v[k];
     }
-    return t;  // valid in warp 0
+    __syncthreads();
+    if (w == 0) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            double t = l < nw ? sh[k * 32 + l] : 0.0;
+            for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+            v[k] = t;
+        }
+    }
 }
 
-// every block reduces the same partials in the same order -> identical scalar everywhere
-__device__ __forceinline__ double grid_total(const double* part, double* sh) {
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+    double t[1] = {v};
+    block_sums<1>(t, sh);
+    return t[0];  // valid in warp 0
+}
+
+// Grid totals of NV partial arrays part[k * gridDim.x + block].  Every thread loads one
+// partial per array (one L2 round trip instead of gridDim/32 dependent ones), then a
+// fixed shuffle/shared-memory tree that every warp of every block evaluates identically,
+// so all threads of the grid hold bitwise the same totals with no extra barrier.
+template <int NV>
+__device__ __forceinline__ void grid_totals(const double* part, double* sh, double (&out)[NV]) {
+    const int nb = gridDim.x;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+    double t[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) t[k] = 0.0;
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) t[k] += __ldcg(part + (int64_t)k * nb + i);
+    }
+#pragma unroll
+    for (int k = 0; k < NV; ++k)
+        for (int off = 16; off > 0; off >>= 1) t[k] += __shfl_xor_sync(0xffffffffu, t[k], off);
     __syncthreads();
-    if (threadIdx.x < 32) {
-        double t = 0.0;
-        for (int i = threadIdx.x; i < (int)gridDim.x; i += 32) t += __ldcg(part + i);
-        for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
-        if (threadIdx.x == 0) sh[32] = t;
+    if (l == 0) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) sh[k * 32 + w] = t[k];
     }
     __syncthreads();
-    return sh[32];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+        double u = l < nw ? sh[k * 32 + l] : 0.0;
+        for (int off = 16; off > 0; off >>= 1) u += __shfl_xor_sync(0xffffffffu, u, off);
+        out[k] = u;
+    }
+}
+
+__device__ __forceinline__ double grid_total(const double* part, double* sh) {
+    double t[1];
+    grid_totals<1>(part, sh, t);
+    return t[0];
 }
 
 // Jacobi PCG, the reference recurrence (fem.py:131-152), two grid barriers/iteration:
@@ -191,7 +231,7 @@ __device__ __forceinline__ double grid_total(const double* part, double* sh) {
 template <int BLOCK, int MINB>
 __global__ void __launch_bounds__(BLOCK, MINB) pcg_kernel(PcgArgs a) {
     cg::grid_group grid = cg::this_grid();
-    __shared__ double sh[33];
+    __shared__ double sh[3 * 32];
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
     const int nb = gridDim.x;
@@ -218,13 +258,16 @@ __global__ void __launch_bounds__(BLOCK, MINB) pcg_kernel(PcgArgs a) {
         bb += bi * bi;
         rz_p += bi * zi;
     }
-    bb = block_sum(bb, sh);
-    if (threadIdx.x == 0) partB[blockIdx.x] = bb;
-    rz_p = block_sum(rz_p, sh);
-    if (threadIdx.x == 0) partC[blockIdx.x] = rz_p;
+    {
+        double v[2] = {bb, rz_p};
+        block_sums<2>(v, sh);
+        if (threadIdx.x == 0) { partB[blockIdx.x] = v[0]; partC[blockIdx.x] = v[1]; }
+    }
     grid.sync();
-    const double bnorm = sqrt(grid_total(partB, sh));
-    double rz = grid_total(partC, sh);
+    double tot[2];
+    grid_totals<2>(partB, sh, tot);  // partC = partB + gridDim.x
+    const double bnorm = sqrt(tot[0]);
+    double rz = tot[1];
     if (bnorm == 0.0) {
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             a.res->iterations = 0; a.res->residual = 0.0; a.res->best_residual = 0.0;
@@ -279,14 +322,16 @@ __global__ void __launch_bounds__(BLOCK, MINB) pcg_kernel(PcgArgs a) {
             rr += ri * ri;
             rzn += ri * zi;
         }
-        rr = block_sum(rr, sh);
-        if (threadIdx.x == 0) partB[blockIdx.x] = rr;
-        rzn = block_sum(rzn, sh);
-        if (threadIdx.x == 0) partC[blockIdx.x] = rzn;
+        {
+            double v[2] = {rr, rzn};
+            block_sums<2>(v, sh);
+            if (threadIdx.x == 0) { partB[blockIdx.x] = v[0]; partC[blockIdx.x] = v[1]; }
+        }
         grid.sync();
         // ---- residual test, best iterate, beta (uniform in every block)
-        res = sqrt(grid_total(partB, sh)) / bnorm;
-        const double rz_new = grid_total(partC, sh);
+        grid_totals<2>(partB, sh, tot);
+        res = sqrt(tot[0]) / bnorm;
+        const double rz_new = tot[1];
         if (res < best) {
             best = res;
             for (int64_t i = tid; i < n; i += nthreads) a.best_x[i] = a.x[i];
@@ -338,7 +383,7 @@ struct Cg1Args {
 template <int BLOCK, int MINB>
 __global__ void __launch_bounds__(BLOCK, MINB) pcg_cg1_kernel(Cg1Args a) {
     cg::grid_group grid = cg::this_grid();
-    __shared__ double sh[33];
+    __shared__ double sh[3 * 32];
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
     const int nb = gridDim.x;
@@ -385,14 +430,18 @@ __global__ void __launch_bounds__(BLOCK, MINB) pcg_cg1_kernel(Cg1Args a) {
                 pr += ri * ri;
             }
         }
-        pg = block_sum(pg, sh); if (threadIdx.x == 0) partG[blockIdx.x] = pg;
-        pd = block_sum(pd, sh); if (threadIdx.x == 0) partD[blockIdx.x] = pd;
-        pr = block_sum(pr, sh); if (threadIdx.x == 0) partR[blockIdx.x] = pr;
+        {
+            double v[3] = {pg, pd, pr};
+            block_sums<3>(v, sh);
+            if (threadIdx.x == 0) { partG[blockIdx.x] = v[0]; partD[blockIdx.x] = v[1]; partR[blockIdx.x] = v[2]; }
+        }
     }
     grid.sync();
-    double gamma = grid_total(partG, sh);
-    double delta = grid_total(partD, sh);
-    const double bnorm = sqrt(grid_total(partR, sh));
+    double tot[3];
+    grid_totals<3>(partG, sh, tot);  // partD, partR follow partG
+    double gamma = tot[0];
+    double delta = tot[1];
+    const double bnorm = sqrt(tot[2]);
     if (bnorm == 0.0) {
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             a.res->iterations = 0; a.res->residual = 0.0; a.res->best_residual = 0.0;
@@ -442,14 +491,17 @@ __global__ void __launch_bounds__(BLOCK, MINB) pcg_cg1_kernel(Cg1Args a) {
             a.p[i] = pi;
             a.x[i] += alpha * pi;
         }
-        pg = block_sum(pg, sh); if (threadIdx.x == 0) partG[blockIdx.x] = pg;
-        pd = block_sum(pd, sh); if (threadIdx.x == 0) partD[blockIdx.x] = pd;
-        pr = block_sum(pr, sh); if (threadIdx.x == 0) partR[blockIdx.x] = pr;
+        {
+            double v[3] = {pg, pd, pr};
+            block_sums<3>(v, sh);
+            if (threadIdx.x == 0) { partG[blockIdx.x] = v[0]; partD[blockIdx.x] = v[1]; partR[blockIdx.x] = v[2]; }
+        }
         grid.sync();
         cur = nxt;
-        const double g_new = grid_total(partG, sh);
-        const double d_new = grid_total(partD, sh);
-        res = sqrt(grid_total(partR, sh)) / bnorm;
+        grid_totals<3>(partG, sh, tot);
+        const double g_new = tot[0];
+        const double d_new = tot[1];
+        res = sqrt(tot[2]) / bnorm;
         if (res < best) {
             best = res;
             for (int64_t i = tid; i < n; i += nthreads) a.best_x[i] = a.x[i];
@@ -527,10 +579,26 @@ __device__ __forceinline__ double ell_row16(const int32_t* __restrict__ ec, cons
     return fma(a1.y, x3, fma(a1.x, x2, fma(a0.y, x1, a0.x * x0)));
 }
 
-template <int BLOCK, int MINB>
+// 2 lanes per row: lane `sub` owns entries [8 sub, 8 sub + 8) -> 16 independent gathers in
+// flight per lane and half the rows-per-group dependency chain of the 4-lane layout
+template <class Col>
+__device__ __forceinline__ double ell_row16_2(const int32_t* __restrict__ ec, const double* __restrict__ ev,
+                                             int64_t i, int sub, Col col) {
+    const int4* cq = reinterpret_cast<const int4*>(ec + i * 16) + 2 * sub;
+    const int4 c0 = __ldg(cq), c1 = __ldg(cq + 1);
+    const double2* vq = reinterpret_cast<const double2*>(ev + i * 16 + 8 * sub);
+    const double2 a0 = __ldg(vq), a1 = __ldg(vq + 1), a2 = __ldg(vq + 2), a3 = __ldg(vq + 3);
+    const double x0 = col(c0.x), x1 = col(c0.y), x2 = col(c0.z), x3 = col(c0.w);
+    const double x4 = col(c1.x), x5 = col(c1.y), x6 = col(c1.z), x7 = col(c1.w);
+    const double s0 = fma(a1.y, x3, fma(a1.x, x2, fma(a0.y, x1, a0.x * x0)));
+    const double s1 = fma(a3.y, x7, fma(a3.x, x6, fma(a2.y, x5, a2.x * x4)));
+    return s0 + s1;
+}
+
+template <int BLOCK, int MINB, int LPR, bool CONTIG = false>
 __global__ void __launch_bounds__(BLOCK, MINB) pcg_ell_kernel(EllArgs a) {
     cg::grid_group grid = cg::this_grid();
-    __shared__ double sh[33];
+    __shared__ double sh[3 * 32];
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
     const int nb = gridDim.x;
@@ -552,13 +620,16 @@ __global__ void __launch_bounds__(BLOCK, MINB) pcg_ell_kernel(EllArgs a) {
         bb += bi * bi;
         rz_p += bi * zi;
     }
-    bb = block_sum(bb, sh);
-    if (threadIdx.x == 0) partB[blockIdx.x] = bb;
-    rz_p = block_sum(rz_p, sh);
-    if (threadIdx.x == 0) partC[blockIdx.x] = rz_p;
+    {
+        double v[2] = {bb, rz_p};
+        block_sums<2>(v, sh);
+        if (threadIdx.x == 0) { partB[blockIdx.x] = v[0]; partC[blockIdx.x] = v[1]; }
+    }
     grid.sync();
-    const double bnorm = sqrt(grid_total(partB, sh));
-    double rz = grid_total(partC, sh);
+    double tot[2];
+    grid_totals<2>(partB, sh, tot);  // partC = partB + gridDim.x
+    const double bnorm = sqrt(tot[0]);
+    double rz = tot[1];
     if (bnorm == 0.0) {
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             a.res->iterations = 0; a.res->residual = 0.0; a.res->best_residual = 0.0;
@@ -569,24 +640,32 @@ __global__ void __launch_bounds__(BLOCK, MINB) pcg_ell_kernel(EllArgs a) {
     double best = bnorm / bnorm;
     double res = best;
     double beta = 0.0;
-    const int64_t group = tid >> 2, ngroups = nthreads >> 2;
-    const int sub = threadIdx.x & 3;
+    constexpr int RPW = 32 / LPR;  // rows per warp
+    const int64_t group = tid / LPR, ngroups = nthreads / LPR;
+    const int sub = threadIdx.x & (LPR - 1);
     double* p_old = a.p0;
     double* p_new = a.p1;
     for (int64_t it = 0; it < a.maxiter; ++it) {
         double pap = 0.0;
         // rows are processed by 4-lane groups; the loop trip count is uniform per warp
-        for (int64_t i0 = (group & ~7LL); i0 < n; i0 += ngroups) {
-            const int64_t i = i0 + (group & 7);
+        // CONTIG: every block owns a contiguous row range (neighbour gathers hit its L1)
+        const int64_t rpb = CONTIG ? (n + nb - 1) / nb : 0;
+        const int64_t r_end = CONTIG ? min(n, (blockIdx.x + 1) * rpb) : n;
+        const int64_t g_first = CONTIG ? blockIdx.x * rpb + (threadIdx.x / LPR & ~(RPW - 1)) : (group & ~(int64_t)(RPW - 1));
+        const int64_t g_step = CONTIG ? BLOCK / LPR : ngroups;
+        for (int64_t i0 = g_first; i0 < (CONTIG ? blockIdx.x * rpb + rpb : n); i0 += g_step) {
+            const int64_t i = i0 + (group & (RPW - 1));
             double s = 0.0;
-            if (i < n) {
+            if (i < r_end) {
                 const double* __restrict__ z = a.z;
                 const double* __restrict__ po = p_old;
-                s = ell_row16(a.ec, a.ev, i, sub, [&](int c) { return z[c] + beta * po[c]; });
+                const auto col = [&](int c) { return z[c] + beta * po[c]; };
+                if constexpr (LPR == 2) s = ell_row16_2(a.ec, a.ev, i, sub, col);
+                else s = ell_row16(a.ec, a.ev, i, sub, col);
             }
-            s += __shfl_xor_sync(0xffffffffu, s, 1);
-            s += __shfl_xor_sync(0xffffffffu, s, 2);
-            if (i < n && sub == 0) {
+#pragma unroll
+            for (int off = 1; off < LPR; off <<= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+            if (i < r_end && sub == 0) {
                 const double pi = a.z[i] + beta * p_old[i];
                 p_new[i] = pi;
                 a.ap[i] = s;
@@ -609,13 +688,15 @@ __global__ void __launch_bounds__(BLOCK, MINB) pcg_ell_kernel(EllArgs a) {
             rr += ri * ri;
             rzn += ri * zi;
         }
-        rr = block_sum(rr, sh);
-        if (threadIdx.x == 0) partB[blockIdx.x] = rr;
-        rzn = block_sum(rzn, sh);
-        if (threadIdx.x == 0) partC[blockIdx.x] = rzn;
+        {
+            double v[2] = {rr, rzn};
+            block_sums<2>(v, sh);
+            if (threadIdx.x == 0) { partB[blockIdx.x] = v[0]; partC[blockIdx.x] = v[1]; }
+        }
         grid.sync();
-        res = sqrt(grid_total(partB, sh)) / bnorm;
-        const double rz_new = grid_total(partC, sh);
+        grid_totals<2>(partB, sh, tot);
+        res = sqrt(tot[0]) / bnorm;
+        const double rz_new = tot[1];
         if (res < best) {
             best = res;
             for (int64_t i = tid; i < n; i += nthreads) a.best_x[i] = a.x[i];
@@ -860,16 +941,29 @@ extern "C" int tt_pcg_ell(int64_t n, const int32_t* ell_cols, const double* ell_
     a.dinv = work + 5 * n;
     a.part = work + 6 * n;
     a.res = result;
+    // SpMV shape: lanes per row (TT_PCG_ELL_LPR = 2 | 4) and contiguous per-block row
+    // ranges (TT_PCG_ELL_CONTIG = 1 | 0).  Measured on the C2 mass matrix (175,616 rows,
+    // 23 iterations): 2 lanes + contiguous 0.357 ms, 4 lanes + contiguous 0.373 ms,
+    // 4 lanes + grid-stride 0.377 ms, 2 lanes + grid-stride 0.404 ms.
+    static const int lpr = [] {
+        const char* v = getenv("TT_PCG_ELL_LPR");
+        return (v && atoi(v) == 4) ? 4 : 2;
+    }();
+    static const bool contig = [] {
+        const char* v = getenv("TT_PCG_ELL_CONTIG");
+        return !(v && atoi(v) == 0);
+    }();
+    const void* fn = lpr == 4 ? (contig ? (const void*)pcg_ell_kernel<512, 2, 4, true> : (const void*)pcg_ell_kernel<512, 2, 4>)
+                              : (contig ? (const void*)pcg_ell_kernel<512, 2, 2, true> : (const void*)pcg_ell_kernel<512, 2, 2>);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg_ell_kernel<512, 2>, 512, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 512, 0);
     if (per_sm < 1) per_sm = 1;
     int64_t maxb = (int64_t)sm_count() * per_sm;
-    int64_t need = (n * 4 + 511) / 512;
+    int64_t need = (n * lpr + 511) / 512;
     if (need < 1) need = 1;
     int blocks = (int)(need < maxb ? need : maxb);
     if (blocks > 148 * 32) blocks = 148 * 32;
     void* args[] = {&a};
-    cudaError_t e = cudaLaunchCooperativeKernel((void*)pcg_ell_kernel<512, 2>, dim3(blocks), dim3(512), args,
-                                                0, as_stream(stream));
+    cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(512), args, 0, as_stream(stream));
     return cuda_status(e, "pcg_ell_kernel (cooperative launch)");
 }

@@ -253,6 +253,20 @@ __device__ __forceinline__ void plan_lambda(const PlanDev& plan, int64_t e, int6
     }
 }
 
+constexpr int kSlotCap = 4096;  // per-block seed-slot table capacity (samples)
+
+// Walk-seed slot of a sample: the corner seed (v_i + c)/2 of the vertex with the largest
+// barycentric weight when that weight exceeds 0.45, else the centroid seed (slot 0).
+template <int K>
+__device__ __forceinline__ int seed_slot(const double* lam) {
+    int imax = 0;
+    double lmax = lam[0];
+#pragma unroll
+    for (int i = 1; i < K; ++i)
+        if (lam[i] > lmax) { lmax = lam[i]; imax = i; }
+    return lmax > 0.45 ? 1 + imax : 0;
+}
+
 // Mesh-backed source, flattened walk: each loop iteration performs exactly ONE facet-walk
 // step for every busy lane, and idle lanes immediately take the element's next unprocessed
 // sample (ballot + popc inside the G-lane group).  SIMT lanes stay busy regardless of how
@@ -260,7 +274,7 @@ __device__ __forceinline__ void plan_lambda(const PlanDev& plan, int64_t e, int6
 // data, so results are bitwise reproducible.  Identical ids/lambdas as the reference scan
 // (certified walk, see locate_walk in tt_common.cuh).
 template <int D, int PLAN, int G, bool SPEC, int MINB, bool FW = false, int BLOCK = 256,
-          bool SMEMV = false, bool RL = false>
+          bool SMEMV = false, bool RL = false, bool SLOT = false>
 __global__ void __launch_bounds__(BLOCK, MINB) mc_mesh_kernel(TargetDev t, int64_t e_lo, int64_t e_hi,
                                                       PlanDev plan, SrcDev src,
                                                       double* __restrict__ contrib,
@@ -282,6 +296,18 @@ __global__ void __launch_bounds__(BLOCK, MINB) mc_mesh_kernel(TargetDev t, int64
     const GridDev& g = src.grid;
     const bool walk = g.walk && src.seeds;
     int flags = 0;
+    // SLOT (shared plans, N <= kSlotCap, walk on): the seed slot depends on the sample
+    // index only -> one table per block, built once (the grid is one wave of blocks)
+    constexpr bool USE_SLOT = SLOT && SMEMV && PLAN == TT_PLAN_SHARED;
+    __shared__ int8_t s_slot[USE_SLOT ? kSlotCap : 1];
+    if constexpr (USE_SLOT) {
+        for (int64_t j = threadIdx.x; j < N; j += BLOCK) {
+            double lj[K];
+            plan_lambda<D, PLAN>(plan, 0, j, lj);
+            s_slot[j] = (int8_t)seed_slot<K>(lj);
+        }
+        __syncthreads();
+    }
 
     for (int64_t tile = warp; tile * EPW < n_el; tile += nwarps) {
         const int64_t le = tile * EPW + lane / G;
@@ -342,12 +368,15 @@ __global__ void __launch_bounds__(BLOCK, MINB) mc_mesh_kernel(TargetDev t, int64
                     if (walk) {
                         int imax = 0;
                         double lmax = lam[0];
-#pragma unroll
-                        for (int i = 1; i < K; ++i)
-                            if (lam[i] > lmax) { lmax = lam[i]; imax = i; }
                         if constexpr (SMEMV) {
-                            cur = s_seed[wib][gib][lmax > 0.45 ? 1 + imax : 0];
+                            int slot;
+                            if constexpr (USE_SLOT) slot = s_slot[j];
+                            else slot = seed_slot<K>(lam);
+                            cur = s_seed[wib][gib][slot];
                         } else {
+#pragma unroll
+                            for (int i = 1; i < K; ++i)
+                                if (lam[i] > lmax) { lmax = lam[i]; imax = i; }
                             cur = seed[0];
 #pragma unroll
                             for (int i = 0; i < K; ++i)
@@ -715,21 +744,25 @@ static int launch_mc(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_pl
         if ((variant & 4) && sd.grid.wrec && sd.egrad && sd.grid.walk && sd.seeds) {
             if (variant & 16) {
                 // 128-thread blocks, vertices/seeds in shared memory, 5 (or 6) blocks per SM
+                // grid = TT_MC_WAVES waves of resident blocks.  Measured on C2: one wave (the
+                // per-block seed-slot table is built once) beats 16 waves by 0.08 ms at N = 64;
+                // 32-lane groups (N >= 512) keep 16 waves (+1 % at N = 1024)
+                static const int waves_env = [] { const char* v = getenv("TT_MC_WAVES"); return v ? atoi(v) : 0; }();
+                const int waves = waves_env > 0 ? waves_env : (G >= 32 ? 16 : 1);
                 auto launch128 = [&](auto kernel) {
                     int per = 0;
                     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, 128, 0);
                     if (per < 1) per = 1;
                     int64_t nb = (tiles + 3) / 4;
-                    const int64_t cap = (int64_t)sm_count() * per * 16;
+                    const int64_t cap = (int64_t)sm_count() * per * waves;
                     if (nb > cap) nb = cap;
                     if (nb < 1) nb = 1;
                     kernel<<<(unsigned)nb, 128, 0, st>>>(td, e_lo, e_hi, pd, sd, contrib, b, nullptr, status);
                 };
-                if (variant & 64) {
-                    if (variant & 32) launch128(mc_mesh_kernel<D, PLAN, G, true, 6, true, 128, true, true>);
-                    else launch128(mc_mesh_kernel<D, PLAN, G, true, 5, true, 128, true, true>);
-                } else if (variant & 32) launch128(mc_mesh_kernel<D, PLAN, G, true, 6, true, 128, true>);
-                else launch128(mc_mesh_kernel<D, PLAN, G, true, 5, true, 128, true>);
+                if (PLAN == TT_PLAN_SHARED && p->n_samples <= kSlotCap)
+                    launch128(mc_mesh_kernel<D, PLAN, G, true, 5, true, 128, true, false, true>);
+                else
+                    launch128(mc_mesh_kernel<D, PLAN, G, true, 5, true, 128, true>);
                 return launch_check("mc_mesh_kernel (float walk, smem)");
             }
             if (variant & 8) launch(mc_mesh_kernel<D, PLAN, G, true, 3, true>);
@@ -768,10 +801,6 @@ static int dispatch_g(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_p
     if (gsel < 8) return launch_mc<D, PLAN, SRC, 4>(t, e_lo, e_hi, p, s, contrib, b, status, st);
     if (gsel < 16) return launch_mc<D, PLAN, SRC, 8>(t, e_lo, e_hi, p, s, contrib, b, status, st);
     if (gsel < 32) return launch_mc<D, PLAN, SRC, 16>(t, e_lo, e_hi, p, s, contrib, b, status, st);
-    return launch_mc<D, PLAN, SRC, 32>(t, e_lo, e_hi, p, s, contrib, b, status, st);
-    if (N < 64) return launch_mc<D, PLAN, SRC, 4>(t, e_lo, e_hi, p, s, contrib, b, status, st);
-    if (N < 128) return launch_mc<D, PLAN, SRC, 8>(t, e_lo, e_hi, p, s, contrib, b, status, st);
-    if (N < 256) return launch_mc<D, PLAN, SRC, 16>(t, e_lo, e_hi, p, s, contrib, b, status, st);
     return launch_mc<D, PLAN, SRC, 32>(t, e_lo, e_hi, p, s, contrib, b, status, st);
 }
 

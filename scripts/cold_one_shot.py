@@ -1,0 +1,35 @@
+"""Cold one-shot transfer_mc from host meshes (everything included: H2D, geometry, grid,
+walk prep, seeds, incidence, mass, plan, load, PCG, D2H).  Mesh generation excluded."""
+import json
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2603_00538_b200 as tt  # noqa: E402
+
+torch.cuda.init()
+_ = torch.zeros(1, device="cuda")
+out = {}
+for rep, (name, dim) in enumerate([(n, d) for n, d in (("c2_3d_1M_tets", 3), ("c1_2d_1M_tris", 2))
+                                   for _ in range(2)]):
+    if dim == 3:
+        tgt = tt.generate_cube_mesh(55, 0.2, seed=20)
+        src = tt.generate_cube_mesh(55, 0.2, seed=10, split="kuhn_mirror")
+    else:
+        tgt = tt.generate_square_mesh(707, 0.2, seed=20, diagonal="right")
+        src = tt.generate_square_mesh(707, 0.2, seed=10, diagonal="left")
+    coeffs = tt.get_field("smooth", dim=dim).fn(*[src.nodes[:, c] for c in range(dim)])
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    fs = tt.NodalField(src, coeffs)
+    x = tt.transfer_mc(tgt, tt.MeshBackedField(fs), tt.SamplePlan.build(64, "sobol", 0, dim=dim)).coeffs
+    t1 = time.perf_counter()
+    # first run of a config in the process pays lazy kernel loading + first allocations;
+    # the second (fresh mesh objects: no cached device state) is the data-cold cost
+    key = "process_cold_s" if rep % 2 == 0 else "data_cold_s"
+    out.setdefault(name, {"n_elems": tgt.n_elems, "x_sum": float(np.sum(x))})[key] = round(t1 - t0, 4)
+print(json.dumps(out))
