@@ -253,6 +253,15 @@ __device__ __forceinline__ void plan_lambda(const PlanDev& plan, int64_t e, int6
     }
 }
 
+#ifdef TT_MC_STATS
+// instrumentation build only (-DTT_MC_STATS): loop iterations, busy lanes, samples, walk
+// steps, exact fallbacks of mc_mesh_kernel
+__device__ unsigned long long g_mc_stats[8];
+#define TT_STAT(i, v) atomicAdd(&g_mc_stats[i], (unsigned long long)(v))
+#else
+#define TT_STAT(i, v) ((void)0)
+#endif
+
 constexpr int kSlotCap = 4096;  // per-block seed-slot table capacity (samples)
 
 // Walk-seed slot of a sample: the corner seed (v_i + c)/2 of the vertex with the largest
@@ -299,7 +308,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) mc_mesh_kernel(TargetDev t, int64
     // SLOT (shared plans, N <= kSlotCap, walk on): the seed slot depends on the sample
     // index only -> one table per block, built once (the grid is one wave of blocks)
     constexpr bool USE_SLOT = SLOT && SMEMV && PLAN == TT_PLAN_SHARED;
-    __shared__ int8_t s_slot[USE_SLOT ? kSlotCap : 1];
+    extern __shared__ int8_t s_slot[];  // N bytes (launch: dynamic shared memory)
     if constexpr (USE_SLOT) {
         for (int64_t j = threadIdx.x; j < N; j += BLOCK) {
             double lj[K];
@@ -390,6 +399,12 @@ __global__ void __launch_bounds__(BLOCK, MINB) mc_mesh_kernel(TargetDev t, int64
             }
             next += __popc(m);
             if (!__any_sync(FULL, busy)) break;
+#ifdef TT_MC_STATS
+            {
+                const unsigned bm = __ballot_sync(FULL, busy);
+                if (lane == 0) { TT_STAT(0, 1); TT_STAT(1, __popc(bm)); }
+            }
+#endif
             if (!busy) continue;
             double l[K];
             int hit = -1;
@@ -447,6 +462,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) mc_mesh_kernel(TargetDev t, int64
                             if (imin == i) nb = w.nbr[i];
                         cur = nb;
                         ++steps;
+                        TT_STAT(3, 1);
                     }
                 } else {
                     cur = -1;
@@ -514,6 +530,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) mc_mesh_kernel(TargetDev t, int64
                 done = true;
             }
             if (done) {
+                TT_STAT(2, 1);
+                if (!fw_hit) TT_STAT(4, 1);
                 if (ids_out) ids_out[le * N + jcur] = hit;
                 double f = 0.0;
                 if (FW && fw_hit) {
@@ -749,6 +767,8 @@ static int launch_mc(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_pl
                 // 32-lane groups (N >= 512) keep 16 waves (+1 % at N = 1024)
                 static const int waves_env = [] { const char* v = getenv("TT_MC_WAVES"); return v ? atoi(v) : 0; }();
                 const int waves = waves_env > 0 ? waves_env : (G >= 32 ? 16 : 1);
+                const bool slot = PLAN == TT_PLAN_SHARED && p->n_samples <= kSlotCap;
+                const size_t dyn_smem = slot ? (size_t)((p->n_samples + 15) / 16 * 16) : 0;
                 auto launch128 = [&](auto kernel) {
                     int per = 0;
                     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, 128, 0);
@@ -757,12 +777,16 @@ static int launch_mc(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_pl
                     const int64_t cap = (int64_t)sm_count() * per * waves;
                     if (nb > cap) nb = cap;
                     if (nb < 1) nb = 1;
-                    kernel<<<(unsigned)nb, 128, 0, st>>>(td, e_lo, e_hi, pd, sd, contrib, b, nullptr, status);
+                    // dynamic shared memory = the seed-slot table (N bytes, SLOT kernels only):
+                    // every byte of shared memory is L1 the walk's records lose (measured:
+                    // +20 KB/block costs 0.056 ms at C2)
+                    kernel<<<(unsigned)nb, 128, dyn_smem, st>>>(td, e_lo, e_hi, pd, sd, contrib, b, nullptr, status);
                 };
-                if (PLAN == TT_PLAN_SHARED && p->n_samples <= kSlotCap)
+                if (slot) {
                     launch128(mc_mesh_kernel<D, PLAN, G, true, 5, true, 128, true, false, true>);
-                else
+                } else {
                     launch128(mc_mesh_kernel<D, PLAN, G, true, 5, true, 128, true>);
+                }
                 return launch_check("mc_mesh_kernel (float walk, smem)");
             }
             if (variant & 8) launch(mc_mesh_kernel<D, PLAN, G, true, 3, true>);
@@ -1068,3 +1092,14 @@ extern "C" int tt_reduce_nodes_peers(int64_t n_nodes, int k, const int64_t* inc_
         n_nodes, k, inc_start, inc, n_ranks, range_lo, contrib_ptrs, b);
     return launch_check("reduce_nodes_peers_kernel");
 }
+
+#ifdef TT_MC_STATS
+extern "C" int tt_debug_mc_stats(unsigned long long* out, int reset) {
+    cudaMemcpyFromSymbol(out, g_mc_stats, sizeof(unsigned long long) * 8);
+    if (reset) {
+        unsigned long long z[8] = {0};
+        cudaMemcpyToSymbol(g_mc_stats, z, sizeof z);
+    }
+    return 0;
+}
+#endif
