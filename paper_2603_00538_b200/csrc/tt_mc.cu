@@ -419,7 +419,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) mc_mesh_kernel(TargetDev t, int64
                     // gradient record: f = c_last + g . (x - o), accurate to a few ulps
                     WRec<D> w;
                     load_wrec<D>(g.wrec, cur, w);
-                    if (src.egrad) {
+                    if (SPEC && src.egrad) {  // speculative: the gradient record of the element tested
                         const double2* q = reinterpret_cast<const double2*>(src.egrad + (int64_t)cur * 4);
                         pc0 = __ldg(q);
                         pc1 = __ldg(q + 1);
@@ -448,6 +448,11 @@ __global__ void __launch_bounds__(BLOCK, MINB) mc_mesh_kernel(TargetDev t, int64
                         hit = cur;
                         done = true;
                         fw_hit = true;
+                        if (!SPEC) {  // load the gradient record of the hit only
+                            const double2* q = reinterpret_cast<const double2*>(src.egrad + (int64_t)cur * 4);
+                            pc0 = __ldg(q);
+                            pc1 = __ldg(q + 1);
+                        }
                         const double gv[4] = {pc0.x, pc0.y, pc1.x, pc1.y};
                         double f = gv[D];
 #pragma unroll

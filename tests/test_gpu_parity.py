@@ -518,3 +518,39 @@ def test_mc_operator_fold_3d(tt):
     ones = tt.NodalField(src, np.ones(src.n_nodes))
     ref1 = tt.assemble_load_mc(tgt, tt.AnalyticField(lambda x, y, z: np.full_like(x, 1.0)), plan)
     np.testing.assert_allclose(op.load(ones).cpu().numpy(), ref1, rtol=1e-12)
+
+
+@pytest.mark.parametrize("n", [4096, 4100])
+def test_3d_mesh_backed_large_n_matches_oracle(tt, n):
+    """N <= 4096 uses the per-block seed-slot table (N bytes of dynamic shared memory),
+    N > 4096 the kernel that derives the slot per sample: both equal the oracle."""
+    tgt = tt.generate_cube_mesh(2, 0.2, seed=20, split="kuhn")
+    src = tt.generate_cube_mesh(4, 0.2, seed=10, split="kuhn_mirror")
+    fs = tt.NodalField.from_function(src, tt.get_field("smooth", dim=3).fn)
+    plan = tt.SamplePlan.build(n, "sobol", 0, dim=3)
+    b = tt.assemble_load_mc(tgt, tt.MeshBackedField(fs), plan)
+    g = O.Grid(src.nodes, src.elements)
+    area = np.abs(O.signed_measure(tgt.nodes, tgt.elements))
+    contrib = O.accumulate(tgt.nodes, tgt.elements, area, O.bary_map(O.sobol(n, 3)),
+                           lambda P: O.mesh_backed_eval(g, fs.coeffs, P))
+    assert _rel(b, O.reduce_to_nodes(tgt.n_nodes, tgt.elements, contrib)) <= 1e-12
+
+
+@pytest.mark.parametrize("shape", [("4", "1"), ("4", "0"), ("2", "0")])
+def test_ell_pcg_spmv_shapes_agree(tt, golden, c1, shape):
+    """Non-default ELL SpMV shapes (TT_PCG_ELL_LPR lanes per row, TT_PCG_ELL_CONTIG row
+    ranges; read once per process) reach the reference x like the default."""
+    import json
+    import os
+    import subprocess
+    import sys
+    code = ("import numpy as np, json, sys; sys.path.insert(0, '.'); import paper_2603_00538_b200 as tt;"
+            "z = np.load('tests/golden/ref_2d.npz');"
+            "t = tt.TriMesh.from_arrays(z['c1t_nodes'], z['c1t_elements']);"
+            "x = tt.cg_solve(tt.assemble_mass_matrix(t), z['b_c1_mesh_smooth'], tol=1e-14);"
+            "print(json.dumps(float(np.max(np.abs(x - z['x_c1_mesh_tol14'])))))")
+    env = dict(os.environ, TT_PCG_ELL_LPR=shape[0], TT_PCG_ELL_CONTIG=shape[1])
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                         cwd=str(__import__("pathlib").Path(__file__).resolve().parents[1]))
+    assert out.returncode == 0, out.stderr
+    assert json.loads(out.stdout.strip().splitlines()[-1]) <= 1e-12
