@@ -222,6 +222,21 @@ __device__ __forceinline__ double grid_total(const double* part, double* sh) {
     return t[0];
 }
 
+// x double-buffering for the best-iterate bookkeeping (fem.py:141-152): the iterate lives
+// in X[c], the best iterate in X[bi] (X = {x, best_x}).  An update writes in place unless
+// X[c] is the best, then into the other buffer, so no per-iteration copy is needed.  On
+// exit the final iterate goes to x and the best to best_x; every thread settles exactly
+// the rows it updated (the same tid-strided rows), so no barrier is needed.
+__device__ __forceinline__ void settle_iterates(double* x, double* bx, int c, int bi, int64_t n,
+                                                int64_t tid, int64_t nthreads) {
+    if (c == 0 && bi == 1) return;
+    for (int64_t i = tid; i < n; i += nthreads) {
+        const double xc = (c == 0 ? x : bx)[i], xb = (bi == 0 ? x : bx)[i];
+        x[i] = xc;
+        bx[i] = xb;
+    }
+}
+
 // Jacobi PCG, the reference recurrence (fem.py:131-152), two grid barriers/iteration:
 //   A: p_new = z + beta p_old formed on the fly for every gathered column (identical
 //      bits in every block), own rows stored; Ap = M p_new; partial p.Ap    | sync
@@ -282,6 +297,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) pcg_kernel(PcgArgs a) {
     const int64_t warp_id = tid >> 5, nwarps = nthreads >> 5;
     const int lane = threadIdx.x & 31;
     const int sub = lane % kRowG;
+    int xc = 0, xbi = 0;  // current / best iterate buffers (settle_iterates)
     double* p_old = a.p0;
     double* p_new = a.p1;
     for (int64_t it = 0; it < a.maxiter; ++it) {
@@ -311,12 +327,15 @@ __global__ void __launch_bounds__(BLOCK, MINB) pcg_kernel(PcgArgs a) {
         // ---- B: alpha, x += alpha p, r -= alpha Ap, z = dinv r; partial rr, rz
         const double alpha = rz / grid_total(partA, sh);
         double rr = 0.0, rzn = 0.0;
+        const double* xs = xc == 0 ? a.x : a.best_x;  // may alias xw (in-place update)
+        const int xw_i = xc == xbi ? 1 - xc : xc;
+        double* xw = xw_i == 0 ? a.x : a.best_x;
         for (int64_t i = tid; i < n; i += nthreads) {
             const double pi = p_new[i];
-            const double xi = a.x[i] + alpha * pi;
+            const double xi = xs[i] + alpha * pi;
             const double ri = a.r[i] - alpha * a.ap[i];
             const double zi = a.dinv[i] * ri;
-            a.x[i] = xi;
+            xw[i] = xi;
             a.r[i] = ri;
             a.z[i] = zi;
             rr += ri * ri;
@@ -332,11 +351,13 @@ __global__ void __launch_bounds__(BLOCK, MINB) pcg_kernel(PcgArgs a) {
         grid_totals<2>(partB, sh, tot);
         res = sqrt(tot[0]) / bnorm;
         const double rz_new = tot[1];
+        xc = xw_i;
         if (res < best) {
             best = res;
-            for (int64_t i = tid; i < n; i += nthreads) a.best_x[i] = a.x[i];
+            xbi = xc;
         }
         if (res <= a.tol) {
+            settle_iterates(a.x, a.best_x, xc, xbi, n, tid, nthreads);
             if (blockIdx.x == 0 && threadIdx.x == 0) {
                 a.res->iterations = it + 1; a.res->residual = res; a.res->best_residual = best;
                 a.res->converged = 1; a.res->zero_rhs = 0;
@@ -347,6 +368,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) pcg_kernel(PcgArgs a) {
         rz = rz_new;
         double* t = p_old; p_old = p_new; p_new = t;
     }
+    settle_iterates(a.x, a.best_x, xc, xbi, n, tid, nthreads);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         a.res->iterations = a.maxiter; a.res->residual = res; a.res->best_residual = best;
         a.res->converged = 0; a.res->zero_rhs = 0;
@@ -643,6 +665,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) pcg_ell_kernel(EllArgs a) {
     constexpr int RPW = 32 / LPR;  // rows per warp
     const int64_t group = tid / LPR, ngroups = nthreads / LPR;
     const int sub = threadIdx.x & (LPR - 1);
+    int xc = 0, xbi = 0;  // current / best iterate buffers (settle_iterates)
     double* p_old = a.p0;
     double* p_new = a.p1;
     for (int64_t it = 0; it < a.maxiter; ++it) {
@@ -677,12 +700,15 @@ __global__ void __launch_bounds__(BLOCK, MINB) pcg_ell_kernel(EllArgs a) {
         grid.sync();
         const double alpha = rz / grid_total(partA, sh);
         double rr = 0.0, rzn = 0.0;
+        const double* xs = xc == 0 ? a.x : a.best_x;  // may alias xw (in-place update)
+        const int xw_i = xc == xbi ? 1 - xc : xc;
+        double* xw = xw_i == 0 ? a.x : a.best_x;
         for (int64_t i = tid; i < n; i += nthreads) {
             const double pi = p_new[i];
-            const double xi = a.x[i] + alpha * pi;
+            const double xi = xs[i] + alpha * pi;
             const double ri = a.r[i] - alpha * a.ap[i];
             const double zi = a.dinv[i] * ri;
-            a.x[i] = xi;
+            xw[i] = xi;
             a.r[i] = ri;
             a.z[i] = zi;
             rr += ri * ri;
@@ -697,11 +723,13 @@ __global__ void __launch_bounds__(BLOCK, MINB) pcg_ell_kernel(EllArgs a) {
         grid_totals<2>(partB, sh, tot);
         res = sqrt(tot[0]) / bnorm;
         const double rz_new = tot[1];
+        xc = xw_i;
         if (res < best) {
             best = res;
-            for (int64_t i = tid; i < n; i += nthreads) a.best_x[i] = a.x[i];
+            xbi = xc;
         }
         if (res <= a.tol) {
+            settle_iterates(a.x, a.best_x, xc, xbi, n, tid, nthreads);
             if (blockIdx.x == 0 && threadIdx.x == 0) {
                 a.res->iterations = it + 1; a.res->residual = res; a.res->best_residual = best;
                 a.res->converged = 1; a.res->zero_rhs = 0;
@@ -712,6 +740,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) pcg_ell_kernel(EllArgs a) {
         rz = rz_new;
         double* t = p_old; p_old = p_new; p_new = t;
     }
+    settle_iterates(a.x, a.best_x, xc, xbi, n, tid, nthreads);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         a.res->iterations = a.maxiter; a.res->residual = res; a.res->best_residual = best;
         a.res->converged = 0; a.res->zero_rhs = 0;

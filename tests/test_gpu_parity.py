@@ -554,3 +554,38 @@ def test_ell_pcg_spmv_shapes_agree(tt, golden, c1, shape):
                          cwd=str(__import__("pathlib").Path(__file__).resolve().parents[1]))
     assert out.returncode == 0, out.stderr
     assert json.loads(out.stdout.strip().splitlines()[-1]) <= 1e-12
+
+
+@pytest.mark.parametrize("path", ["ell", "csr"])
+def test_pcg_best_iterate_matches_oracle(tt, path):
+    """NoConvergence carries the best iterate (fem.py:141-152).  An SPD matrix whose
+    preconditioned residual is NOT monotone (increases at iterations 2, 6, 8, 10) drives
+    every state of the device's double-buffered iterate bookkeeping; best_x, the
+    residual and the converged x match the oracle recurrence."""
+    import scipy.sparse as sp
+    import torch
+    from paper_2603_00538_b200 import fem
+    rng = np.random.default_rng(4)
+    n = 40
+    B = sp.diags([rng.standard_normal(n - k) for k in range(4)], [0, 1, 2, 3]).tocsr()
+    A = (B.T @ B + 1e-3 * sp.eye(n)).tocsr()
+    A.sort_indices()
+    b = rng.standard_normal(n)
+    dev = torch.device("cuda")
+    M = fem.SparseSymMatrix(n, torch.as_tensor(A.indptr.astype(np.int64), device=dev),
+                            torch.as_tensor(A.indices.astype(np.int32), device=dev),
+                            torch.as_tensor(A.data, device=dev))
+    fem._PCG_PATH = path
+    try:
+        for maxiter in range(1, 11):
+            with pytest.raises(tt.NoConvergence) as got:
+                tt.cg_solve(M, b, tol=1e-16, maxiter=maxiter)
+            with pytest.raises(O.NoConvergence) as ref:
+                O.cg_solve(A, b, tol=1e-16, maxiter=maxiter)
+            assert got.value.residual == pytest.approx(ref.value.residual, rel=1e-9)
+            assert _rel(got.value.best_x, ref.value.best_x) <= 1e-9
+        x = tt.cg_solve(M, b, tol=1e-13)
+        xr, _ = O.cg_solve(A, b, tol=1e-13)
+        assert _rel(x, xr) <= 1e-8
+    finally:
+        fem._PCG_PATH = "ell"
