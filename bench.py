@@ -317,6 +317,11 @@ def run_ours(args):
     alg_bytes = (E_loc * (4 * K + 8 * D * K + 8 + 8 * K)       # target conn, coords, measure, contrib
                  + 8 * (n_cells + 1) + 4 * int(loc.cell_elems_dev.numel())
                  + src.n_elems * (8 * (D * D + D) + 4 * K) + 8 * src.n_nodes)
+    folded = args.config == "c5" and ops[plan.n_samples].R is not None
+    if folded:
+        # b = R c: CSR row pointers, column indices and values, c and b, each once
+        nnz_r = int(ops[plan.n_samples].R[2].numel())
+        alg_bytes = 8 * (tgt.n_nodes + 1) + 12 * nnz_r + 8 * src.n_nodes + 8 * tgt.n_nodes
     peak_hbm = None
     try:
         peak_hbm = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"]
@@ -334,7 +339,8 @@ def run_ours(args):
         pass
     same = args.config == "c2" and args.samples == 64 and world == 1 and args.mode == "sobol"
     traffic = ncu.get("dram_bytes_per_launch") if same else None
-    fp64_fl = ncu.get("fp64_flops_per_sample", 0.0) * E_loc * args.samples
+    fp64_fl = (2.0 * nnz_r if folded                 # one FMA per nonzero of R
+               else ncu.get("fp64_flops_per_sample", 0.0) * E_loc * args.samples)
     fp64_achieved = fp64_fl / (k_ms * 1e-3) / 1e12 if fp64_fl else None
 
     # --- e2e: public API, pinned host coefficients in, x out, every step
@@ -409,23 +415,30 @@ def run_ours(args):
                     "h2d_bytes_per_step": src.n_nodes * 8, "d2h_bytes_per_step": tgt.n_nodes * 8,
                     "api": "NodalField(pinned H2D) -> transfer_mc(MeshBackedField) | "
                            "MCTransferOperator.apply (c5) | DistributedCoupling.step (N>1) -> x D2H"},
-            "roofline": {"bound": "hbm", "kernel": "mc_load_kernel<3,SHARED,CACHED>" if args.config == "c5" else "mc_mesh_kernel<3,SHARED,G,spec>",
+            "roofline": {"bound": "hbm",
+                         "kernel": ("spmv_rect (folded R @ c)" if folded else "mc_load_kernel<3,SHARED,CACHED>")
+                         if args.config == "c5" else "mc_mesh_kernel<3,SHARED,G,spec>",
                          "achieved": achieved, "peak": peak_hbm, "unit": "GB/s",
                          "frac": achieved / peak_hbm, "peak_source": peak_src,
                          "traffic": traffic, "kernel_ms": k_ms, "algorithmic_bytes": alg_bytes,
                          "traffic_source": "profiles/r01/ncu_dominant_kernel.json" if traffic else None,
                          "fp64": {"achieved": fp64_achieved, "peak": fp64, "unit": "TFLOP/s",
                                   "frac": fp64_achieved / fp64 if fp64_achieved else None,
-                                  "flops_per_sample": ncu.get("fp64_flops_per_sample"),
+                                  "flops_per_sample": (2.0 * nnz_r / (E_loc * args.samples) if folded
+                                                       else ncu.get("fp64_flops_per_sample")),
                                   "peak_source": "measured in this run (tt_fp64_peak_probe, DFMA)"},
                          "l1_data_pipe_pct_ncu": ncu.get("l1_data_pipe_pct") if same else None,
-                         "note": "fused gather kernel: < 1 compulsory HBM byte per sample (DRAM 2 %); "
+                         "note": ("streaming CSR SpMV over the folded load matrix R (12 B per nonzero); "
+                                  "the PCG that follows dominates the step") if folded else
+                                 "fused gather kernel: < 1 compulsory HBM byte per sample (DRAM 2 %); "
                                  "limited by dependent-load latency and the L1 data pipe (ncu)"},
             "fp64_peak_tflops": fp64,
             "sweep": sweep,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
-            "gpu_launches": (3 if args.config == "c5" else 4) * args.steps,
+            # per step: c5 folded = spmv_rect + pcg_ell; c5 cached = pack_coeffs + mc_load +
+            # reduce_nodes + pcg_ell; else pack_grad + mc kernel + reduce_nodes + pcg_ell
+            "gpu_launches": (2 if folded else 4) * args.steps,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

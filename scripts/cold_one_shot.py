@@ -1,5 +1,6 @@
 """Cold one-shot transfer_mc from host meshes (everything included: H2D, geometry, grid,
-walk prep, seeds, incidence, mass, plan, load, PCG, D2H).  Mesh generation excluded."""
+walk prep, seeds, incidence, mass, plan, load, PCG, D2H).  Mesh generation excluded.
+Prints per-config runs, the first-in-process time and the data-cold minimum."""
 import json
 import sys
 import time
@@ -14,8 +15,9 @@ import paper_2603_00538_b200 as tt  # noqa: E402
 torch.cuda.init()
 _ = torch.zeros(1, device="cuda")
 out = {}
+REPS = 4
 for rep, (name, dim) in enumerate([(n, d) for n, d in (("c2_3d_1M_tets", 3), ("c1_2d_1M_tris", 2))
-                                   for _ in range(2)]):
+                                   for _ in range(REPS)]):
     if dim == 3:
         tgt = tt.generate_cube_mesh(55, 0.2, seed=20)
         src = tt.generate_cube_mesh(55, 0.2, seed=10, split="kuhn_mirror")
@@ -28,8 +30,13 @@ for rep, (name, dim) in enumerate([(n, d) for n, d in (("c2_3d_1M_tets", 3), ("c
     fs = tt.NodalField(src, coeffs)
     x = tt.transfer_mc(tgt, tt.MeshBackedField(fs), tt.SamplePlan.build(64, "sobol", 0, dim=dim)).coeffs
     t1 = time.perf_counter()
-    # first run of a config in the process pays lazy kernel loading + first allocations;
-    # the second (fresh mesh objects: no cached device state) is the data-cold cost
-    key = "process_cold_s" if rep % 2 == 0 else "data_cold_s"
-    out.setdefault(name, {"n_elems": tgt.n_elems, "x_sum": float(np.sum(x))})[key] = round(t1 - t0, 4)
+    # the first run of a config in the process pays lazy kernel loading and the caching
+    # allocator's growth (fresh cudaMalloc); the later runs use fresh mesh objects (no
+    # cached device state) once the allocator has grown: their minimum is the data-cold cost
+    o = out.setdefault(name, {"n_elems": tgt.n_elems, "x_sum": float(np.sum(x)), "runs_s": []})
+    o["runs_s"].append(round(t1 - t0, 4))
+    del tgt, src, coeffs, x, fs
+for o in out.values():
+    o["process_cold_s"] = o["runs_s"][0]
+    o["data_cold_s"] = min(o["runs_s"][1:])
 print(json.dumps(out))
