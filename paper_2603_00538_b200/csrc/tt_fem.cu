@@ -222,6 +222,20 @@ __device__ __forceinline__ double grid_total(const double* part, double* sh) {
     return t[0];
 }
 
+#ifdef TT_PCG_TRACE
+// instrumentation build only (-DTT_PCG_TRACE): %globaltimer at the phase boundaries of the
+// first 64 iterations, recorded by thread 0 of block 0
+__device__ unsigned long long g_pcg_trace[64][6];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define PCG_MARK(it, k) if (blockIdx.x == 0 && threadIdx.x == 0 && (it) < 64) g_pcg_trace[it][k] = gtimer()
+#else
+#define PCG_MARK(it, k) ((void)0)
+#endif
+
 // x double-buffering for the best-iterate bookkeeping (fem.py:141-152): the iterate lives
 // in X[c], the best iterate in X[bi] (X = {x, best_x}).  An update writes in place unless
 // X[c] is the best, then into the other buffer, so no per-iteration copy is needed.  On
@@ -669,6 +683,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) pcg_ell_kernel(EllArgs a) {
     double* p_old = a.p0;
     double* p_new = a.p1;
     for (int64_t it = 0; it < a.maxiter; ++it) {
+        PCG_MARK(it, 0);
         double pap = 0.0;
         // rows are processed by 4-lane groups; the loop trip count is uniform per warp
         // CONTIG: every block owns a contiguous row range (neighbour gathers hit its L1)
@@ -695,10 +710,13 @@ __global__ void __launch_bounds__(BLOCK, MINB) pcg_ell_kernel(EllArgs a) {
                 pap += pi * s;
             }
         }
+        PCG_MARK(it, 1);
         pap = block_sum(pap, sh);
         if (threadIdx.x == 0) partA[blockIdx.x] = pap;
         grid.sync();
+        PCG_MARK(it, 2);
         const double alpha = rz / grid_total(partA, sh);
+        PCG_MARK(it, 3);
         double rr = 0.0, rzn = 0.0;
         const double* xs = xc == 0 ? a.x : a.best_x;  // may alias xw (in-place update)
         const int xw_i = xc == xbi ? 1 - xc : xc;
@@ -714,12 +732,14 @@ __global__ void __launch_bounds__(BLOCK, MINB) pcg_ell_kernel(EllArgs a) {
             rr += ri * ri;
             rzn += ri * zi;
         }
+        PCG_MARK(it, 4);
         {
             double v[2] = {rr, rzn};
             block_sums<2>(v, sh);
             if (threadIdx.x == 0) { partB[blockIdx.x] = v[0]; partC[blockIdx.x] = v[1]; }
         }
         grid.sync();
+        PCG_MARK(it, 5);
         grid_totals<2>(partB, sh, tot);
         res = sqrt(tot[0]) / bnorm;
         const double rz_new = tot[1];
@@ -746,6 +766,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) pcg_ell_kernel(EllArgs a) {
         a.res->converged = 0; a.res->zero_rhs = 0;
     }
 }
+
 
 __global__ void spmv_kernel(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
                             const double* __restrict__ v, const double* __restrict__ x,
@@ -996,3 +1017,9 @@ extern "C" int tt_pcg_ell(int64_t n, const int32_t* ell_cols, const double* ell_
     cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(512), args, 0, as_stream(stream));
     return cuda_status(e, "pcg_ell_kernel (cooperative launch)");
 }
+
+#ifdef TT_PCG_TRACE
+extern "C" int tt_debug_pcg_trace(unsigned long long* out) {
+    return (int)cudaMemcpyFromSymbol(out, g_pcg_trace, sizeof(g_pcg_trace));
+}
+#endif
