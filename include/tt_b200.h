@@ -56,6 +56,7 @@ extern "C" {
 #define TT_FLAG_CAPACITY         4  /* row/list capacity exceeded in assembly            */
 #define TT_FLAG_INVALID_DENSITY  8  /* InvalidDensity: p <= 0          montecarlo.py:129-130 */
 #define TT_FLAG_NONMANIFOLD     16  /* a facet shared by > 2 elements (mesh.py:50-53)      */
+#define TT_FLAG_WIDE_ROWS       32  /* an ELL column is > 32767 rows from its row: no slab  */
 
 /* ---- enums ---- */
 #define TT_PLAN_SHARED  0   /* one (N, k) barycentric table shared by all elements (reference) */
@@ -306,6 +307,14 @@ int tt_pcg_ell(int64_t n, const int32_t* ell_cols, const double* ell_vals, const
                const double* b, double tol, int64_t maxiter, double* x, double* best_x,
                double* work /* tt_pcg_workspace_doubles(n) */, tt_pcg_result_t* result,
                void* stream);
+/* The same PCG with each block's rows of the ELL matrix held in shared memory for the
+ * whole solve (160 B per row; fits when n <= ~1400 rows per SM).  Precondition: tt_csr_to_ell
+ * did not set TT_FLAG_WIDE_ROWS.  Returns TT_ERR_CAPACITY, launching nothing, when the rows
+ * do not fit (the caller then uses tt_pcg_ell). */
+int tt_pcg_ell_slab(int64_t n, const int32_t* ell_cols, const double* ell_vals, const double* diag,
+                    const double* b, double tol, int64_t maxiter, double* x, double* best_x,
+                    double* work /* tt_pcg_workspace_doubles(n) */, tt_pcg_result_t* result,
+                    void* stream);
 int tt_spmv(int64_t n, const int64_t* row_ptr, const int32_t* cols, const double* vals,
             const double* x, double* y, void* stream);
 

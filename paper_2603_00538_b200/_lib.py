@@ -22,6 +22,7 @@ LIB_PATH = Path(os.environ.get("TT_LIB_PATH") or Path(__file__).resolve().parent
 TT_OK, TT_ERR_INVALID_PARAMETER, TT_ERR_DIMENSION_MISMATCH, TT_ERR_CUDA, TT_ERR_CAPACITY = 0, 1, 2, 3, 4
 TT_FLAG_NONFINITE, TT_FLAG_OUTSIDE_STRICT, TT_FLAG_CAPACITY, TT_FLAG_INVALID_DENSITY = 1, 2, 4, 8
 TT_FLAG_NONMANIFOLD = 16
+TT_FLAG_WIDE_ROWS = 32
 TT_PLAN_SHARED, TT_PLAN_PHILOX = 0, 1
 TT_SRC_EXPR, TT_SRC_MESH, TT_SRC_VALUES, TT_SRC_CACHED = 0, 1, 2, 3
 TT_OUTSIDE_SNAP, TT_OUTSIDE_STRICT = 0, 1
@@ -124,6 +125,7 @@ _SIGNATURES = {
     "tt_pcg": ([_I64, _P, _P, _P, _P, _D, _I64, _P, _P, _P, _P, _P], _I),
     "tt_csr_to_ell": ([_I64, _P, _P, _P, _I, _P, _P, _P, _P, _P], _I),
     "tt_pcg_ell": ([_I64, _P, _P, _P, _P, _D, _I64, _P, _P, _P, _P, _P], _I),
+    "tt_pcg_ell_slab": ([_I64, _P, _P, _P, _P, _D, _I64, _P, _P, _P, _P, _P], _I),
     "tt_spmv": ([_I64, _P, _P, _P, _P, _P, _P], _I),
     "tt_integrate_p1": ([C.POINTER(tt_mesh_t), _P, _P, _P], _I),
     "tt_fp64_peak_probe": ([_I64, _P, C.POINTER(_I), C.POINTER(_I), _P], _I),
@@ -177,6 +179,15 @@ def check(code: int, what: str = ""):
 def call(name: str, *args):
     fn = getattr(lib(), name)
     check(fn(*args), name)
+
+
+def call_status(name: str, *args) -> int:
+    """Call an entry point that reports TT_ERR_CAPACITY as a normal outcome (nothing was
+    launched, the caller picks another kernel); any other error raises."""
+    code = getattr(lib(), name)(*args)
+    if code != TT_ERR_CAPACITY:
+        check(code, name)
+    return code
 
 
 def ptr(t) -> C.c_void_p:

@@ -579,6 +579,7 @@ __global__ void csr_to_ell_kernel(int64_t n, const int64_t* __restrict__ rp, con
         const int c = in ? ci[q0 + t] : (int)i;
         const double a = in ? v[q0 + t] : 0.0;
         if (in && c == i) d = a;
+        if (in && (c - i > 32767 || i - c > 32767)) atomicOr(status, TT_FLAG_WIDE_ROWS);
         ec[i * W + t] = c;
         ev[i * W + t] = a;
     }
@@ -631,10 +632,37 @@ __device__ __forceinline__ double ell_row16_2(const int32_t* __restrict__ ec, co
     return s0 + s1;
 }
 
-template <int BLOCK, int MINB, int LPR, bool CONTIG = false>
+// SLAB (2 lanes per row, contiguous row ranges): the block's rows of the matrix stay in
+// shared memory for the whole solve instead of being re-read from L2 by every SpMV.  One
+// 80-byte chunk per (row, lane): 8 f64 values, then the 8 columns as int16 offsets from the
+// row (|c - i| <= 32767, checked by tt_csr_to_ell).  Consecutive lanes read consecutive
+// chunks, so each quarter-warp LDS.128 touches 8 distinct 16-byte bank groups.
+__device__ __forceinline__ double slab_row(const uint4* __restrict__ ch, int64_t i,
+                                           const double* __restrict__ z, const double* __restrict__ po,
+                                           double beta) {
+    const uint4 w0 = ch[0], w1 = ch[1], w2 = ch[2], w3 = ch[3], cw = ch[4];
+    const auto dlo = [](uint4 w) { return __hiloint2double((int)w.y, (int)w.x); };
+    const auto dhi = [](uint4 w) { return __hiloint2double((int)w.w, (int)w.z); };
+    const auto off = [](unsigned u, int h) { return (int)(short)(h ? (u >> 16) : (u & 0xffffu)); };
+    int c[8];
+    c[0] = (int)i + off(cw.x, 0); c[1] = (int)i + off(cw.x, 1);
+    c[2] = (int)i + off(cw.y, 0); c[3] = (int)i + off(cw.y, 1);
+    c[4] = (int)i + off(cw.z, 0); c[5] = (int)i + off(cw.z, 1);
+    c[6] = (int)i + off(cw.w, 0); c[7] = (int)i + off(cw.w, 1);
+    double x[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) x[t] = z[c[t]] + beta * po[c[t]];
+    const double s0 = fma(dhi(w1), x[3], fma(dlo(w1), x[2], fma(dhi(w0), x[1], dlo(w0) * x[0])));
+    const double s1 = fma(dhi(w3), x[7], fma(dlo(w3), x[6], fma(dhi(w2), x[5], dlo(w2) * x[4])));
+    return s0 + s1;
+}
+
+template <int BLOCK, int MINB, int LPR, bool CONTIG = false, bool SLAB = false>
 __global__ void __launch_bounds__(BLOCK, MINB) pcg_ell_kernel(EllArgs a) {
+    static_assert(!SLAB || (LPR == 2 && CONTIG), "the slab layout is 2 lanes per row, contiguous rows");
     cg::grid_group grid = cg::this_grid();
     __shared__ double sh[3 * 32];
+    extern __shared__ uint4 slab[];  // SLAB: (rows of this block) x 2 chunks x 5 uint4
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
     const int nb = gridDim.x;
@@ -642,6 +670,25 @@ __global__ void __launch_bounds__(BLOCK, MINB) pcg_ell_kernel(EllArgs a) {
     double* partB = a.part + nb;
     double* partC = a.part + 2 * nb;
     const int64_t n = a.n;
+    if constexpr (SLAB) {
+        const int64_t rpb = (n + nb - 1) / nb;
+        const int64_t lo = min(n, blockIdx.x * rpb), hi = min(n, lo + rpb);
+        for (int64_t q = threadIdx.x; q < (hi - lo) * 2; q += BLOCK) {
+            const int64_t i = lo + (q >> 1);
+            const int sub = (int)(q & 1);
+            const int4* cq = reinterpret_cast<const int4*>(a.ec + i * 16) + 2 * sub;
+            const int4 c0 = __ldg(cq), c1 = __ldg(cq + 1);
+            const uint4* vq = reinterpret_cast<const uint4*>(a.ev + i * 16 + 8 * sub);
+            uint4* ch = slab + q * 5;
+            ch[0] = __ldg(vq); ch[1] = __ldg(vq + 1); ch[2] = __ldg(vq + 2); ch[3] = __ldg(vq + 3);
+            const auto pk = [&](int u, int v) {
+                return (unsigned)(unsigned short)(short)(u - (int)i) |
+                       ((unsigned)(unsigned short)(short)(v - (int)i) << 16);
+            };
+            ch[4] = make_uint4(pk(c0.x, c0.y), pk(c0.z, c0.w), pk(c1.x, c1.y), pk(c1.z, c1.w));
+        }
+        // (the first grid.sync below orders these stores before any SpMV read)
+    }
     double bb = 0.0, rz_p = 0.0;
     for (int64_t i = tid; i < n; i += nthreads) {
         const double di = 1.0 / a.diag[i];
@@ -698,7 +745,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) pcg_ell_kernel(EllArgs a) {
                 const double* __restrict__ z = a.z;
                 const double* __restrict__ po = p_old;
                 const auto col = [&](int c) { return z[c] + beta * po[c]; };
-                if constexpr (LPR == 2) s = ell_row16_2(a.ec, a.ev, i, sub, col);
+                if constexpr (SLAB) s = slab_row(slab + ((i - blockIdx.x * rpb) * 2 + sub) * 5, i, z, po, beta);
+                else if constexpr (LPR == 2) s = ell_row16_2(a.ec, a.ev, i, sub, col);
                 else s = ell_row16(a.ec, a.ev, i, sub, col);
             }
 #pragma unroll
@@ -1016,6 +1064,47 @@ extern "C" int tt_pcg_ell(int64_t n, const int32_t* ell_cols, const double* ell_
     void* args[] = {&a};
     cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(512), args, 0, as_stream(stream));
     return cuda_status(e, "pcg_ell_kernel (cooperative launch)");
+}
+
+extern "C" int tt_pcg_ell_slab(int64_t n, const int32_t* ell_cols, const double* ell_vals, const double* diag,
+                               const double* b, double tol, int64_t maxiter, double* x, double* best_x,
+                               double* work, tt_pcg_result_t* result, void* stream) {
+    if (n < 1 || maxiter < 0) {
+        set_error("tt_pcg_ell_slab: bad size");
+        return TT_ERR_INVALID_PARAMETER;
+    }
+    EllArgs a;
+    a.n = n; a.ec = ell_cols; a.ev = ell_vals; a.diag = diag; a.b = b; a.tol = tol; a.maxiter = maxiter;
+    a.x = x; a.best_x = best_x;
+    a.r = work; a.z = work + n; a.p0 = work + 2 * n; a.p1 = work + 3 * n; a.ap = work + 4 * n;
+    a.dinv = work + 5 * n;
+    a.part = work + 6 * n;
+    a.res = result;
+    const void* fn = (const void*)pcg_ell_kernel<512, 2, 2, true, true>;
+    int dev = 0, max_optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const int sms = sm_count();
+    // 2 blocks per SM (the 2 x 512 shape of tt_pcg_ell), else 1 with twice the rows.  With
+    // 2 per SM the block count and row ranges are tt_pcg_ell's, so the partial sums -- and
+    // the iterates -- are bitwise the same
+    const int64_t need = (n * 2 + 511) / 512;
+    for (int bps = 2; bps >= 1; --bps) {
+        const int64_t nb = need < (int64_t)sms * bps ? need : (int64_t)sms * bps;
+        const int64_t rpb = (n + nb - 1) / nb;
+        const int64_t smem = rpb * 160;
+        if (smem + (int64_t)sizeof(double) * 96 > max_optin) continue;
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 512, (size_t)smem);
+        if (per_sm < bps) continue;
+        void* args[] = {&a};
+        cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)nb), dim3(512), args, (size_t)smem,
+                                                    as_stream(stream));
+        return cuda_status(e, "pcg_ell_kernel (slab, cooperative launch)");
+    }
+    set_error("tt_pcg_ell_slab: %lld rows do not fit in shared memory", (long long)n);
+    return TT_ERR_CAPACITY;
 }
 
 #ifdef TT_PCG_TRACE

@@ -662,11 +662,26 @@ __global__ void reduce_nodes_kernel(int64_t n_nodes, int k, const int64_t* __res
     int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (n >= n_nodes) return;
     double s = 0.0;
-    for (int64_t q = inc_start[n]; q < inc_start[n + 1]; ++q) {
-        int64_t ea = inc[q];
-        int64_t e = ea / k;
-        if (e < e_lo || e >= e_hi) continue;
-        s = add(s, contrib[(e - e_lo) * k + (ea - e * k)]);
+    const int64_t q1 = inc_start[n + 1];
+    // 8 incidences per trip: all index loads, then all (independent) contribution gathers,
+    // then the adds in ascending order -- the np.add.at order, with 8 gathers in flight
+    for (int64_t q = inc_start[n]; q < q1; q += 8) {
+        int64_t src[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            src[t] = -1;
+            if (q + t < q1) {
+                const int64_t ea = __ldg(inc + q + t);
+                const int64_t e = ea / k;
+                if (e >= e_lo && e < e_hi) src[t] = (e - e_lo) * k + (ea - e * k);
+            }
+        }
+        double v[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) v[t] = src[t] >= 0 ? __ldg(contrib + src[t]) : 0.0;
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+            if (src[t] >= 0) s = add(s, v[t]);
     }
     b[n] = s;
 }

@@ -171,8 +171,11 @@ class SparseSymMatrix:
                 _lib.call("tt_csr_to_ell", self.n, _lib.ptr(self.row_ptr_dev), _lib.ptr(self.cols_dev),
                           _lib.ptr(self.vals_dev), 16, _lib.ptr(ec), _lib.ptr(ev), _lib.ptr(dg),
                           _lib.ptr(st), _lib.stream_handle())
-                if int(st.item()) == 0:
+                flags = int(st.item())
+                if not flags & _lib.TT_FLAG_CAPACITY:
                     self._ell = (ec, ev, dg)
+                    # shared-memory slab PCG: columns within +-32767 rows of their row
+                    self._slab_ok = not flags & _lib.TT_FLAG_WIDE_ROWS
         return self._ell
 
     def workspace(self):
@@ -213,7 +216,8 @@ def assemble_mass_matrix(mesh, rule: QuadratureRule | None = None) -> SparseSymM
     return SparseSymMatrix(mesh.n_nodes, row_ptr, cols, vals)
 
 
-#: "ell" (default when every row has <= 16 entries) or "csr"
+#: "ell" (default when every row has <= 16 entries: the shared-memory slab PCG when the rows
+#: fit, else the L2-streaming ELL PCG), "ell_l2" (never the slab) or "csr"
 _PCG_PATH = __import__("os").environ.get("TT_PCG_PATH", "ell")
 
 
@@ -232,6 +236,13 @@ def pcg_device(M: SparseSymMatrix, b: torch.Tensor, tol: float = 1e-12,
     best_x = best_x if best_x is not None else torch.empty(n, dtype=torch.float64, device=b.device)
     ell = M.ell() if _PCG_PATH != "csr" else None
     if ell is not None:
+        args = (n, _lib.ptr(ell[0]), _lib.ptr(ell[1]), _lib.ptr(ell[2]), _lib.ptr(b), float(tol), maxiter,
+                _lib.ptr(x), _lib.ptr(best_x), _lib.ptr(work), _lib.ptr(res), _lib.stream_handle())
+        if _PCG_PATH == "ell" and getattr(M, "_slab_ok", False):
+            # rows held in shared memory when they fit (TT_ERR_CAPACITY: nothing launched)
+            if _lib.call_status("tt_pcg_ell_slab", *args) == 0:
+                return x, best_x, res
+            M._slab_ok = False
         _lib.call("tt_pcg_ell", n, _lib.ptr(ell[0]), _lib.ptr(ell[1]), _lib.ptr(ell[2]), _lib.ptr(b),
                   float(tol), maxiter, _lib.ptr(x), _lib.ptr(best_x), _lib.ptr(work), _lib.ptr(res),
                   _lib.stream_handle())

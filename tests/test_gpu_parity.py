@@ -470,14 +470,60 @@ def test_ell_and_csr_pcg_agree(tt, golden, c1):
     assert M.ell() is not None
     b = torch.as_tensor(golden["b_c1_mesh_smooth"], device="cuda")
     xs = []
-    for path in ("ell", "csr"):
+    for path in ("ell", "ell_l2", "csr"):
         fem._PCG_PATH = path
         try:
             xs.append(tt.cg_solve(M, b, tol=1e-14).cpu().numpy())
         finally:
             fem._PCG_PATH = "ell"
+    assert M._slab_ok          # the default ran the shared-memory slab PCG
+    assert np.array_equal(xs[0], xs[1])   # slab and L2 ELL: the same arithmetic, bit for bit
     for x in xs:
         assert np.max(np.abs(x - golden["x_c1_mesh_tol14"])) <= 1e-12
+
+
+@pytest.mark.parametrize("n", [20, 60])
+def test_slab_pcg_3d_and_capacity_fallback(tt, n):
+    """3-D mass matrices: the slab PCG (n=20: 9,261 rows) is bitwise the L2 ELL PCG; at
+    n=60 (226,981 rows, more than fit in 148 SMs' shared memory) tt_pcg_ell_slab reports
+    TT_ERR_CAPACITY without launching and the L2 ELL PCG runs instead."""
+    import torch
+    from paper_2603_00538_b200 import fem
+    tgt = tt.generate_cube_mesh(n, 0.2, seed=20, split="kuhn")
+    M = tt.assemble_mass_matrix(tgt)
+    b = torch.as_tensor(np.random.default_rng(n).random(tgt.n_nodes), device="cuda")
+    xs = []
+    for path in ("ell", "ell_l2"):
+        fem._PCG_PATH = path
+        try:
+            xs.append(tt.cg_solve(M, b, tol=1e-14).cpu().numpy())
+        finally:
+            fem._PCG_PATH = "ell"
+    assert M._slab_ok == (n == 20)
+    assert np.array_equal(xs[0], xs[1])
+    xr, _ = O.cg_solve(M.csr, b.cpu().numpy(), tol=1e-14)
+    assert _rel(xs[0], xr) <= 1e-12
+
+
+def test_slab_pcg_wide_rows_not_used(tt):
+    """A column more than 32767 rows from its row (int16 slab offsets cannot hold it):
+    tt_csr_to_ell flags TT_FLAG_WIDE_ROWS and the solve takes the L2 ELL PCG."""
+    import scipy.sparse as sp
+    import torch
+    n = 40000
+    A = sp.diags([np.full(n, 4.0), np.full(n - 1, -1.0), np.full(n - 1, -1.0)], [0, 1, -1]).tolil()
+    A[0, n - 1] = A[n - 1, 0] = -0.5
+    A = A.tocsr()
+    A.sort_indices()
+    dev = torch.device("cuda")
+    M = tt.SparseSymMatrix(n, torch.as_tensor(A.indptr.astype(np.int64), device=dev),
+                           torch.as_tensor(A.indices.astype(np.int32), device=dev),
+                           torch.as_tensor(A.data, device=dev))
+    b = np.random.default_rng(1).random(n)
+    x = tt.cg_solve(M, b, tol=1e-14)
+    assert M.ell() is not None and not M._slab_ok
+    xr, _ = O.cg_solve(A, b, tol=1e-14)
+    assert _rel(x, xr) <= 1e-12
 
 
 def test_mc_operator_folded_load_matrix(tt, golden, c1):
@@ -556,7 +602,7 @@ def test_ell_pcg_spmv_shapes_agree(tt, golden, c1, shape):
     assert json.loads(out.stdout.strip().splitlines()[-1]) <= 1e-12
 
 
-@pytest.mark.parametrize("path", ["ell", "csr"])
+@pytest.mark.parametrize("path", ["ell", "ell_l2", "csr"])
 def test_pcg_best_iterate_matches_oracle(tt, path):
     """NoConvergence carries the best iterate (fem.py:141-152).  An SPD matrix whose
     preconditioned residual is NOT monotone (increases at iterations 2, 6, 8, 10) drives
