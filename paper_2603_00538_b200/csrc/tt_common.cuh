@@ -370,4 +370,24 @@ __device__ __noinline__ SnapOut<D> snap_point(const GridDev g, double x0, double
     return o;
 }
 
+// Out-of-line exact localisation for the fused kernels' rare paths: the double-precision
+// certified walk from `guess` (the element whose compact float test was inside its
+// uncertainty band -- nearly always certified here in one step) and the reference cell scan
+// when that is uncertain too, or directly the scan when guess < 0.  Out of line so the
+// single diverged lane costs the hot loop no registers.
+template <int D>
+struct LocOut {
+    int e;
+    double l[D + 1];
+};
+
+template <int D>
+__device__ __noinline__ LocOut<D> locate_from(const GridDev g, int guess, double x0, double x1, double x2,
+                                              double eps) {
+    const double x[3] = {x0, x1, x2};
+    LocOut<D> o;
+    o.e = guess >= 0 ? locate_walk<D>(g, x, eps, guess, o.l) : locate_point<D>(g, x, eps, o.l);
+    return o;
+}
+
 }  // namespace tt

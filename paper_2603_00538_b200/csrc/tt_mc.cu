@@ -408,6 +408,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) mc_mesh_kernel(TargetDev t, int64
             if (!busy) continue;
             double l[K];
             int hit = -1;
+            int fb = -1;  // FW: element whose float test fell in its uncertainty band
             bool done = false;
             bool fw_hit = false;
             double fw_f = 0.0;
@@ -459,7 +460,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) mc_mesh_kernel(TargetDev t, int64
                         for (int c = 0; c < D; ++c) f = fma(gv[c], r[c], f);
                         fw_f = f;
                     } else if (lmin > -w.tau) {
-                        cur = -1;  // within the uncertainty band of a facet: exact scan
+                        fb = cur;  // within the uncertainty band of a facet: exact double walk
+                        cur = -1;
                     } else {
                         int nb = w.nbr[0];
 #pragma unroll
@@ -521,7 +523,14 @@ __global__ void __launch_bounds__(BLOCK, MINB) mc_mesh_kernel(TargetDev t, int64
                         map_point<D>(lam, v, x);
                     }
                 }
-                hit = locate_point<D>(g, x, EPS, l);
+                if constexpr (FW) {
+                    // double certified walk from the band element (then the reference scan),
+                    // out of line: one diverged lane, ~1 dependent record load instead of
+                    // the ~14-candidate scan chain
+                    hit = fb >= 0 ? locate_walk<D>(g, x, EPS, fb, l) : locate_point<D>(g, x, EPS, l);
+                } else {
+                    hit = locate_point<D>(g, x, EPS, l);
+                }
                 if (hit < 0) {
                     if (src.outside == TT_OUTSIDE_STRICT) {
                         flags |= TT_FLAG_OUTSIDE_STRICT;
