@@ -125,7 +125,7 @@ int main(int argc, char** argv) {
     G.walk = 1;
     G.wrec = wrec;
     int32_t* seeds;
-    CU(cudaMalloc((void**)&seeds, 4 * 4 * tne));
+    CU(cudaMalloc((void**)&seeds, sizeof(int32_t) * TT_SEED_ANCHORS * tne));
     CK(tt_seed_elements(&G, &T, 0, tne, seeds, st));
 
     /* plan: Sobol(N, skip 0) -> barycentric (SamplePlan.build(N, "sobol", 0)) */

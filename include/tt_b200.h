@@ -160,8 +160,8 @@ typedef struct tt_source {
     const double*  coeffs;    /* TT_SRC_MESH (n_s,) nodal coefficients */
     const double*  values;    /* TT_SRC_VALUES (e_hi - e_lo, N) */
     const int32_t* cached_ids;/* TT_SRC_CACHED (e_hi - e_lo, N) source element per sample */
-    const int32_t* seeds;     /* TT_SRC_MESH optional (E_target, dim+2) walk start elements
-                                 per target element (tt_seed_elements), or NULL */
+    const int32_t* seeds;     /* TT_SRC_MESH optional (E_target, TT_SEED_ANCHORS) walk start
+                                 elements per target element (tt_seed_elements), or NULL */
     const double*  elem_coeffs;/* TT_SRC_MESH/CACHED optional (E_s, 4) per-element vertex
                                  coefficients (tt_pack_coeffs); replaces src_elems+coeffs */
     const double*  elem_grad;  /* TT_SRC_MESH optional (E_s, 4): gradient g (dim) and the value at
@@ -217,9 +217,11 @@ int tt_locate_many(const double* points, int64_t count, int nx, int ny,
 int tt_grid_walk_prep(const tt_mesh_t* mesh, const int64_t* inc_start, const int32_t* inc,
                       double eps, double* rec, double* wrec /* or NULL */, int32_t* status,
                       void* stream);
-/* seeds[(e - e_lo)*(dim+2) + s] = source element containing, for s = 0, the target
- * element's centroid c and, for s = 1 + i, the point (v_i + c)/2 (reference scan, snapped
- * when outside): walk starts for the element's samples (nearest by max barycentric). */
+/* seeds[(e - e_lo)*TT_SEED_ANCHORS + s] = source element containing anchor point s of the
+ * target element (reference scan, snapped when outside): s = 0 the centroid c, s = 1 + i the
+ * point (v_i + c)/2, then 16 - (dim+2) k-means anchors (scripts/seed_anchors.py).  Walk
+ * starts: a sample starts at its nearest anchor's element. */
+#define TT_SEED_ANCHORS 16
 int tt_seed_elements(const tt_grid_t* grid, const tt_mesh_t* target, int64_t e_lo,
                      int64_t e_hi, int32_t* seeds, void* stream);
 int tt_nearest(const tt_grid_t* grid, const double* points, int64_t count,
@@ -240,7 +242,7 @@ int tt_mc_load(const tt_mesh_t* target, int64_t e_lo, int64_t e_hi, const tt_pla
                int32_t* status, void* stream);
 
 int tt_mc_cache_ids(const tt_mesh_t* target, int64_t e_lo, int64_t e_hi, const tt_plan_t* plan,
-                    const tt_grid_t* grid, const int32_t* seeds /* (E_target, dim+2) or NULL */,
+                    const tt_grid_t* grid, const int32_t* seeds /* (E_target, TT_SEED_ANCHORS) or NULL */,
                     int32_t* ids /* (e_hi-e_lo, N): located or snapped */, void* stream);
 
 /* out[e*4 + i] = coeffs[elems[e*k + i]] (i < k, zero padded): one aligned 32-byte record

@@ -23,6 +23,7 @@ TT_OK, TT_ERR_INVALID_PARAMETER, TT_ERR_DIMENSION_MISMATCH, TT_ERR_CUDA, TT_ERR_
 TT_FLAG_NONFINITE, TT_FLAG_OUTSIDE_STRICT, TT_FLAG_CAPACITY, TT_FLAG_INVALID_DENSITY = 1, 2, 4, 8
 TT_FLAG_NONMANIFOLD = 16
 TT_FLAG_WIDE_ROWS = 32
+TT_SEED_ANCHORS = 16
 TT_PLAN_SHARED, TT_PLAN_PHILOX = 0, 1
 TT_SRC_EXPR, TT_SRC_MESH, TT_SRC_VALUES, TT_SRC_CACHED = 0, 1, 2, 3
 TT_OUTSIDE_SNAP, TT_OUTSIDE_STRICT = 0, 1

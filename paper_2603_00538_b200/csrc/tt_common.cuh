@@ -370,6 +370,51 @@ __device__ __noinline__ SnapOut<D> snap_point(const GridDev g, double x0, double
     return o;
 }
 
+// Walk-seed anchors in barycentric coordinates (scripts/seed_anchors.py): the first k+1
+// are the centroid and the corner points (v_i + c)/2, the rest k-means centres of the
+// uniform simplex with those fixed.  A target element keeps the source element of each
+// anchor (tt_seed_elements); a sample starts its walk at its nearest anchor's element.
+constexpr int kSeeds = TT_SEED_ANCHORS;
+static __constant__ double kAnchor2[16][3] = {
+    {0.333333, 0.333333, 0.333333},
+    {0.666667, 0.166667, 0.166667},
+    {0.166667, 0.666667, 0.166667},
+    {0.166667, 0.166667, 0.666667},
+    {0.363773, 0.564304, 0.071923},
+    {0.106860, 0.449307, 0.443833},
+    {0.085589, 0.834295, 0.080116},
+    {0.070230, 0.624320, 0.305449},
+    {0.531959, 0.357019, 0.111022},
+    {0.532957, 0.113448, 0.353596},
+    {0.083635, 0.082097, 0.834268},
+    {0.367931, 0.073020, 0.559049},
+    {0.069731, 0.308081, 0.622189},
+    {0.268066, 0.246854, 0.485080},
+    {0.274587, 0.482372, 0.243041},
+    {0.832589, 0.083788, 0.083623},
+};
+static __constant__ double kAnchor3[16][4] = {
+    {0.250000, 0.250000, 0.250000, 0.250000},
+    {0.625000, 0.125000, 0.125000, 0.125000},
+    {0.125000, 0.625000, 0.125000, 0.125000},
+    {0.125000, 0.125000, 0.625000, 0.125000},
+    {0.125000, 0.125000, 0.125000, 0.625000},
+    {0.774629, 0.074457, 0.075479, 0.075435},
+    {0.465274, 0.310278, 0.118290, 0.106158},
+    {0.109478, 0.385985, 0.392791, 0.111746},
+    {0.129884, 0.111950, 0.465907, 0.292258},
+    {0.103289, 0.395581, 0.111945, 0.389184},
+    {0.293299, 0.465529, 0.115429, 0.125743},
+    {0.391758, 0.113144, 0.393580, 0.101518},
+    {0.302490, 0.126738, 0.106420, 0.464352},
+    {0.074152, 0.074355, 0.075047, 0.776447},
+    {0.466578, 0.101469, 0.125798, 0.306155},
+    {0.101515, 0.122250, 0.313852, 0.462382},
+};
+
+template <int D>
+TT_D double anchor(int m, int a) { return D == 2 ? kAnchor2[m][a] : kAnchor3[m][a]; }
+
 // Out-of-line exact localisation for the fused kernels' rare paths: the double-precision
 // certified walk from `guess` (the element whose compact float test was inside its
 // uncertainty band -- nearly always certified here in one step) and the reference cell scan

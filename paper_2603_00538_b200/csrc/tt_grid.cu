@@ -410,25 +410,23 @@ __global__ void walk_prep_kernel(int64_t E, const double* __restrict__ nodes,
     }
 }
 
-// Walk seeds per target element: the source elements containing its centroid and the
-// k "corner" points (v_i + centroid) / 2 (reference scan; snapped when outside).
-// Layout (E, k + 1): [centroid, corner_0, ..., corner_d].
+// Walk seeds per target element: the source elements containing its kSeeds anchor points
+// (x = sum_a A[s][a] v_a; reference scan, snapped when outside).  Layout (E, kSeeds).
 template <int D>
 __global__ void seed_kernel(GridDev g, const double* __restrict__ nodes,
                             const int32_t* __restrict__ elems, int64_t e_lo, int64_t n_el,
                             int32_t* __restrict__ seeds) {
     constexpr int K = D + 1;
     int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (t >= n_el * (K + 1)) return;
-    const int64_t i = t / (K + 1);
-    const int which = (int)(t % (K + 1));
+    if (t >= n_el * kSeeds) return;
+    const int64_t i = t / kSeeds;
+    const int which = (int)(t % kSeeds);
     const int64_t e = e_lo + i;
     double x[D];
     for (int c = 0; c < D; ++c) {
-        double s = add(nodes[(int64_t)elems[e * K] * D + c], nodes[(int64_t)elems[e * K + 1] * D + c]);
-        for (int a = 2; a < K; ++a) s = add(s, nodes[(int64_t)elems[e * K + a] * D + c]);
-        x[c] = div(s, (double)K);
-        if (which > 0) x[c] = mul(0.5, add(x[c], nodes[(int64_t)elems[e * K + which - 1] * D + c]));
+        double s = mul(anchor<D>(which, 0), nodes[(int64_t)elems[e * K] * D + c]);
+        for (int a = 1; a < K; ++a) s = add(s, mul(anchor<D>(which, a), nodes[(int64_t)elems[e * K + a] * D + c]));
+        x[c] = s;
     }
     double l[D + 1];
     int es = locate_point<D>(g, x, 1e-12, l);
@@ -651,8 +649,8 @@ extern "C" int tt_seed_elements(const tt_grid_t* g, const tt_mesh_t* t, int64_t 
     GridDev gd = to_dev(*g);
     auto s = as_stream(stream);
     if (g->dim == 2)
-        seed_kernel<2><<<grid_for((e_hi - e_lo) * 4, 128), 128, 0, s>>>(gd, t->nodes, t->elems, e_lo, e_hi - e_lo, seeds);
+        seed_kernel<2><<<grid_for((e_hi - e_lo) * kSeeds, 128), 128, 0, s>>>(gd, t->nodes, t->elems, e_lo, e_hi - e_lo, seeds);
     else
-        seed_kernel<3><<<grid_for((e_hi - e_lo) * 5, 128), 128, 0, s>>>(gd, t->nodes, t->elems, e_lo, e_hi - e_lo, seeds);
+        seed_kernel<3><<<grid_for((e_hi - e_lo) * kSeeds, 128), 128, 0, s>>>(gd, t->nodes, t->elems, e_lo, e_hi - e_lo, seeds);
     return launch_check("seed_kernel");
 }

@@ -126,13 +126,14 @@ class UniformGridLocator:
         return g
 
     def seeds_for(self, target) -> torch.Tensor:
-        """Walk starts per target element (E, d+2): source elements containing the
-        centroid c and the points (v_i + c)/2 (cached per target; meshes are immutable)."""
+        """Walk starts per target element (E, 16): source elements containing the
+        element's 16 anchor points -- centroid c, the points (v_i + c)/2, k-means anchors
+        (tt_seed_elements; cached per target, meshes are immutable)."""
         key = id(target)
         hit = self._seeds.get(key)
         if hit is not None and hit[0] is target:
             return hit[1]
-        seeds = torch.empty((target.n_elems, target.DIM + 2), dtype=torch.int32,
+        seeds = torch.empty((target.n_elems, _lib.TT_SEED_ANCHORS), dtype=torch.int32,
                             device=self.cell_start_dev.device)
         g, t = self.desc(), target.device.desc()
         _lib.call("tt_seed_elements", C.byref(g), C.byref(t), 0, target.n_elems, _lib.ptr(seeds),
