@@ -58,9 +58,12 @@ class DistributedCoupling:
         return reduce_load(b, self.group)
 
     def step(self, source, plan, tol: float = 1e-12):
-        from .fem import cg_solve
-        b = self.load(source, plan)
-        return cg_solve(self.target.device.mass, b, tol=tol)
+        from . import _lib
+        from .fem import finish_solve, pcg_device
+        status = _lib.status_word()
+        b = self.load(source, plan, check=False, status=status)
+        x, best_x, res = pcg_device(self.target.device.mass, b, tol=tol)
+        return finish_solve(x, best_x, res, False, status)   # one sync: load status + solve
 
 
 def reduce_nodes_peers(target, contrib_ptrs: torch.Tensor, range_lo: torch.Tensor,

@@ -253,13 +253,31 @@ def pcg_device(M: SparseSymMatrix, b: torch.Tensor, tol: float = 1e-12,
     return x, best_x, res
 
 
-def decode_result(res: torch.Tensor) -> PcgResult:
-    raw = res.cpu().numpy().tobytes()
+_HOST_RES = {}
+
+
+def decode_result(res: torch.Tensor, status: torch.Tensor | None = None):
+    """PcgResult of a launched solve; with ``status``, (PcgResult, status flags) read with
+    one synchronisation (both copied into a pinned host buffer)."""
+    if status is None:
+        raw = res.cpu().numpy().tobytes()
+    else:
+        dev = res.device
+        host = _HOST_RES.get(dev)
+        if host is None:
+            host = _HOST_RES[dev] = torch.empty(res.numel() * 8 + 8, dtype=torch.uint8).pin_memory()
+        nb = res.numel() * 8
+        host[:nb].copy_(res.view(torch.uint8), non_blocking=True)
+        host[nb:nb + 4].copy_(status.view(torch.uint8), non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+        raw = host.numpy().tobytes()
     r = _lib.tt_pcg_result_t.from_buffer_copy(raw[:C.sizeof(_lib.tt_pcg_result_t)])
     out = PcgResult()
     for f in PcgResult.__slots__:
         setattr(out, f, getattr(r, f))
-    return out
+    if status is None:
+        return out
+    return out, int(np.frombuffer(raw[res.numel() * 8:res.numel() * 8 + 4], dtype=np.int32)[0])
 
 
 def cg_solve(M: SparseSymMatrix, b, tol: float = 1e-12, maxiter: int | None = None):
@@ -272,9 +290,20 @@ def cg_solve(M: SparseSymMatrix, b, tol: float = 1e-12, maxiter: int | None = No
     if bd.shape != (M.n,):
         raise DimensionMismatch(f"rhs length {tuple(bd.shape)} for {M.n}x{M.n} matrix")
     x, best_x, res = pcg_device(M, bd, tol, maxiter)
-    r = decode_result(res)
+    return finish_solve(x, best_x, res, was_np)
+
+
+def finish_solve(x, best_x, res, was_np: bool = False, status: torch.Tensor | None = None):
+    """The host side of a launched PCG: ONE synchronisation reads the solver result (and,
+    when given, the status word of the load launched before it), then the reference's
+    outcomes -- the load's SourceEvalFailed/InvalidDensity first, b = 0 -> zeros,
+    NoConvergence(best_x) (fem.py:141-152)."""
+    r, flags = decode_result(res, status) if status is not None else (decode_result(res), 0)
+    if flags:
+        from .montecarlo import _raise_status
+        _raise_status(flags)
     if r.zero_rhs:
-        x = torch.zeros_like(bd)
+        x = torch.zeros_like(x)
     if not r.converged:
         bx = best_x.cpu().numpy() if was_np else best_x
         raise NoConvergence(bx, float(r.best_residual), int(r.iterations))

@@ -18,7 +18,7 @@ import torch
 
 from . import _lib
 from .errors import DimensionMismatch
-from .fem import NodalField, cg_solve
+from .fem import NodalField, finish_solve, pcg_device
 from .locate import UniformGridLocator
 from .montecarlo import SamplePlan, _raise_status, load_vector
 
@@ -26,9 +26,12 @@ from .montecarlo import SamplePlan, _raise_status, load_vector
 def transfer_mc(target, source, plan: SamplePlan, cg_tol: float = 1e-12, workers: int = 1,
                 *, deterministic: bool = True) -> NodalField:
     """One-shot stochastic transfer from a black-box pointwise source (transfer.py:158-163)."""
-    b = load_vector(target, source, plan, deterministic=deterministic)
-    mass = target.device.mass
-    return NodalField(target, cg_solve(mass, b, tol=cg_tol))
+    # load and solve are launched back to back; one synchronisation at the end reads the
+    # load's status word and the solver result together (errors raised as the reference)
+    status = _lib.status_word()
+    b = load_vector(target, source, plan, deterministic=deterministic, check=False, status=status)
+    x, best_x, res = pcg_device(target.device.mass, b, tol=cg_tol)
+    return NodalField(target, finish_solve(x, best_x, res, False, status))
 
 
 class MCTransferOperator:
@@ -87,7 +90,8 @@ class MCTransferOperator:
     def _src_elem(self):
         return self.src_elem_dev.cpu().numpy()
 
-    def load(self, source_field: NodalField, check: bool = True) -> torch.Tensor:
+    def load(self, source_field: NodalField, check: bool = True,
+             status: torch.Tensor | None = None) -> torch.Tensor:
         """b = R c on the device (folded R: one SpMV; else the cached source elements)."""
         if source_field.mesh is not self.source_mesh and \
                 source_field.mesh.n_nodes != self.source_mesh.n_nodes:
@@ -109,7 +113,7 @@ class MCTransferOperator:
         s.cached_ids = _lib.ptr(self.src_elem_dev).value
         s.elem_coeffs = _lib.ptr(source_field.elem_coeffs()).value
         contrib = torch.empty((self.target.n_elems, k), dtype=torch.float64, device=dm.nodes.device)
-        status = _lib.status_word()
+        status = status if status is not None else _lib.status_word()
         mdesc, pdesc = dm.desc(), self.plan.desc()
         _lib.call("tt_mc_load", C.byref(mdesc), 0, self.target.n_elems, C.byref(pdesc), C.byref(s),
                   _lib.ptr(contrib), None, _lib.ptr(status), _lib.stream_handle())
@@ -120,10 +124,14 @@ class MCTransferOperator:
 
     def apply(self, source_field: NodalField) -> NodalField:
         """Transfer a nodal field on the source mesh (precomputed localisation)."""
-        b = self.load(source_field)
-        return NodalField(self.target, cg_solve(self.mass, b, tol=self.cg_tol))
+        status = _lib.status_word()
+        b = self.load(source_field, check=False, status=status)
+        x, best_x, res = pcg_device(self.mass, b, tol=self.cg_tol)
+        return NodalField(self.target, finish_solve(x, best_x, res, False, status))
 
     def apply_sampled(self, source) -> NodalField:
         """Transfer from a pointwise black box, re-querying every sample."""
-        b = load_vector(self.target, source, self.plan)
-        return NodalField(self.target, cg_solve(self.mass, b, tol=self.cg_tol))
+        status = _lib.status_word()
+        b = load_vector(self.target, source, self.plan, check=False, status=status)
+        x, best_x, res = pcg_device(self.mass, b, tol=self.cg_tol)
+        return NodalField(self.target, finish_solve(x, best_x, res, False, status))
