@@ -299,24 +299,28 @@ int tt_pcg(int64_t n, const int64_t* row_ptr, const int32_t* cols, const double*
            const double* b, double tol, int64_t maxiter, double* x, double* best_x,
            double* work /* tt_pcg_workspace_doubles(n) */, tt_pcg_result_t* result /* device */,
            void* stream);
-/* ELL form of the mass matrix (width 16, padding (row, 0.0)) and the PCG over it; the
- * same recurrence as tt_pcg with the row-pointer round trip removed from every SpMV row.
- * TT_FLAG_CAPACITY in *status when a row has more than 16 entries (use tt_pcg then). */
+/* ELL form of the mass matrix (width 16, or 8 when every row has <= 8 entries -- the 2-D
+ * meshes; padding (row, 0.0)) and the PCG over it; the same recurrence as tt_pcg with the
+ * row-pointer round trip removed from every SpMV row.  TT_FLAG_CAPACITY in *status when a
+ * row has more than `width` entries (use tt_pcg then); TT_FLAG_WIDE_ROWS when a column is
+ * more than 32767 rows from its row (no slab). */
 int tt_csr_to_ell(int64_t n, const int64_t* row_ptr, const int32_t* cols, const double* vals,
-                  int width, int32_t* ell_cols /* (n, 16) */, double* ell_vals /* (n, 16) */,
+                  int width, int32_t* ell_cols /* (n, width) */, double* ell_vals /* (n, width) */,
                   double* diag /* (n,) */, int32_t* status, void* stream);
-int tt_pcg_ell(int64_t n, const int32_t* ell_cols, const double* ell_vals, const double* diag,
+int tt_pcg_ell(int64_t n, int width, const int32_t* ell_cols, const double* ell_vals, const double* diag,
                const double* b, double tol, int64_t maxiter, double* x, double* best_x,
                double* work /* tt_pcg_workspace_doubles(n) */, tt_pcg_result_t* result,
                void* stream);
-/* The same PCG with each block's rows of the ELL matrix held in shared memory for the
- * whole solve (160 B per row; fits when n <= ~1400 rows per SM).  Precondition: tt_csr_to_ell
- * did not set TT_FLAG_WIDE_ROWS.  Returns TT_ERR_CAPACITY, launching nothing, when the rows
- * do not fit (the caller then uses tt_pcg_ell). */
-int tt_pcg_ell_slab(int64_t n, const int32_t* ell_cols, const double* ell_vals, const double* diag,
-                    const double* b, double tol, int64_t maxiter, double* x, double* best_x,
-                    double* work /* tt_pcg_workspace_doubles(n) */, tt_pcg_result_t* result,
-                    void* stream);
+/* The same PCG with each block's rows of the ELL matrix held in shared memory for the whole
+ * solve (80 B per row per 8 columns): all of them when they fit (n up to ~207k rows at width
+ * 16, ~415k at width 8), else the first part of every block's range (at least 1/4 of it;
+ * TT_PCG_SLAB_MIN_FRAC) with the rest streamed from L2/HBM.  Precondition: tt_csr_to_ell did
+ * not set TT_FLAG_WIDE_ROWS.  Returns TT_ERR_CAPACITY, launching nothing, when too few rows
+ * fit (the caller then uses tt_pcg_ell). */
+int tt_pcg_ell_slab(int64_t n, int width, const int32_t* ell_cols, const double* ell_vals,
+                    const double* diag, const double* b, double tol, int64_t maxiter, double* x,
+                    double* best_x, double* work /* tt_pcg_workspace_doubles(n) */,
+                    tt_pcg_result_t* result, void* stream);
 int tt_spmv(int64_t n, const int64_t* row_ptr, const int32_t* cols, const double* vals,
             const double* x, double* y, void* stream);
 

@@ -125,8 +125,8 @@ _SIGNATURES = {
     "tt_pcg_workspace_doubles": ([_I64], _I64),
     "tt_pcg": ([_I64, _P, _P, _P, _P, _D, _I64, _P, _P, _P, _P, _P], _I),
     "tt_csr_to_ell": ([_I64, _P, _P, _P, _I, _P, _P, _P, _P, _P], _I),
-    "tt_pcg_ell": ([_I64, _P, _P, _P, _P, _D, _I64, _P, _P, _P, _P, _P], _I),
-    "tt_pcg_ell_slab": ([_I64, _P, _P, _P, _P, _D, _I64, _P, _P, _P, _P, _P], _I),
+    "tt_pcg_ell": ([_I64, _I, _P, _P, _P, _P, _D, _I64, _P, _P, _P, _P, _P], _I),
+    "tt_pcg_ell_slab": ([_I64, _I, _P, _P, _P, _P, _D, _I64, _P, _P, _P, _P, _P], _I),
     "tt_spmv": ([_I64, _P, _P, _P, _P, _P, _P], _I),
     "tt_integrate_p1": ([C.POINTER(tt_mesh_t), _P, _P, _P], _I),
     "tt_fp64_peak_probe": ([_I64, _P, C.POINTER(_I), C.POINTER(_I), _P], _I),

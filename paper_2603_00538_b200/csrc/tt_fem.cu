@@ -604,6 +604,7 @@ struct EllArgs {
     double* dinv;
     double* part;
     tt_pcg_result_t* res;
+    int64_t slab_rows;  // SLAB: rows per block held in shared memory (the rest read from L2)
 };
 
 template <class Col>
@@ -616,14 +617,15 @@ __device__ __forceinline__ double ell_row16(const int32_t* __restrict__ ec, cons
     return fma(a1.y, x3, fma(a1.x, x2, fma(a0.y, x1, a0.x * x0)));
 }
 
-// 2 lanes per row: lane `sub` owns entries [8 sub, 8 sub + 8) -> 16 independent gathers in
-// flight per lane and half the rows-per-group dependency chain of the 4-lane layout
-template <class Col>
-__device__ __forceinline__ double ell_row16_2(const int32_t* __restrict__ ec, const double* __restrict__ ev,
-                                             int64_t i, int sub, Col col) {
-    const int4* cq = reinterpret_cast<const int4*>(ec + i * 16) + 2 * sub;
+// W/8 lanes per row (W = 16: 2 lanes; W = 8, the 2-D matrices: 1 lane): lane `sub` owns
+// entries [8 sub, 8 sub + 8) -> 16 independent gathers in flight per lane and half the
+// rows-per-group dependency chain of the 4-lane layout
+template <int W, class Col>
+__device__ __forceinline__ double ell_row8(const int32_t* __restrict__ ec, const double* __restrict__ ev,
+                                           int64_t i, int sub, Col col) {
+    const int4* cq = reinterpret_cast<const int4*>(ec + i * W) + 2 * sub;
     const int4 c0 = __ldg(cq), c1 = __ldg(cq + 1);
-    const double2* vq = reinterpret_cast<const double2*>(ev + i * 16 + 8 * sub);
+    const double2* vq = reinterpret_cast<const double2*>(ev + i * W + 8 * sub);
     const double2 a0 = __ldg(vq), a1 = __ldg(vq + 1), a2 = __ldg(vq + 2), a3 = __ldg(vq + 3);
     const double x0 = col(c0.x), x1 = col(c0.y), x2 = col(c0.z), x3 = col(c0.w);
     const double x4 = col(c1.x), x5 = col(c1.y), x6 = col(c1.z), x7 = col(c1.w);
@@ -632,11 +634,12 @@ __device__ __forceinline__ double ell_row16_2(const int32_t* __restrict__ ec, co
     return s0 + s1;
 }
 
-// SLAB (2 lanes per row, contiguous row ranges): the block's rows of the matrix stay in
-// shared memory for the whole solve instead of being re-read from L2 by every SpMV.  One
-// 80-byte chunk per (row, lane): 8 f64 values, then the 8 columns as int16 offsets from the
-// row (|c - i| <= 32767, checked by tt_csr_to_ell).  Consecutive lanes read consecutive
-// chunks, so each quarter-warp LDS.128 touches 8 distinct 16-byte bank groups.
+// SLAB (W/8 lanes per row, contiguous row ranges): the block's rows of the matrix -- all of
+// them, or the first a.slab_rows when they do not fit -- stay in shared memory for the whole
+// solve instead of being re-read from L2/HBM by every SpMV.  One 80-byte chunk per (row,
+// lane): 8 f64 values, then the 8 columns as int16 offsets from the row (|c - i| <= 32767,
+// checked by tt_csr_to_ell).  Consecutive lanes read consecutive chunks (stride 5 x 16 B),
+// so each quarter-warp LDS.128 touches 8 distinct 16-byte bank groups.
 __device__ __forceinline__ double slab_row(const uint4* __restrict__ ch, int64_t i,
                                            const double* __restrict__ z, const double* __restrict__ po,
                                            double beta) {
@@ -657,9 +660,10 @@ __device__ __forceinline__ double slab_row(const uint4* __restrict__ ch, int64_t
     return s0 + s1;
 }
 
-template <int BLOCK, int MINB, int LPR, bool CONTIG = false, bool SLAB = false>
+template <int BLOCK, int MINB, int LPR, bool CONTIG = false, bool SLAB = false, int W = 16>
 __global__ void __launch_bounds__(BLOCK, MINB) pcg_ell_kernel(EllArgs a) {
-    static_assert(!SLAB || (LPR == 2 && CONTIG), "the slab layout is 2 lanes per row, contiguous rows");
+    static_assert(!SLAB || (LPR == W / 8 && CONTIG), "the slab layout is W/8 lanes per row, contiguous rows");
+    static_assert(LPR == W / 8 || (W == 16 && LPR == 4), "lanes per row");
     cg::grid_group grid = cg::this_grid();
     __shared__ double sh[3 * 32];
     extern __shared__ uint4 slab[];  // SLAB: (rows of this block) x 2 chunks x 5 uint4
@@ -672,13 +676,13 @@ __global__ void __launch_bounds__(BLOCK, MINB) pcg_ell_kernel(EllArgs a) {
     const int64_t n = a.n;
     if constexpr (SLAB) {
         const int64_t rpb = (n + nb - 1) / nb;
-        const int64_t lo = min(n, blockIdx.x * rpb), hi = min(n, lo + rpb);
-        for (int64_t q = threadIdx.x; q < (hi - lo) * 2; q += BLOCK) {
-            const int64_t i = lo + (q >> 1);
-            const int sub = (int)(q & 1);
-            const int4* cq = reinterpret_cast<const int4*>(a.ec + i * 16) + 2 * sub;
+        const int64_t lo = min(n, blockIdx.x * rpb), hi = min(n, lo + min(rpb, a.slab_rows));
+        for (int64_t q = threadIdx.x; q < (hi - lo) * LPR; q += BLOCK) {
+            const int64_t i = lo + q / LPR;
+            const int sub = (int)(q % LPR);
+            const int4* cq = reinterpret_cast<const int4*>(a.ec + i * W) + 2 * sub;
             const int4 c0 = __ldg(cq), c1 = __ldg(cq + 1);
-            const uint4* vq = reinterpret_cast<const uint4*>(a.ev + i * 16 + 8 * sub);
+            const uint4* vq = reinterpret_cast<const uint4*>(a.ev + i * W + 8 * sub);
             uint4* ch = slab + q * 5;
             ch[0] = __ldg(vq); ch[1] = __ldg(vq + 1); ch[2] = __ldg(vq + 2); ch[3] = __ldg(vq + 3);
             const auto pk = [&](int u, int v) {
@@ -745,9 +749,10 @@ __global__ void __launch_bounds__(BLOCK, MINB) pcg_ell_kernel(EllArgs a) {
                 const double* __restrict__ z = a.z;
                 const double* __restrict__ po = p_old;
                 const auto col = [&](int c) { return z[c] + beta * po[c]; };
-                if constexpr (SLAB) s = slab_row(slab + ((i - blockIdx.x * rpb) * 2 + sub) * 5, i, z, po, beta);
-                else if constexpr (LPR == 2) s = ell_row16_2(a.ec, a.ev, i, sub, col);
-                else s = ell_row16(a.ec, a.ev, i, sub, col);
+                const int64_t li = i - blockIdx.x * rpb;  // (CONTIG) row within the block
+                if (SLAB && li < a.slab_rows) s = slab_row(slab + (li * LPR + sub) * 5, i, z, po, beta);
+                else if constexpr (LPR == 4) s = ell_row16(a.ec, a.ev, i, sub, col);
+                else s = ell_row8<W>(a.ec, a.ev, i, sub, col);
             }
 #pragma unroll
             for (int off = 1; off < LPR; off <<= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
@@ -1016,8 +1021,8 @@ extern "C" int tt_integrate_p1(const tt_mesh_t* m, const double* coeffs, double*
 extern "C" int tt_csr_to_ell(int64_t n, const int64_t* rp, const int32_t* ci, const double* v, int width,
                              int32_t* ell_cols, double* ell_vals, double* diag, int32_t* status,
                              void* stream) {
-    if (n < 1 || width != 16) {
-        set_error("tt_csr_to_ell: width must be 16");
+    if (n < 1 || (width != 16 && width != 8)) {
+        set_error("tt_csr_to_ell: width must be 8 or 16");
         return TT_ERR_INVALID_PARAMETER;
     }
     csr_to_ell_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(n, rp, ci, v, width, ell_cols, ell_vals,
@@ -1025,25 +1030,34 @@ extern "C" int tt_csr_to_ell(int64_t n, const int64_t* rp, const int32_t* ci, co
     return launch_check("csr_to_ell_kernel");
 }
 
-extern "C" int tt_pcg_ell(int64_t n, const int32_t* ell_cols, const double* ell_vals, const double* diag,
-                          const double* b, double tol, int64_t maxiter, double* x, double* best_x,
-                          double* work, tt_pcg_result_t* result, void* stream) {
-    if (n < 1 || maxiter < 0) {
-        set_error("tt_pcg_ell: bad size");
-        return TT_ERR_INVALID_PARAMETER;
+static bool ell_args(EllArgs& a, int64_t n, int width, const int32_t* ell_cols, const double* ell_vals,
+                     const double* diag, const double* b, double tol, int64_t maxiter, double* x,
+                     double* best_x, double* work, tt_pcg_result_t* result, const char* who) {
+    if (n < 1 || maxiter < 0 || (width != 8 && width != 16)) {
+        set_error("%s: bad size or width (8 | 16)", who);
+        return false;
     }
-    EllArgs a;
     a.n = n; a.ec = ell_cols; a.ev = ell_vals; a.diag = diag; a.b = b; a.tol = tol; a.maxiter = maxiter;
     a.x = x; a.best_x = best_x;
     a.r = work; a.z = work + n; a.p0 = work + 2 * n; a.p1 = work + 3 * n; a.ap = work + 4 * n;
     a.dinv = work + 5 * n;
     a.part = work + 6 * n;
     a.res = result;
-    // SpMV shape: lanes per row (TT_PCG_ELL_LPR = 2 | 4) and contiguous per-block row
-    // ranges (TT_PCG_ELL_CONTIG = 1 | 0).  Measured on the C2 mass matrix (175,616 rows,
+    a.slab_rows = 0;
+    return true;
+}
+
+extern "C" int tt_pcg_ell(int64_t n, int width, const int32_t* ell_cols, const double* ell_vals,
+                          const double* diag, const double* b, double tol, int64_t maxiter, double* x,
+                          double* best_x, double* work, tt_pcg_result_t* result, void* stream) {
+    EllArgs a;
+    if (!ell_args(a, n, width, ell_cols, ell_vals, diag, b, tol, maxiter, x, best_x, work, result, "tt_pcg_ell"))
+        return TT_ERR_INVALID_PARAMETER;
+    // SpMV shape (W = 16): lanes per row (TT_PCG_ELL_LPR = 2 | 4) and contiguous per-block
+    // row ranges (TT_PCG_ELL_CONTIG = 1 | 0).  Measured on the C2 mass matrix (175,616 rows,
     // 23 iterations): 2 lanes + contiguous 0.357 ms, 4 lanes + contiguous 0.373 ms,
-    // 4 lanes + grid-stride 0.377 ms, 2 lanes + grid-stride 0.404 ms.
-    static const int lpr = [] {
+    // 4 lanes + grid-stride 0.377 ms, 2 lanes + grid-stride 0.404 ms.  W = 8: 1 lane per row.
+    static const int lpr_env = [] {
         const char* v = getenv("TT_PCG_ELL_LPR");
         return (v && atoi(v) == 4) ? 4 : 2;
     }();
@@ -1051,7 +1065,9 @@ extern "C" int tt_pcg_ell(int64_t n, const int32_t* ell_cols, const double* ell_
         const char* v = getenv("TT_PCG_ELL_CONTIG");
         return !(v && atoi(v) == 0);
     }();
-    const void* fn = lpr == 4 ? (contig ? (const void*)pcg_ell_kernel<512, 2, 4, true> : (const void*)pcg_ell_kernel<512, 2, 4>)
+    const int lpr = width == 8 ? 1 : lpr_env;
+    const void* fn = width == 8 ? (const void*)pcg_ell_kernel<512, 2, 1, true, false, 8>
+                   : lpr == 4 ? (contig ? (const void*)pcg_ell_kernel<512, 2, 4, true> : (const void*)pcg_ell_kernel<512, 2, 4>)
                               : (contig ? (const void*)pcg_ell_kernel<512, 2, 2, true> : (const void*)pcg_ell_kernel<512, 2, 2>);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 512, 0);
@@ -1066,44 +1082,51 @@ extern "C" int tt_pcg_ell(int64_t n, const int32_t* ell_cols, const double* ell_
     return cuda_status(e, "pcg_ell_kernel (cooperative launch)");
 }
 
-extern "C" int tt_pcg_ell_slab(int64_t n, const int32_t* ell_cols, const double* ell_vals, const double* diag,
-                               const double* b, double tol, int64_t maxiter, double* x, double* best_x,
-                               double* work, tt_pcg_result_t* result, void* stream) {
-    if (n < 1 || maxiter < 0) {
-        set_error("tt_pcg_ell_slab: bad size");
-        return TT_ERR_INVALID_PARAMETER;
-    }
+extern "C" int tt_pcg_ell_slab(int64_t n, int width, const int32_t* ell_cols, const double* ell_vals,
+                               const double* diag, const double* b, double tol, int64_t maxiter, double* x,
+                               double* best_x, double* work, tt_pcg_result_t* result, void* stream) {
     EllArgs a;
-    a.n = n; a.ec = ell_cols; a.ev = ell_vals; a.diag = diag; a.b = b; a.tol = tol; a.maxiter = maxiter;
-    a.x = x; a.best_x = best_x;
-    a.r = work; a.z = work + n; a.p0 = work + 2 * n; a.p1 = work + 3 * n; a.ap = work + 4 * n;
-    a.dinv = work + 5 * n;
-    a.part = work + 6 * n;
-    a.res = result;
-    const void* fn = (const void*)pcg_ell_kernel<512, 2, 2, true, true>;
+    if (!ell_args(a, n, width, ell_cols, ell_vals, diag, b, tol, maxiter, x, best_x, work, result,
+                  "tt_pcg_ell_slab"))
+        return TT_ERR_INVALID_PARAMETER;
+    const int lpr = width / 8;  // lanes per row = 80-byte chunks per row
+    const void* fn = width == 8 ? (const void*)pcg_ell_kernel<512, 2, 1, true, true, 8>
+                                : (const void*)pcg_ell_kernel<512, 2, 2, true, true, 16>;
     int dev = 0, max_optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     const int sms = sm_count();
+    // rows that must be slab-resident for the slab to pay (TT_PCG_SLAB_MIN_FRAC, default 1/4):
+    // the rest of a block's rows stream from L2/HBM as in tt_pcg_ell
+    static const double min_frac = [] {
+        const char* v = getenv("TT_PCG_SLAB_MIN_FRAC");
+        return v ? atof(v) : 0.25;
+    }();
     // 2 blocks per SM (the 2 x 512 shape of tt_pcg_ell), else 1 with twice the rows.  With
     // 2 per SM the block count and row ranges are tt_pcg_ell's, so the partial sums -- and
     // the iterates -- are bitwise the same
-    const int64_t need = (n * 2 + 511) / 512;
+    const int64_t need = (n * lpr + 511) / 512;
     for (int bps = 2; bps >= 1; --bps) {
         const int64_t nb = need < (int64_t)sms * bps ? need : (int64_t)sms * bps;
         const int64_t rpb = (n + nb - 1) / nb;
-        const int64_t smem = rpb * 160;
-        if (smem + (int64_t)sizeof(double) * 96 > max_optin) continue;
+        const int64_t per_row = 80 * lpr;
+        // per-SM shared memory: 228 KB less 1 KB per block reserved, less the static part
+        const int64_t avail = (int64_t)(bps == 2 ? (228 * 1024) / 2 - 1024 : max_optin) - (int64_t)sizeof(double) * 96;
+        const int64_t cap = avail / per_row;
+        const int64_t rows = rpb < cap ? rpb : cap;
+        if (rows < 1 || (rows < rpb && rows < min_frac * rpb)) continue;
+        const int64_t smem = rows * per_row;
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 512, (size_t)smem);
         if (per_sm < bps) continue;
+        a.slab_rows = rows;
         void* args[] = {&a};
         cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)nb), dim3(512), args, (size_t)smem,
                                                     as_stream(stream));
         return cuda_status(e, "pcg_ell_kernel (slab, cooperative launch)");
     }
-    set_error("tt_pcg_ell_slab: %lld rows do not fit in shared memory", (long long)n);
+    set_error("tt_pcg_ell_slab: too few of the %lld rows fit in shared memory", (long long)n);
     return TT_ERR_CAPACITY;
 }
 

@@ -158,22 +158,24 @@ class SparseSymMatrix:
     __matmul__ = matvec
 
     def ell(self):
-        """(cols (n,16) i32, vals (n,16) f64, diag (n,)) when every row has <= 16 entries
-        (the P1 mass matrices of the generated meshes), else None -> CSR PCG."""
+        """(cols (n,W) i32, vals (n,W) f64, diag (n,), W) with W = 8 when every row has <= 8
+        entries (2-D P1 mass matrices), 16 when <= 16 (3-D), else None -> CSR PCG."""
         if not hasattr(self, "_ell"):
             self._ell = None
-            if int((self.row_ptr_dev[1:] - self.row_ptr_dev[:-1]).max().item()) <= 16:
+            width = int((self.row_ptr_dev[1:] - self.row_ptr_dev[:-1]).max().item())
+            W = 8 if width <= 8 else 16
+            if width <= 16:
                 dev = self.vals_dev.device
-                ec = torch.empty((self.n, 16), dtype=torch.int32, device=dev)
-                ev = torch.empty((self.n, 16), dtype=torch.float64, device=dev)
+                ec = torch.empty((self.n, W), dtype=torch.int32, device=dev)
+                ev = torch.empty((self.n, W), dtype=torch.float64, device=dev)
                 dg = torch.empty(self.n, dtype=torch.float64, device=dev)
                 st = _lib.status_word()
                 _lib.call("tt_csr_to_ell", self.n, _lib.ptr(self.row_ptr_dev), _lib.ptr(self.cols_dev),
-                          _lib.ptr(self.vals_dev), 16, _lib.ptr(ec), _lib.ptr(ev), _lib.ptr(dg),
+                          _lib.ptr(self.vals_dev), W, _lib.ptr(ec), _lib.ptr(ev), _lib.ptr(dg),
                           _lib.ptr(st), _lib.stream_handle())
                 flags = int(st.item())
                 if not flags & _lib.TT_FLAG_CAPACITY:
-                    self._ell = (ec, ev, dg)
+                    self._ell = (ec, ev, dg, W)
                     # shared-memory slab PCG: columns within +-32767 rows of their row
                     self._slab_ok = not flags & _lib.TT_FLAG_WIDE_ROWS
         return self._ell
@@ -236,16 +238,14 @@ def pcg_device(M: SparseSymMatrix, b: torch.Tensor, tol: float = 1e-12,
     best_x = best_x if best_x is not None else torch.empty(n, dtype=torch.float64, device=b.device)
     ell = M.ell() if _PCG_PATH != "csr" else None
     if ell is not None:
-        args = (n, _lib.ptr(ell[0]), _lib.ptr(ell[1]), _lib.ptr(ell[2]), _lib.ptr(b), float(tol), maxiter,
-                _lib.ptr(x), _lib.ptr(best_x), _lib.ptr(work), _lib.ptr(res), _lib.stream_handle())
+        args = (n, ell[3], _lib.ptr(ell[0]), _lib.ptr(ell[1]), _lib.ptr(ell[2]), _lib.ptr(b), float(tol),
+                maxiter, _lib.ptr(x), _lib.ptr(best_x), _lib.ptr(work), _lib.ptr(res), _lib.stream_handle())
         if _PCG_PATH == "ell" and getattr(M, "_slab_ok", False):
             # rows held in shared memory when they fit (TT_ERR_CAPACITY: nothing launched)
             if _lib.call_status("tt_pcg_ell_slab", *args) == 0:
                 return x, best_x, res
             M._slab_ok = False
-        _lib.call("tt_pcg_ell", n, _lib.ptr(ell[0]), _lib.ptr(ell[1]), _lib.ptr(ell[2]), _lib.ptr(b),
-                  float(tol), maxiter, _lib.ptr(x), _lib.ptr(best_x), _lib.ptr(work), _lib.ptr(res),
-                  _lib.stream_handle())
+        _lib.call("tt_pcg_ell", *args)
         return x, best_x, res
     _lib.call("tt_pcg", n, _lib.ptr(M.row_ptr_dev), _lib.ptr(M.cols_dev), _lib.ptr(M.vals_dev),
               _lib.ptr(b), float(tol), maxiter, _lib.ptr(x), _lib.ptr(best_x), _lib.ptr(work),

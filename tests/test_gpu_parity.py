@@ -482,14 +482,15 @@ def test_ell_and_csr_pcg_agree(tt, golden, c1):
         assert np.max(np.abs(x - golden["x_c1_mesh_tol14"])) <= 1e-12
 
 
-@pytest.mark.parametrize("n", [20, 60])
-def test_slab_pcg_3d_and_capacity_fallback(tt, n):
-    """3-D mass matrices: the slab PCG (n=20: 9,261 rows) is bitwise the L2 ELL PCG; at
-    n=60 (226,981 rows, more than fit in 148 SMs' shared memory) tt_pcg_ell_slab reports
-    TT_ERR_CAPACITY without launching and the L2 ELL PCG runs instead."""
+@pytest.mark.parametrize("dim,n", [(3, 20), (3, 60), (2, 707)])
+def test_slab_pcg_full_and_partial(tt, dim, n):
+    """The slab PCG is bitwise the L2 ELL PCG: 3-D n=20 (9,261 rows, width 16) fits whole;
+    3-D n=60 (226,981 rows) and 2-D n=707 (501,264 rows, width 8) keep the first part of
+    every block's rows in shared memory and stream the rest."""
     import torch
     from paper_2603_00538_b200 import fem
-    tgt = tt.generate_cube_mesh(n, 0.2, seed=20, split="kuhn")
+    tgt = (tt.generate_cube_mesh(n, 0.2, seed=20, split="kuhn") if dim == 3
+           else tt.generate_square_mesh(n, 0.2, seed=20, diagonal="right"))
     M = tt.assemble_mass_matrix(tgt)
     b = torch.as_tensor(np.random.default_rng(n).random(tgt.n_nodes), device="cuda")
     xs = []
@@ -499,10 +500,31 @@ def test_slab_pcg_3d_and_capacity_fallback(tt, n):
             xs.append(tt.cg_solve(M, b, tol=1e-14).cpu().numpy())
         finally:
             fem._PCG_PATH = "ell"
-    assert M._slab_ok == (n == 20)
+    assert M.ell()[3] == (8 if dim == 2 else 16)
+    assert M._slab_ok
     assert np.array_equal(xs[0], xs[1])
     xr, _ = O.cg_solve(M.csr, b.cpu().numpy(), tol=1e-14)
     assert _rel(xs[0], xr) <= 1e-12
+
+
+def test_slab_pcg_capacity_fallback(tt):
+    """TT_PCG_SLAB_MIN_FRAC above the fraction that fits: tt_pcg_ell_slab reports
+    TT_ERR_CAPACITY without launching and the L2 ELL PCG solves (same x bits)."""
+    import os
+    import subprocess
+    import sys
+    code = ("import numpy as np, torch, sys; sys.path.insert(0, '.'); import paper_2603_00538_b200 as tt;"
+            "from paper_2603_00538_b200 import fem;"
+            "t = tt.generate_cube_mesh(60, 0.2, seed=20, split='kuhn'); M = tt.assemble_mass_matrix(t);"
+            "b = torch.as_tensor(np.random.default_rng(3).random(t.n_nodes), device='cuda');"
+            "x = tt.cg_solve(M, b, tol=1e-14).cpu().numpy(); assert not M._slab_ok;"
+            "fem._PCG_PATH = 'ell_l2'; y = tt.cg_solve(M, b, tol=1e-14).cpu().numpy();"
+            "assert np.array_equal(x, y); print('ok')")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                         env=dict(os.environ, TT_PCG_SLAB_MIN_FRAC="0.99"),
+                         cwd=str(__import__("pathlib").Path(__file__).resolve().parents[1]))
+    assert out.returncode == 0, out.stderr
+    assert out.stdout.strip().endswith("ok")
 
 
 def test_slab_pcg_wide_rows_not_used(tt):
