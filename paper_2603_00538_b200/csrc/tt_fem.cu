@@ -624,9 +624,16 @@ template <int W, class Col>
 __device__ __forceinline__ double ell_row8(const int32_t* __restrict__ ec, const double* __restrict__ ev,
                                            int64_t i, int sub, Col col) {
     const int4* cq = reinterpret_cast<const int4*>(ec + i * W) + 2 * sub;
+#ifdef TT_ELL_STREAM
+    // matrix rows stream through L2 evict-first, keeping the PCG vectors L2-resident
+    const int4 c0 = __ldcs(cq), c1 = __ldcs(cq + 1);
+    const double2* vq = reinterpret_cast<const double2*>(ev + i * W + 8 * sub);
+    const double2 a0 = __ldcs(vq), a1 = __ldcs(vq + 1), a2 = __ldcs(vq + 2), a3 = __ldcs(vq + 3);
+#else
     const int4 c0 = __ldg(cq), c1 = __ldg(cq + 1);
     const double2* vq = reinterpret_cast<const double2*>(ev + i * W + 8 * sub);
     const double2 a0 = __ldg(vq), a1 = __ldg(vq + 1), a2 = __ldg(vq + 2), a3 = __ldg(vq + 3);
+#endif
     const double x0 = col(c0.x), x1 = col(c0.y), x2 = col(c0.z), x3 = col(c0.w);
     const double x4 = col(c1.x), x5 = col(c1.y), x6 = col(c1.z), x7 = col(c1.w);
     const double s0 = fma(a1.y, x3, fma(a1.x, x2, fma(a0.y, x1, a0.x * x0)));
