@@ -99,17 +99,34 @@ __global__ void key_to_csr_kernel(int64_t nnz, int64_t n_cols, const int64_t* __
     atomicAdd(row_counts + row, 1ull);
 }
 
-__global__ void spmv_rect_kernel(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                                 const double* __restrict__ v, const double* __restrict__ x,
-                                 double* __restrict__ y) {
-    // one warp per row: R rows hold ~50-100 entries
-    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (w >= n) return;
+// y = R x.  LPR lanes per row (R rows hold ~35 entries at C5), rows of a warp contiguous;
+// each lane issues its column and value loads 4 at a time before the gathers, so a lane
+// keeps ~8 independent loads in flight instead of one dependent chain per entry.
+template <int LPR>
+__global__ void __launch_bounds__(256) spmv_rect_kernel(int64_t n, const int64_t* __restrict__ rp,
+                                                        const int32_t* __restrict__ ci,
+                                                        const double* __restrict__ v,
+                                                        const double* __restrict__ x, double* __restrict__ y) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t row = t / LPR;
+    const int sub = (int)(t % LPR);
     double s = 0.0;
-    for (int64_t q = rp[w] + lane; q < rp[w + 1]; q += 32) s = fma(v[q], __ldg(x + ci[q]), s);
-    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    if (lane == 0) y[w] = s;
+    if (row < n) {
+        const int64_t q1 = __ldg(rp + row + 1);
+        int64_t q = __ldg(rp + row) + sub;
+        for (; q + 3 * LPR < q1; q += 4 * LPR) {
+            int c[4];
+            double a[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) { c[k] = __ldg(ci + q + k * LPR); a[k] = __ldg(v + q + k * LPR); }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) s = fma(a[k], __ldg(x + c[k]), s);
+        }
+        for (; q < q1; q += LPR) s = fma(__ldg(v + q), __ldg(x + __ldg(ci + q)), s);
+    }
+#pragma unroll
+    for (int off = LPR / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (row < n && sub == 0) y[row] = s;
 }
 
 template <typename T>
@@ -251,6 +268,16 @@ extern "C" int tt_mc_fold_finish(void* handle, int64_t* row_ptr, int32_t* cols, 
 extern "C" int tt_spmv_rect(int64_t n_rows, const int64_t* rp, const int32_t* ci, const double* v,
                             const double* x, double* y, void* stream) {
     if (n_rows == 0) return TT_OK;
-    spmv_rect_kernel<<<grid_for(n_rows * 32, 256), 256, 0, as_stream(stream)>>>(n_rows, rp, ci, v, x, y);
+    // lanes per row (TT_SPMV_RECT_LPR = 4 | 8 | 16 | 32; default 8)
+    static const int lpr = [] {
+        const char* e = getenv("TT_SPMV_RECT_LPR");
+        const int v = e ? atoi(e) : 8;
+        return (v == 4 || v == 16 || v == 32) ? v : 8;
+    }();
+    auto st = as_stream(stream);
+    if (lpr == 4) spmv_rect_kernel<4><<<grid_for(n_rows * 4, 256), 256, 0, st>>>(n_rows, rp, ci, v, x, y);
+    else if (lpr == 16) spmv_rect_kernel<16><<<grid_for(n_rows * 16, 256), 256, 0, st>>>(n_rows, rp, ci, v, x, y);
+    else if (lpr == 32) spmv_rect_kernel<32><<<grid_for(n_rows * 32, 256), 256, 0, st>>>(n_rows, rp, ci, v, x, y);
+    else spmv_rect_kernel<8><<<grid_for(n_rows * 8, 256), 256, 0, st>>>(n_rows, rp, ci, v, x, y);
     return launch_check("spmv_rect_kernel");
 }
