@@ -142,7 +142,7 @@ int main(int argc, char** argv) {
     double* dc = dup(c, 8 * snn);
     double* grad;
     CU(cudaMalloc((void**)&grad, 32 * sne));
-    CK(tt_pack_grad(&S, srec, dc, grad, st));
+    CK(tt_pack_grad(&S, dc, grad, st));
     tt_source_t src = {0};
     src.kind = TT_SRC_MESH;
     src.outside = TT_OUTSIDE_SNAP;

@@ -250,9 +250,9 @@ int tt_mc_cache_ids(const tt_mesh_t* target, int64_t e_lo, int64_t e_hi, const t
 int tt_pack_coeffs(const tt_mesh_t* src, const double* coeffs, double* out, void* stream);
 
 /* out[e*4 ..] = (g, c_last): the P1 field's gradient on element e and its value at the
- * last vertex (the record origin), from the packed binv: g_j = sum_i binv_ij (c_i - c_last). */
-int tt_pack_grad(const tt_mesh_t* src, const double* rec, const double* coeffs, double* out,
-                 void* stream);
+ * last vertex (the walk record's origin): g solves E g = d, rows e_i = v_i - v_last,
+ * d_i = c_i - c_last, from the vertex coordinates (src->nodes, src->elems). */
+int tt_pack_grad(const tt_mesh_t* src, const double* coeffs, double* out, void* stream);
 
 /* MCTransferOperator's sparse load matrix R (n_t x n_s, transfer.py:56-110) folded on
  * the device from the cached sample ids (shared plans): tt_mc_fold computes it into an

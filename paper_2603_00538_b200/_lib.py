@@ -111,7 +111,7 @@ _SIGNATURES = {
     "tt_mc_cache_ids": ([C.POINTER(tt_mesh_t), _I64, _I64, C.POINTER(tt_plan_t),
                          C.POINTER(tt_grid_t), _P, _P, _P], _I),
     "tt_pack_coeffs": ([C.POINTER(tt_mesh_t), _P, _P, _P], _I),
-    "tt_pack_grad": ([C.POINTER(tt_mesh_t), _P, _P, _P, _P], _I),
+    "tt_pack_grad": ([C.POINTER(tt_mesh_t), _P, _P, _P], _I),
     "tt_mc_fold": ([C.POINTER(tt_mesh_t), C.POINTER(tt_plan_t), C.POINTER(tt_mesh_t), _P, _P,
                     C.POINTER(_I64), C.POINTER(_P), _P], _I),
     "tt_mc_fold_finish": ([_P, _P, _P, _P, _P], _I),

@@ -660,25 +660,57 @@ __global__ void pack_coeffs_kernel(int64_t E, int k, const int32_t* __restrict__
     o[1] = make_double2(c[2], c[3]);
 }
 
+// Per-element (gradient g, value at the origin vertex) of the P1 field: f = c_last +
+// g.(x - v_last) on the element.  g solves E g = d with rows e_i = v_i - v_last and
+// d_i = c_i - c_last (the walk record's binv is E^-T), via cross products / Cramer's rule
+// from the vertex coordinates: the coordinates and coefficients are L2-resident gathers,
+// so the kernel streams only the connectivity in and the 32 B records out.
 template <int D>
 __global__ void pack_grad_kernel(int64_t E, const int32_t* __restrict__ elems,
-                                 const double* __restrict__ rec, const double* __restrict__ coeffs,
+                                 const double* __restrict__ nodes, const double* __restrict__ coeffs,
                                  double* __restrict__ out) {
     constexpr int K = D + 1;
-    constexpr int S = (D == 2) ? 8 : 16;
     int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (e >= E) return;
-    double c[K];
-    for (int i = 0; i < K; ++i) c[i] = coeffs[elems[e * K + i]];
-    const double* b = rec + e * S;
-    double o[4] = {0.0, 0.0, 0.0, 0.0};
-    // g_j = sum_i binv_ij (c_i - c_last); lambda_i = sum_j binv_ij r_j, lambda_last = 1 - sum
-    for (int j = 0; j < D; ++j) {
-        double gj = 0.0;
-        for (int i = 0; i < D; ++i) gj = fma(b[i * D + j], c[i] - c[D], gj);
-        o[j] = gj;
+    int n[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) n[i] = __ldg(elems + e * K + i);
+    double v[K][D], c[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+        c[i] = __ldg(coeffs + n[i]);
+#pragma unroll
+        for (int k = 0; k < D; ++k) v[i][k] = __ldg(nodes + (int64_t)n[i] * D + k);
     }
-    o[D] = c[D];
+    double o[4] = {0.0, 0.0, 0.0, 0.0};
+    o[D] = c[D];  // record = (g_0 .. g_{D-1}, c_last[, 0])
+    if constexpr (D == 2) {
+        const double a0 = v[0][0] - v[2][0], a1 = v[0][1] - v[2][1];
+        const double b0 = v[1][0] - v[2][0], b1 = v[1][1] - v[2][1];
+        const double d0 = c[0] - c[2], d1 = c[1] - c[2];
+        const double inv = 1.0 / (a0 * b1 - a1 * b0);
+        o[0] = (b1 * d0 - a1 * d1) * inv;
+        o[1] = (a0 * d1 - b0 * d0) * inv;
+    } else {
+        double ed[3][3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int k = 0; k < 3; ++k) ed[i][k] = v[i][k] - v[3][k];
+        const auto cross = [](const double* x, const double* y, double* z) {
+            z[0] = x[1] * y[2] - x[2] * y[1];
+            z[1] = x[2] * y[0] - x[0] * y[2];
+            z[2] = x[0] * y[1] - x[1] * y[0];
+        };
+        double c12[3], c20[3], c01[3];
+        cross(ed[1], ed[2], c12);
+        cross(ed[2], ed[0], c20);
+        cross(ed[0], ed[1], c01);
+        const double inv = 1.0 / (ed[0][0] * c12[0] + ed[0][1] * c12[1] + ed[0][2] * c12[2]);
+        const double d0 = c[0] - c[3], d1 = c[1] - c[3], d2 = c[2] - c[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) o[k] = (d0 * c12[k] + d1 * c20[k] + d2 * c01[k]) * inv;
+    }
     double2* q = reinterpret_cast<double2*>(out + e * 4);
     q[0] = make_double2(o[0], o[1]);
     q[1] = make_double2(o[2], o[3]);
@@ -1116,17 +1148,16 @@ extern "C" int tt_pack_coeffs(const tt_mesh_t* m, const double* coeffs, double* 
     return launch_check("pack_coeffs_kernel");
 }
 
-extern "C" int tt_pack_grad(const tt_mesh_t* m, const double* rec, const double* coeffs, double* out,
-                            void* stream) {
-    if (!m || (m->dim != 2 && m->dim != 3) || !rec || !coeffs || !out) {
+extern "C" int tt_pack_grad(const tt_mesh_t* m, const double* coeffs, double* out, void* stream) {
+    if (!m || (m->dim != 2 && m->dim != 3) || !m->nodes || !m->elems || !coeffs || !out) {
         set_error("tt_pack_grad: bad arguments");
         return TT_ERR_INVALID_PARAMETER;
     }
     if (m->n_elems == 0) return TT_OK;
     if (m->dim == 2)
-        pack_grad_kernel<2><<<grid_for(m->n_elems, 256), 256, 0, as_stream(stream)>>>(m->n_elems, m->elems, rec, coeffs, out);
+        pack_grad_kernel<2><<<grid_for(m->n_elems, 256), 256, 0, as_stream(stream)>>>(m->n_elems, m->elems, m->nodes, coeffs, out);
     else
-        pack_grad_kernel<3><<<grid_for(m->n_elems, 256), 256, 0, as_stream(stream)>>>(m->n_elems, m->elems, rec, coeffs, out);
+        pack_grad_kernel<3><<<grid_for(m->n_elems, 256), 256, 0, as_stream(stream)>>>(m->n_elems, m->elems, m->nodes, coeffs, out);
     return launch_check("pack_grad_kernel");
 }
 

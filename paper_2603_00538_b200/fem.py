@@ -76,7 +76,7 @@ class NodalField:
         dm = self.mesh.device
         out = torch.empty((self.mesh.n_elems, 4), dtype=torch.float64, device=self.coeffs_dev.device)
         desc = dm.desc()
-        _lib.call("tt_pack_grad", C.byref(desc), _lib.ptr(dm.rec), _lib.ptr(self.coeffs_dev),
+        _lib.call("tt_pack_grad", C.byref(desc), _lib.ptr(self.coeffs_dev),
                   _lib.ptr(out), _lib.stream_handle())
         self._grad = (key, out)
         return out
