@@ -176,3 +176,29 @@ def test_cli_parser_and_errors(tmp_path):
     assert cli.main(["transfer", "--gen-source", "3"]) == 1          # missing target mesh
     m = cli.parse_gen_spec("cube:2,0.1,3")
     assert m.DIM == 3 and m.n_elems == 48
+
+
+def test_walk_seed_anchor_tables_are_reproducible():
+    """The 16 walk-seed anchors compiled into tt_common.cuh are what scripts/seed_anchors.py
+    derives (centroid + corner points fixed, k-means for the rest): barycentric, sum 1."""
+    import re
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    src = (root / "paper_2603_00538_b200" / "csrc" / "tt_common.cuh").read_text()
+    out = subprocess.run([sys.executable, str(root / "scripts" / "seed_anchors.py")], capture_output=True,
+                         text=True, check=True).stdout
+    for D in (2, 3):
+        def table(text):
+            body = re.search(rf"kAnchor{D}\[16\]\[{D + 1}\] = \{{(.*?)\}};", text, re.S).group(1)
+            return np.array([[float(v) for v in row.split(",")] for row in re.findall(r"\{([^{}]*)\}", body)])
+        compiled, derived = table(src), table(out)
+        assert compiled.shape == (16, D + 1)
+        np.testing.assert_array_equal(compiled, derived)
+        np.testing.assert_allclose(compiled.sum(1), 1.0, atol=5e-6)
+        assert np.all(compiled > 0)
+        K = D + 1
+        assert np.allclose(compiled[0], 1.0 / K)                      # centroid first
+        for i in range(K):                                              # then (v_i + c) / 2
+            assert compiled[1 + i, i] == pytest.approx((1 + K) / (2 * K), abs=1e-6)
