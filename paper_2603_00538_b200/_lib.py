@@ -156,8 +156,15 @@ def load_library(require_device: bool = True):
     return _lib
 
 
+_lib_dev = None
+
+
 def lib():
-    return load_library(True)
+    """The library, with a CUDA device checked once per process (hot path: every call)."""
+    global _lib_dev
+    if _lib_dev is None:
+        _lib_dev = load_library(True)
+    return _lib_dev
 
 
 def stream_handle(stream=None):
