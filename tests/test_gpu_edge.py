@@ -125,3 +125,34 @@ def test_peer_reduction_is_gpu_count_invariant(tt, world):
     lo = torch.tensor([a for a, _ in spans], dtype=torch.int64, device="cuda")
     b = reduce_nodes_peers(tgt, ptrs, lo)
     assert torch.equal(b, full)
+
+
+@pytest.mark.parametrize("n", [1, 2, 5, 33, 600])
+def test_pcg_small_systems_all_paths(tt, n):
+    """Tiny SPD systems through the slab, L2-ELL and CSR PCGs (block ranges with no rows,
+    a single row, partial warps): each matches the oracle recurrence."""
+    import scipy.sparse as sp
+    import torch
+    from paper_2603_00538_b200 import fem
+    rng = np.random.default_rng(n)
+    main = 4.0 + rng.random(n)
+    A = sp.diags([main] + ([rng.random(n - 1), ] * 2 if n > 1 else []),
+                 [0] + ([1, -1] if n > 1 else [])).tocsr()
+    A = ((A + A.T) * 0.5).tocsr()
+    A.sort_indices()
+    b = rng.standard_normal(n)
+    dev = torch.device("cuda")
+    xs = []
+    for path in ("ell", "ell_l2", "csr"):
+        M = fem.SparseSymMatrix(n, torch.as_tensor(A.indptr.astype(np.int64), device=dev),
+                                torch.as_tensor(A.indices.astype(np.int32), device=dev),
+                                torch.as_tensor(A.data, device=dev))
+        fem._PCG_PATH = path
+        try:
+            xs.append(tt.cg_solve(M, b, tol=1e-14))
+        finally:
+            fem._PCG_PATH = "ell"
+    xr, _ = O.cg_solve(A, b, tol=1e-14)
+    for x in xs:
+        assert np.max(np.abs(x - xr)) <= 1e-12 * max(1.0, np.max(np.abs(xr)))
+    assert np.array_equal(xs[0], xs[1])   # slab and L2 ELL: same partition, same bits
