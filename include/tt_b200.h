@@ -313,7 +313,7 @@ int tt_pcg_ell(int64_t n, int width, const int32_t* ell_cols, const double* ell_
                void* stream);
 /* The same PCG with each block's rows of the ELL matrix held in shared memory for the whole
  * solve (80 B per row per 8 columns): all of them when they fit (n up to ~207k rows at width
- * 16, ~415k at width 8), else the first part of every block's range (at least 1/4 of it;
+ * 16, ~415k at width 8), else the first part of every block's range (at least 1/2 of it;
  * TT_PCG_SLAB_MIN_FRAC) with the rest streamed from L2/HBM.  Precondition: tt_csr_to_ell did
  * not set TT_FLAG_WIDE_ROWS.  Returns TT_ERR_CAPACITY, launching nothing, when too few rows
  * fit (the caller then uses tt_pcg_ell). */
