@@ -156,3 +156,22 @@ def test_pcg_small_systems_all_paths(tt, n):
     for x in xs:
         assert np.max(np.abs(x - xr)) <= 1e-12 * max(1.0, np.max(np.abs(xr)))
     assert np.array_equal(xs[0], xs[1])   # slab and L2 ELL: same partition, same bits
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_gradient_records_match_numpy(tt, dim):
+    """tt_pack_grad: per element (g, c_last) with f = c_last + g.(x - v_last) equal to the
+    P1 interpolant -- checked against numpy's solve of E g = d at every element."""
+    mesh = (tt.generate_square_mesh(9, 0.2, seed=3) if dim == 2
+            else tt.generate_cube_mesh(4, 0.2, seed=3))
+    rng = np.random.default_rng(dim)
+    field = tt.NodalField(mesh, rng.standard_normal(mesh.n_nodes))
+    rec = field.elem_grad().cpu().numpy()
+    v = mesh.nodes[mesh.elements]                       # (E, k, d)
+    c = field.coeffs[mesh.elements]                     # (E, k)
+    Emat = v[:, :dim] - v[:, dim:dim + 1]               # rows e_i = v_i - v_last
+    g = np.linalg.solve(Emat, (c[:, :dim] - c[:, dim:dim + 1])[..., None])[..., 0]
+    np.testing.assert_allclose(rec[:, :dim], g, rtol=1e-12, atol=1e-12)
+    np.testing.assert_array_equal(rec[:, dim], c[:, dim])
+    if dim == 2:
+        assert np.all(rec[:, 3] == 0.0)
