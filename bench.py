@@ -371,14 +371,18 @@ def run_ours(args):
         # transfer_mc / MCTransferOperator.apply / DistributedCoupling.step, x back to host
         c_dev.copy_(c_host, non_blocking=True)
         field = tt.NodalField(src, c_dev)
+        # (transfer_mc / apply take the pinned host buffer as `out`: the x D2H is queued
+        # before the call's one synchronisation and `.coeffs` is a view of it)
         if args.config == "c5":
-            xx = ops[plan.n_samples].apply(field).coeffs_dev
+            xh = ops[plan.n_samples].apply(field, out=x_host).coeffs
         elif coupling is not None:
             xx = coupling.step(tt.MeshBackedField(field, loc), plan, tol=1e-12)
+            x_host.copy_(xx, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            xh = x_host
         else:
-            xx = tt.transfer_mc(tgt, tt.MeshBackedField(field, loc), plan, cg_tol=1e-12).coeffs_dev
-        x_host.copy_(xx, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
+            xh = tt.transfer_mc(tgt, tt.MeshBackedField(field, loc), plan, cg_tol=1e-12, out=x_host).coeffs
+        assert xh.shape[0] == tgt.n_nodes
     for _ in range(args.warmup):
         e2e_step()
     torch.cuda.synchronize()
@@ -429,8 +433,9 @@ def run_ours(args):
                                   "phase": "load (source pack + fused MC kernel + node gather), max over ranks"},
             "e2e": {"value": S / (e2e_ms * 1e-3), "unit": "samples/s", "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": src.n_nodes * 8, "d2h_bytes_per_step": tgt.n_nodes * 8,
-                    "api": "NodalField(pinned H2D) -> transfer_mc(MeshBackedField) | "
-                           "MCTransferOperator.apply (c5) | DistributedCoupling.step (N>1) -> x D2H"},
+                    "api": "NodalField(pinned H2D) -> transfer_mc(MeshBackedField, out=pinned x).coeffs | "
+                           "MCTransferOperator.apply(field, out=pinned x).coeffs (c5) | "
+                           "DistributedCoupling.step + x D2H (N>1)"},
             "roofline": {"bound": "hbm",
                          "kernel": ("spmv_rect (folded R @ c)" if folded else "mc_load_kernel<3,SHARED,CACHED>")
                          if args.config == "c5" else "mc_mesh_kernel<3,SHARED,G,spec>",

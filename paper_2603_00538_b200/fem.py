@@ -310,6 +310,25 @@ def finish_solve(x, best_x, res, was_np: bool = False, status: torch.Tensor | No
     return x.cpu().numpy() if was_np else x
 
 
+def solved_field(mesh, x, best_x, res, status: torch.Tensor | None = None,
+                 out: torch.Tensor | None = None) -> NodalField:
+    """NodalField of a launched solve.  ``out``: a caller-owned pinned host tensor (n,)
+    f64; the D2H of x into it is queued BEFORE the one synchronisation of
+    ``finish_solve``, so ``.coeffs`` (the host array the reference returns; a view of
+    ``out``) costs no second round trip."""
+    if out is not None:
+        if out.device.type != "cpu" or out.dtype != torch.float64 or out.shape != (mesh.n_nodes,):
+            raise DimensionMismatch(f"out must be a host float64 tensor of shape ({mesh.n_nodes},)")
+        out.copy_(x, non_blocking=True)
+    xf = finish_solve(x, best_x, res, False, status)
+    field = NodalField(mesh, xf)
+    if out is not None:
+        if xf is not x:                  # b = 0: the solution is the zero vector
+            out.zero_()
+        field._host = out.numpy()
+    return field
+
+
 def integrate_field(field: NodalField, rule: QuadratureRule | None = None) -> float:
     """Integral of a P1 field over the mesh (fem.py:155-161), device reduction."""
     dm = field.mesh.device

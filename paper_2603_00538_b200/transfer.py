@@ -18,20 +18,22 @@ import torch
 
 from . import _lib
 from .errors import DimensionMismatch
-from .fem import NodalField, finish_solve, pcg_device
+from .fem import NodalField, pcg_device, solved_field
 from .locate import UniformGridLocator
 from .montecarlo import SamplePlan, _raise_status, load_vector
 
 
 def transfer_mc(target, source, plan: SamplePlan, cg_tol: float = 1e-12, workers: int = 1,
-                *, deterministic: bool = True) -> NodalField:
-    """One-shot stochastic transfer from a black-box pointwise source (transfer.py:158-163)."""
+                *, deterministic: bool = True, out=None) -> NodalField:
+    """One-shot stochastic transfer from a black-box pointwise source (transfer.py:158-163).
+    ``out`` (extension): a pinned host float64 tensor receiving the coefficients, copied
+    before the call's one synchronisation (``.coeffs`` is then a view of it)."""
     # load and solve are launched back to back; one synchronisation at the end reads the
     # load's status word and the solver result together (errors raised as the reference)
     status = _lib.status_word()
     b = load_vector(target, source, plan, deterministic=deterministic, check=False, status=status)
     x, best_x, res = pcg_device(target.device.mass, b, tol=cg_tol)
-    return NodalField(target, finish_solve(x, best_x, res, False, status))
+    return solved_field(target, x, best_x, res, status, out)
 
 
 class MCTransferOperator:
@@ -122,16 +124,17 @@ class MCTransferOperator:
             _raise_status(int(status.item()))
         return b
 
-    def apply(self, source_field: NodalField) -> NodalField:
-        """Transfer a nodal field on the source mesh (precomputed localisation)."""
+    def apply(self, source_field: NodalField, *, out=None) -> NodalField:
+        """Transfer a nodal field on the source mesh (precomputed localisation); ``out`` as
+        in ``transfer_mc``."""
         status = _lib.status_word()
         b = self.load(source_field, check=False, status=status)
         x, best_x, res = pcg_device(self.mass, b, tol=self.cg_tol)
-        return NodalField(self.target, finish_solve(x, best_x, res, False, status))
+        return solved_field(self.target, x, best_x, res, status, out)
 
-    def apply_sampled(self, source) -> NodalField:
+    def apply_sampled(self, source, *, out=None) -> NodalField:
         """Transfer from a pointwise black box, re-querying every sample."""
         status = _lib.status_word()
         b = load_vector(self.target, source, self.plan, check=False, status=status)
         x, best_x, res = pcg_device(self.mass, b, tol=self.cg_tol)
-        return NodalField(self.target, finish_solve(x, best_x, res, False, status))
+        return solved_field(self.target, x, best_x, res, status, out)

@@ -244,3 +244,24 @@ def test_c_abi_example_matches_python_api(tt):
     assert abs(c["x0"] - x[0]) <= 1e-12
     assert abs(c["checksum"] - float(np.sum(x * ((np.arange(len(x)) % 7) + 1)))) <= 1e-10
     assert abs(c["integral"] - tt.integrate_field(tt.NodalField(tgt, x))) <= 1e-13
+
+
+def test_transfer_out_buffer(tt, small_pair):
+    """transfer_mc / MCTransferOperator.apply with a pinned host `out`: the same coefficients,
+    and .coeffs is a view of `out` (the D2H was queued before the call's one sync)."""
+    import torch
+    target, source_mesh = small_pair
+    field = tt.NodalField.from_function(source_mesh, lambda x, y: np.sin(2 * x) - y)
+    plan = tt.SamplePlan.build(64, mode="sobol", seed=0)
+    ref = tt.transfer_mc(target, tt.MeshBackedField(field), plan).coeffs
+    out = torch.empty(target.n_nodes, dtype=torch.float64).pin_memory()
+    got = tt.transfer_mc(target, tt.MeshBackedField(field), plan, out=out)
+    assert np.shares_memory(got.coeffs, out.numpy())
+    np.testing.assert_array_equal(got.coeffs, ref)
+    op = tt.MCTransferOperator(target, source_mesh, plan)
+    out2 = torch.empty(target.n_nodes, dtype=torch.float64).pin_memory()
+    np.testing.assert_array_equal(op.apply(field, out=out2).coeffs, op.apply(field).coeffs)
+    zero = tt.NodalField(source_mesh, np.zeros(source_mesh.n_nodes))
+    assert np.all(op.apply(zero, out=out2).coeffs == 0.0)          # b = 0 -> zeros in `out`
+    with pytest.raises(tt.DimensionMismatch):
+        tt.transfer_mc(target, tt.MeshBackedField(field), plan, out=torch.empty(3, dtype=torch.float64))
