@@ -897,16 +897,25 @@ template <int D, int PLAN, int SRC>
 static int dispatch_g(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_plan_t* p,
                       const tt_source_t* s, double* contrib, double* b, int32_t* status,
                       cudaStream_t st) {
-    // lanes per element: ~16 samples per lane (measured best: amortises the per-element
-    // setup while the dynamic schedule keeps the group's lanes busy)
+    // lanes per element G.  Measured on C2 (fused mesh kernel, ms per load): N = 32 / 48
+    // G = 4 0.694 / 0.927 vs G = 2 0.744 / 1.053; N = 64 G = 4 best (G = 8 +5 %);
+    // N = 128 G = 4 ~ G = 8; N = 256 G = 16 3.76 vs G = 8 3.87; N = 512 G = 16 6.94 vs
+    // G = 32 7.35; N = 1024 G = 16 13.41 vs 13.68.  TT_MC_SPL=<samples per lane> restores
+    // the plain N / spl rule for experiments.
     const int64_t N = p->n_samples;
-    static int spl = [] { const char* v = getenv("TT_MC_SPL"); return v ? atoi(v) : 16; }();
-    const int64_t gsel = N / spl;  // lanes so that each lane gets ~spl samples
+    static int spl = [] { const char* v = getenv("TT_MC_SPL"); return v ? atoi(v) : 0; }();
+    int G;
+    if (spl > 0 || SRC != TT_SRC_MESH) {  // other sources: ~16 samples per lane
+        const int64_t gsel = N / (spl > 0 ? spl : 16);
+        G = gsel < 4 ? 2 : gsel < 8 ? 4 : gsel < 16 ? 8 : gsel < 32 ? 16 : 32;
+    } else {
+        G = N < 32 ? 2 : N < 128 ? 4 : N < 256 ? 8 : N < 2048 ? 16 : 32;
+    }
     if constexpr (SRC == TT_SRC_MESH)
-        if (gsel < 4) return launch_mc<D, PLAN, SRC, 2>(t, e_lo, e_hi, p, s, contrib, b, status, st);
-    if (gsel < 8) return launch_mc<D, PLAN, SRC, 4>(t, e_lo, e_hi, p, s, contrib, b, status, st);
-    if (gsel < 16) return launch_mc<D, PLAN, SRC, 8>(t, e_lo, e_hi, p, s, contrib, b, status, st);
-    if (gsel < 32) return launch_mc<D, PLAN, SRC, 16>(t, e_lo, e_hi, p, s, contrib, b, status, st);
+        if (G == 2) return launch_mc<D, PLAN, SRC, 2>(t, e_lo, e_hi, p, s, contrib, b, status, st);
+    if (G <= 4) return launch_mc<D, PLAN, SRC, 4>(t, e_lo, e_hi, p, s, contrib, b, status, st);
+    if (G == 8) return launch_mc<D, PLAN, SRC, 8>(t, e_lo, e_hi, p, s, contrib, b, status, st);
+    if (G == 16) return launch_mc<D, PLAN, SRC, 16>(t, e_lo, e_hi, p, s, contrib, b, status, st);
     return launch_mc<D, PLAN, SRC, 32>(t, e_lo, e_hi, p, s, contrib, b, status, st);
 }
 
