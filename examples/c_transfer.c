@@ -126,7 +126,7 @@ int main(int argc, char** argv) {
     G.wrec = wrec;
     int32_t* seeds;
     CU(cudaMalloc((void**)&seeds, sizeof(int32_t) * TT_SEED_ANCHORS * tne));
-    CK(tt_seed_elements(&G, &T, 0, tne, seeds, st));
+    CK(tt_seed_elements(&G, &T, 0, tne, seeds, NULL, st));
 
     /* plan: Sobol(N, skip 0) -> barycentric (SamplePlan.build(N, "sobol", 0)) */
     double *par, *lam;

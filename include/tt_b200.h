@@ -57,6 +57,12 @@ extern "C" {
 #define TT_FLAG_INVALID_DENSITY  8  /* InvalidDensity: p <= 0          montecarlo.py:129-130 */
 #define TT_FLAG_NONMANIFOLD     16  /* a facet shared by > 2 elements (mesh.py:50-53)      */
 #define TT_FLAG_WIDE_ROWS       32  /* an ELL column is > 32767 rows from its row: no slab  */
+#define TT_FLAG_SNAPPED         64  /* tt_seed_elements: an anchor point was outside (snapped) */
+
+/* tt_source_t.hints */
+#define TT_HINT_DEFER_SNAP       1  /* outside samples likely (the seeds saw TT_FLAG_SNAPPED):
+                                       run their nearest-element searches warp-cooperatively at
+                                       the end of each tile instead of on the diverged lane */
 
 /* ---- enums ---- */
 #define TT_PLAN_SHARED  0   /* one (N, k) barycentric table shared by all elements (reference) */
@@ -153,7 +159,7 @@ typedef struct tt_source {
     int32_t kind;             /* TT_SRC_* */
     int32_t outside;          /* TT_OUTSIDE_SNAP | TT_OUTSIDE_STRICT (mesh sources) */
     int32_t dim;              /* point dimension the source is queried in (2 or 3) */
-    int32_t reserved;
+    int32_t hints;            /* TT_HINT_* bits (performance only, never results) */
     tt_expr_t expr;           /* TT_SRC_EXPR program (passed by value into the kernel) */
     tt_grid_t grid;           /* TT_SRC_MESH locator over the source mesh */
     const int32_t* src_elems; /* TT_SRC_MESH (E_s, k) */
@@ -223,7 +229,8 @@ int tt_grid_walk_prep(const tt_mesh_t* mesh, const int64_t* inc_start, const int
  * starts: a sample starts at its nearest anchor's element. */
 #define TT_SEED_ANCHORS 16
 int tt_seed_elements(const tt_grid_t* grid, const tt_mesh_t* target, int64_t e_lo,
-                     int64_t e_hi, int32_t* seeds, void* stream);
+                     int64_t e_hi, int32_t* seeds, int32_t* status /* TT_FLAG_SNAPPED, or NULL */,
+                     void* stream);
 int tt_nearest(const tt_grid_t* grid, const double* points, int64_t count,
                int32_t* elem /* out */, void* stream);
 int tt_snap(const tt_grid_t* grid, const double* points, int64_t count,

@@ -24,6 +24,8 @@ TT_FLAG_NONFINITE, TT_FLAG_OUTSIDE_STRICT, TT_FLAG_CAPACITY, TT_FLAG_INVALID_DEN
 TT_FLAG_NONMANIFOLD = 16
 TT_FLAG_WIDE_ROWS = 32
 TT_SEED_ANCHORS = 16
+TT_FLAG_SNAPPED = 64
+TT_HINT_DEFER_SNAP = 1
 TT_PLAN_SHARED, TT_PLAN_PHILOX = 0, 1
 TT_SRC_EXPR, TT_SRC_MESH, TT_SRC_VALUES, TT_SRC_CACHED = 0, 1, 2, 3
 TT_OUTSIDE_SNAP, TT_OUTSIDE_STRICT = 0, 1
@@ -68,7 +70,7 @@ class tt_expr_t(C.Structure):
 
 class tt_source_t(C.Structure):
     _fields_ = [("kind", C.c_int32), ("outside", C.c_int32), ("dim", C.c_int32),
-                ("reserved", C.c_int32), ("expr", tt_expr_t), ("grid", tt_grid_t),
+                ("hints", C.c_int32), ("expr", tt_expr_t), ("grid", tt_grid_t),
                 ("src_elems", C.c_void_p), ("coeffs", C.c_void_p), ("values", C.c_void_p),
                 ("cached_ids", C.c_void_p), ("seeds", C.c_void_p), ("elem_coeffs", C.c_void_p),
                 ("elem_grad", C.c_void_p)]
@@ -101,7 +103,7 @@ _SIGNATURES = {
     "tt_locate": ([C.POINTER(tt_grid_t), _P, _I64, _D, _P, _P, _P], _I),
     "tt_locate_many": ([_P, _I64, _I, _I, C.POINTER(_D), _P, _P, _P, _P, _D, _P, _P, _P], _I),
     "tt_grid_walk_prep": ([C.POINTER(tt_mesh_t), _P, _P, _D, _P, _P, _P, _P], _I),
-    "tt_seed_elements": ([C.POINTER(tt_grid_t), C.POINTER(tt_mesh_t), _I64, _I64, _P, _P], _I),
+    "tt_seed_elements": ([C.POINTER(tt_grid_t), C.POINTER(tt_mesh_t), _I64, _I64, _P, _P, _P], _I),
     "tt_nearest": ([C.POINTER(tt_grid_t), _P, _I64, _P, _P], _I),
     "tt_snap": ([C.POINTER(tt_grid_t), _P, _I64, _P, _P, _P], _I),
     "tt_map_points": ([C.POINTER(tt_mesh_t), _I64, _I64, C.POINTER(tt_plan_t), _P, _P], _I),

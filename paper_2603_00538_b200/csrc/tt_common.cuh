@@ -335,6 +335,71 @@ TT_D int nearest_element(const GridDev& g, const double* x) {
     return best;
 }
 
+// nearest_element with the 32 lanes of a warp cooperating (all lanes call it with the same
+// x): each ring's cells are dealt out to the lanes, every lane keeps the lexicographic
+// minimum of (d2, id) over its candidates, the ring bookkeeping (first non-empty ring, stop
+// one ring later) is warp-uniform, and a shuffle tree takes the minimum over the lanes.
+// The minimum of (d2, id) does not depend on the order candidates are visited, so the
+// result is nearest_element's, bit for bit.
+template <int D>
+__device__ __noinline__ int nearest_element_warp(const GridDev g, double x0, double x1, double x2) {
+    const double x[3] = {x0, x1, x2};
+    const int lane = threadIdx.x & 31;
+    int home[3];
+    const int n[3] = {g.n0, g.n1, g.n2};
+    for (int c = 0; c < D; ++c) {
+        double t = mul(div(sub(x[c], g.lo[c]), sub(g.hi[c], g.lo[c])), (double)n[c]);
+        t = t < 0.0 ? 0.0 : t;
+        t = t > (double)(n[c] - 1) ? (double)(n[c] - 1) : t;
+        home[c] = (int)t;
+    }
+    if constexpr (D == 2) home[2] = 0;
+    int best = -1;
+    double best_d2 = __longlong_as_double(0x7ff0000000000000LL);  // +inf
+    int first = -1;
+    int max_ring = n[0] > n[1] ? n[0] : n[1];
+    if constexpr (D == 3) max_ring = max_ring > n[2] ? max_ring : n[2];
+    for (int ring = 0; ring <= max_ring; ++ring) {
+        if (first >= 0 && ring > first + 1) break;
+        const int side = 2 * ring + 1;
+        const int rz = (D == 3) ? ring : 0;
+        const int64_t cube = (int64_t)side * side * (D == 3 ? side : 1);
+        bool found = false;
+        for (int64_t q = lane; q < cube; q += 32) {
+            const int cx = home[0] - ring + (int)(q % side);
+            const int cy = home[1] - ring + (int)((q / side) % side);
+            const int cz = home[2] - rz + (D == 3 ? (int)(q / ((int64_t)side * side)) : 0);
+            if (cx < 0 || cx >= n[0] || cy < 0 || cy >= n[1] || cz < 0 || cz >= n[2]) continue;
+            const int dx = abs(cx - home[0]), dy = abs(cy - home[1]), dz = abs(cz - home[2]);
+            int cheb = dx > dy ? dx : dy;
+            cheb = cheb > dz ? cheb : dz;
+            if (cheb != ring) continue;
+            const int64_t c = ((int64_t)cx * n[1] + cy) * n[2] + cz;
+            const int64_t j0 = __ldg(g.cell_start + c), j1 = __ldg(g.cell_start + c + 1);
+            for (int64_t j = j0; j < j1; ++j) {
+                const int e = __ldg(g.cell_elems + j);
+                const double d0 = sub(__ldg(g.centroids + (int64_t)e * D + 0), x[0]);
+                const double d1 = sub(__ldg(g.centroids + (int64_t)e * D + 1), x[1]);
+                double d2 = add(mul(d0, d0), mul(d1, d1));
+                if constexpr (D == 3) {
+                    const double dd = sub(__ldg(g.centroids + (int64_t)e * D + 2), x[2]);
+                    d2 = add(d2, mul(dd, dd));
+                }
+                if (d2 < best_d2 || (d2 == best_d2 && e < best)) { best = e; best_d2 = d2; }
+                found = true;
+            }
+        }
+        if (first < 0 && __any_sync(0xffffffffu, found)) first = ring;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const double od = __shfl_xor_sync(0xffffffffu, best_d2, off);
+        const int oe = __shfl_xor_sync(0xffffffffu, best, off);
+        if (oe >= 0 && (best < 0 || od < best_d2 || (od == best_d2 && oe < best))) { best = oe; best_d2 = od; }
+    }
+    return best;
+}
+
 // Snapped barycentrics: clip(lambda, 0) / sum (montecarlo.py:58-63)
 template <int D>
 TT_D void snap_lambda(const GridDev& g, int e, const double* x, double* lam) {

@@ -415,7 +415,7 @@ __global__ void walk_prep_kernel(int64_t E, const double* __restrict__ nodes,
 template <int D>
 __global__ void seed_kernel(GridDev g, const double* __restrict__ nodes,
                             const int32_t* __restrict__ elems, int64_t e_lo, int64_t n_el,
-                            int32_t* __restrict__ seeds) {
+                            int32_t* __restrict__ seeds, int32_t* __restrict__ status) {
     constexpr int K = D + 1;
     int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (t >= n_el * kSeeds) return;
@@ -430,7 +430,10 @@ __global__ void seed_kernel(GridDev g, const double* __restrict__ nodes,
     }
     double l[D + 1];
     int es = locate_point<D>(g, x, 1e-12, l);
-    if (es < 0) es = nearest_element<D>(g, x);
+    if (es < 0) {
+        es = nearest_element<D>(g, x);
+        if (status) atomicOr(status, TT_FLAG_SNAPPED);
+    }
     seeds[t] = es;
 }
 
@@ -640,7 +643,7 @@ extern "C" int tt_grid_walk_prep(const tt_mesh_t* m, const int64_t* inc_start, c
 }
 
 extern "C" int tt_seed_elements(const tt_grid_t* g, const tt_mesh_t* t, int64_t e_lo, int64_t e_hi,
-                                int32_t* seeds, void* stream) {
+                                int32_t* seeds, int32_t* status, void* stream) {
     if (!grid_ok(g) || !t || t->dim != g->dim || e_lo < 0 || e_hi > t->n_elems || e_lo > e_hi) {
         set_error("tt_seed_elements: bad arguments");
         return TT_ERR_INVALID_PARAMETER;
@@ -649,8 +652,8 @@ extern "C" int tt_seed_elements(const tt_grid_t* g, const tt_mesh_t* t, int64_t 
     GridDev gd = to_dev(*g);
     auto s = as_stream(stream);
     if (g->dim == 2)
-        seed_kernel<2><<<grid_for((e_hi - e_lo) * kSeeds, 128), 128, 0, s>>>(gd, t->nodes, t->elems, e_lo, e_hi - e_lo, seeds);
+        seed_kernel<2><<<grid_for((e_hi - e_lo) * kSeeds, 128), 128, 0, s>>>(gd, t->nodes, t->elems, e_lo, e_hi - e_lo, seeds, status);
     else
-        seed_kernel<3><<<grid_for((e_hi - e_lo) * kSeeds, 128), 128, 0, s>>>(gd, t->nodes, t->elems, e_lo, e_hi - e_lo, seeds);
+        seed_kernel<3><<<grid_for((e_hi - e_lo) * kSeeds, 128), 128, 0, s>>>(gd, t->nodes, t->elems, e_lo, e_hi - e_lo, seeds, status);
     return launch_check("seed_kernel");
 }

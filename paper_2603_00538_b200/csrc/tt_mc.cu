@@ -303,7 +303,7 @@ __device__ __forceinline__ int seed_slot_nearest(const double* lam) {
 // data, so results are bitwise reproducible.  Identical ids/lambdas as the reference scan
 // (certified walk, see locate_walk in tt_common.cuh).
 template <int D, int PLAN, int G, bool SPEC, int MINB, bool FW = false, int BLOCK = 256,
-          bool SMEMV = false, bool RL = false, bool SLOT = false>
+          bool SMEMV = false, bool RL = false, bool SLOT = false, bool DEFER = false>
 __global__ void __launch_bounds__(BLOCK, MINB) mc_mesh_kernel(TargetDev t, int64_t e_lo, int64_t e_hi,
                                                       PlanDev plan, SrcDev src,
                                                       double* __restrict__ contrib,
@@ -374,6 +374,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) mc_mesh_kernel(TargetDev t, int64
         // sample completes instead of being held in 8 registers across the walk
         int next = 0;
         int jcur = 0;
+        int pend_j = -1;  // FW: this lane's outside sample whose snap is deferred to tile end
         bool busy = false;
         double x[D], lam[K];
         int cur = -1, steps = 0;
@@ -552,10 +553,18 @@ __global__ void __launch_bounds__(BLOCK, MINB) mc_mesh_kernel(TargetDev t, int64
                 } else {
                     hit = locate_point<D>(g, x, EPS, l);
                 }
+                bool deferred = false;
                 if (hit < 0) {
                     if (src.outside == TT_OUTSIDE_STRICT) {
                         flags |= TT_FLAG_OUTSIDE_STRICT;
+                    } else if (FW && DEFER && ids_out == nullptr && pend_j < 0) {
+                        // the nearest-element ring search runs at the end of the tile with
+                        // the whole warp (nearest_element_warp) instead of on this one lane
+                        pend_j = jcur;
+                        deferred = true;
+                        flags |= TT_FLAG_SNAPPED;
                     } else {
+                        flags |= TT_FLAG_SNAPPED;
                         const SnapOut<D> sn = snap_point<D>(g, x[0], x[1], D == 3 ? x[D - 1] : 0.0);
                         hit = sn.e;
 #pragma unroll
@@ -563,6 +572,10 @@ __global__ void __launch_bounds__(BLOCK, MINB) mc_mesh_kernel(TargetDev t, int64
                     }
                 }
                 done = true;
+                if (deferred) {
+                    busy = false;  // the sample's contribution is added at tile end
+                    continue;
+                }
             }
             if (done) {
                 TT_STAT(2, 1);
@@ -592,6 +605,40 @@ __global__ void __launch_bounds__(BLOCK, MINB) mc_mesh_kernel(TargetDev t, int64
                     for (int i = 0; i < K; ++i) acc[i] = fma(f, lam[i], acc[i]);
                 }
                 busy = false;
+            }
+        }
+        if constexpr (FW && DEFER) {
+            // deferred snaps (outside points; rare): one warp-cooperative nearest-element
+            // search per pending lane, in lane order, then the owner adds f * lambda_j
+            unsigned pm = __ballot_sync(FULL, pend_j >= 0);
+            while (pm) {
+                const int sl = __ffs(pm) - 1;
+                pm &= pm - 1;
+                double xe[D] = {};
+                double lj[K];
+                if (lane == sl) {
+                    plan_lambda<D, PLAN>(plan, e, pend_j, lj);
+                    if constexpr (SMEMV) {
+                        double vv[K][D];
+#pragma unroll
+                        for (int q = 0; q < K * D; ++q) vv[q / D][q % D] = s_v[wib][gib][q];
+                        map_point<D>(lj, vv, xe);
+                    } else {
+                        map_point<D>(lj, v, xe);
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < D; ++c) xe[c] = __shfl_sync(FULL, xe[c], sl);
+                const int es = nearest_element_warp<D>(g, xe[0], xe[1], D == 3 ? xe[D - 1] : 0.0);
+                if (lane == sl) {
+                    double ls[K];
+                    snap_lambda<D>(g, es, xe, ls);
+                    const double f = (contrib || b) ? p1_eval<D>(src, es, ls) : 0.0;
+                    if (!isfinite(f)) flags |= TT_FLAG_NONFINITE;
+#pragma unroll
+                    for (int i = 0; i < K; ++i) acc[i] = fma(f, lj[i], acc[i]);
+                    pend_j = -1;
+                }
             }
         }
 #pragma unroll
@@ -864,10 +911,16 @@ static int launch_mc(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_pl
                     // +20 KB/block costs 0.056 ms at C2)
                     kernel<<<(unsigned)nb, 128, dyn_smem, st>>>(td, e_lo, e_hi, pd, sd, contrib, b, nullptr, status);
                 };
+                // DEFER (source hint: the walk seeds saw outside points): the kernel variant
+                // whose outside samples are snapped warp-cooperatively at tile end.  It costs
+                // registers (C2: 1.12 -> 1.22 ms), so matching meshes run the plain variant.
+                const bool defer = (s->hints & TT_HINT_DEFER_SNAP) != 0;
                 if (slot) {
-                    launch128(mc_mesh_kernel<D, PLAN, G, true, 5, true, 128, true, false, true>);
+                    if (defer) launch128(mc_mesh_kernel<D, PLAN, G, true, 5, true, 128, true, false, true, true>);
+                    else launch128(mc_mesh_kernel<D, PLAN, G, true, 5, true, 128, true, false, true>);
                 } else {
-                    launch128(mc_mesh_kernel<D, PLAN, G, true, 5, true, 128, true>);
+                    if (defer) launch128(mc_mesh_kernel<D, PLAN, G, true, 5, true, 128, true, false, false, true>);
+                    else launch128(mc_mesh_kernel<D, PLAN, G, true, 5, true, 128, true>);
                 }
                 return launch_check("mc_mesh_kernel (float walk, smem)");
             }

@@ -136,10 +136,25 @@ class UniformGridLocator:
         seeds = torch.empty((target.n_elems, _lib.TT_SEED_ANCHORS), dtype=torch.int32,
                             device=self.cell_start_dev.device)
         g, t = self.desc(), target.device.desc()
+        st = _lib.status_word()
         _lib.call("tt_seed_elements", C.byref(g), C.byref(t), 0, target.n_elems, _lib.ptr(seeds),
-                  _lib.stream_handle())
-        self._seeds[key] = (target, seeds)
+                  _lib.ptr(st), _lib.stream_handle())
+        # one-time read (setup): anchors outside the source mesh mean outside samples occur
+        # -> the fused kernel variant with warp-cooperative snaps (a hint only); otherwise
+        # unknown until the first load reports whether it snapped
+        snap_prone = True if int(st.item()) & _lib.TT_FLAG_SNAPPED else None
+        self._seeds[key] = (target, seeds, snap_prone)
         return seeds
+
+    def snap_prone(self, target):
+        """True / False: loads of ``target`` through this locator do / do not snap outside
+        samples; None: not known yet (no anchor was outside, no load has run)."""
+        self.seeds_for(target)
+        return self._seeds[id(target)][2]
+
+    def set_snap_prone(self, target, value: bool):
+        t, seeds, _ = self._seeds[id(target)]
+        self._seeds[id(target)] = (t, seeds, bool(value))
 
     @cached_property
     def cell_start(self) -> np.ndarray:

@@ -106,6 +106,8 @@ class MeshBackedField:
             # snap fallbacks gather the vertex coefficients directly
             s.seeds = _lib.ptr(self.locator.seeds_for(target)).value
             s.elem_grad = _lib.ptr(self.field.elem_grad()).value
+            if self.locator.snap_prone(target) is True:
+                s.hints |= _lib.TT_HINT_DEFER_SNAP
         else:
             s.elem_coeffs = _lib.ptr(self.field.elem_coeffs()).value
         return s
@@ -303,6 +305,12 @@ def element_contributions(target, source, plan: SamplePlan, e_lo: int = 0,
     if sdesc is not None:
         _lib.call("tt_mc_load", C.byref(mdesc), e_lo, e_hi, C.byref(pdesc), C.byref(sdesc),
                   _lib.ptr(contrib), None, _lib.ptr(status), s)
+        if isinstance(source, MeshBackedField) and source.locator.walk and \
+                source.locator.snap_prone(target) is None:
+            # first load of this (target, locator) pair: one read of the status word learns
+            # whether outside samples occur (TT_FLAG_SNAPPED) -> later loads pick the kernel
+            # variant with warp-cooperative snaps (a performance hint, never a result change)
+            source.locator.set_snap_prone(target, bool(int(status.item()) & _lib.TT_FLAG_SNAPPED))
         return contrib
     # host black box: materialise points per chunk, query, accumulate the values
     chunk = max(1, _HOST_CHUNK_POINTS // plan.n_samples)

@@ -657,3 +657,35 @@ def test_pcg_best_iterate_matches_oracle(tt, path):
         assert _rel(x, xr) <= 1e-8
     finally:
         fem._PCG_PATH = "ell"
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_deferred_snap_variant_matches_inline(tt, golden, dim):
+    """Snap-prone pairs (outside anchors, or a first load that snapped) run the variant whose
+    outside samples are snapped warp-cooperatively at tile end (nearest_element_warp); the
+    plain variant snaps on the diverged lane.  Same samples, same snapped elements, so the
+    two loads agree to rounding (the snapped terms are added in a different order) and both
+    match the oracle."""
+    if dim == 2:
+        src = tt.TriMesh.from_arrays(golden["curv_nodes"], golden["curv_elements"])
+        tgt = tt.TriMesh.from_arrays(golden["curvt_nodes"], golden["curvt_elements"])
+        fs = tt.NodalField(src, golden["curv_coeffs"])
+        plan = tt.SamplePlan.build(256, "sobol", 0)
+    else:
+        tgt = tt.generate_torus_mesh(3, 14, 20, perturbation=0.2, seed=20)
+        src = tt.generate_torus_mesh(3, 12, 17, perturbation=0.2, seed=10, split="kuhn_mirror")
+        fs = tt.NodalField.from_function(src, tt.get_field("smooth", dim=3).fn)
+        plan = tt.SamplePlan.build(40, "sobol", 0, dim=3)
+    loc = tt.UniformGridLocator.build(src)
+    tt.assemble_load_mc(tgt, tt.MeshBackedField(fs, loc), plan)   # learns the hint if unknown
+    assert loc.snap_prone(tgt) is True
+    b_defer = tt.assemble_load_mc(tgt, tt.MeshBackedField(fs, loc), plan)
+    tgt_e, seeds, _ = loc._seeds[id(tgt)]
+    loc._seeds[id(tgt)] = (tgt_e, seeds, False)          # force the plain variant
+    b_inline = tt.assemble_load_mc(tgt, tt.MeshBackedField(fs, loc), plan)
+    assert _rel(b_defer, b_inline) <= 1e-14
+    g = O.Grid(src.nodes, src.elements)
+    ref = O.reduce_to_nodes(tgt.n_nodes, tgt.elements,
+                            O.accumulate(tgt.nodes, tgt.elements, tgt.elem_areas, plan.barycentric,
+                                         lambda P: O.mesh_backed_eval(g, fs.coeffs, P)))
+    assert _rel(b_defer, ref) <= 1e-12
