@@ -563,8 +563,10 @@ __global__ void __launch_bounds__(BLOCK, MINB) mc_mesh_kernel(TargetDev t, int64
                         pend_j = jcur;
                         deferred = true;
                         flags |= TT_FLAG_SNAPPED;
+                        TT_STAT(5, 1);
                     } else {
                         flags |= TT_FLAG_SNAPPED;
+                        TT_STAT(5, 1);
                         const SnapOut<D> sn = snap_point<D>(g, x[0], x[1], D == 3 ? x[D - 1] : 0.0);
                         hit = sn.e;
 #pragma unroll
