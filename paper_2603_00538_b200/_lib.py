@@ -170,8 +170,14 @@ def lib():
 
 
 def stream_handle(stream=None):
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return C.c_void_p(s.cuda_stream)
+    if stream is not None:
+        return C.c_void_p(stream.cuda_stream)
+    # the current stream's raw handle straight from the CUDA context torch keeps: this is
+    # on every ABI call, and torch.cuda.current_stream() builds a Stream object through
+    # device-index normalisation (~5-15 us of host time per call)
+    lib()
+    torch.cuda.init()   # no-op once initialised; the raw query needs the lazy init done
+    return C.c_void_p(torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice()))
 
 
 def check(code: int, what: str = ""):
@@ -208,7 +214,8 @@ def ptr(t) -> C.c_void_p:
 
 def device() -> torch.device:
     lib()
-    return torch.device("cuda", torch.cuda.current_device())
+    torch.cuda.init()
+    return torch.device("cuda", torch._C._cuda_getDevice())
 
 
 def sm_count() -> int:
