@@ -343,8 +343,9 @@ def load_vector(target, source, plan: SamplePlan, e_lo: int = 0, e_hi: int | Non
     e_hi = target.n_elems if e_hi is None else e_hi
     dm = target.device
     status = status if status is not None else _lib.status_word()
-    sdesc, keep = _source_desc(source, target.DIM, target)
-    if deterministic or sdesc is None:
+    # (the deterministic path builds the source descriptor once, inside element_contributions)
+    sdesc, keep = (None, ()) if deterministic else _source_desc(source, target.DIM, target)
+    if sdesc is None:
         contrib = element_contributions(target, source, plan, e_lo, e_hi, status=status)
         b = dm.reduce_nodes(contrib, e_lo, e_hi)
     else:

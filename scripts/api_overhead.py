@@ -42,4 +42,4 @@ if "--profile" in sys.argv:
     for _ in range(200):
         step()
     pr.disable()
-    pstats.Stats(pr).sort_stats("tottime").print_stats(25)
+    pstats.Stats(pr).sort_stats(sys.argv[2] if len(sys.argv) > 2 else "tottime").print_stats(40)
