@@ -108,6 +108,8 @@ typedef struct tt_mesh {
     const double*  nodes;     /* (n_nodes, dim) row-major */
     const int32_t* elems;     /* (n_elems, k) row-major, positively oriented */
     const double*  measure;   /* (n_elems,) |area| / |volume| (may be NULL where unused) */
+    const int32_t* gid;       /* optional (n_elems,) global element ids of a partition mesh:
+                                 the Philox stream counter of element e is gid[e] (NULL = e) */
 } tt_mesh_t;
 
 /* Packed per-element locate record, stride TT_REC_STRIDE(dim) doubles (64 B in 2-D,

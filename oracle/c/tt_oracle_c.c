@@ -9,6 +9,9 @@
  *   nearest + snap       locate.py:97-127, montecarlo.py:58-63
  *   P1 evaluation        fem.py:36-38
  *   accumulate           montecarlo.py:128-131     contrib[e,a] += f/(N p) * lam_a, p = 1/|T|
+ *   grid build           locate.py:42-70           every element into each cell its bbox overlaps,
+ *                                                  ascending ids per cell (counting sort = the
+ *                                                  reference's stable argsort)
  * Compile: gcc -O2 -fopenmp -ffp-contract=off -fPIC -shared (no FMA: bit-exact ids).
  */
 #include <math.h>
@@ -118,7 +121,8 @@ int64_t tto_mc_load_mesh(int dim, const double* t_nodes, const int32_t* t_elems,
                          const int32_t* gdims, const double* glo, const double* ghi,
                          const int64_t* cell_start, const int32_t* cell_elems,
                          const double* binv, const double* origin, const double* centroids,
-                         double eps, double* contrib, int nthreads) {
+                         double eps, double* contrib, int32_t* ids /* (e_hi-e_lo, N) or NULL */,
+                         int nthreads) {
     grid_t g;
     g.dim = dim;
     for (int c = 0; c < 3; ++c) { g.n[c] = gdims[c]; g.lo[c] = glo[c]; g.hi[c] = ghi[c]; }
@@ -158,6 +162,7 @@ int64_t tto_mc_load_mesh(int dim, const double* t_nodes, const int32_t* t_elems,
                     for (int i = 2; i <= dim; ++i) sum = sum + l[i];
                     for (int i = 0; i <= dim; ++i) l[i] = l[i] / sum;
                 }
+                if (ids) ids[(e - e_lo) * N + j] = es;
                 const int32_t* conn = s_elems + (int64_t)es * k;
                 double f = s_coeffs[conn[0]] * l[0];
                 for (int i = 1; i < k; ++i) f = f + s_coeffs[conn[i]] * l[i];
@@ -169,4 +174,57 @@ int64_t tto_mc_load_mesh(int dim, const double* t_nodes, const int32_t* t_elems,
         }
     }
     return bad ? -1 : outside;
+}
+
+/* Uniform-grid build (locate.py:42-70), d = 2, 3: per element, the cell range of its
+ * vertex bbox (trunc((v - lo)/(hi - lo) * n) with C int semantics, clamped; z outermost
+ * last: cell = (ix*n1 + iy)*n2 + iz).  Pass 1 (cell_elems == NULL): counts -> exclusive
+ * scan into cell_start (ncell + 1).  Pass 2: fill in ascending element order, which is the
+ * order the reference's stable argsort leaves in every cell. */
+static void elem_cell_range(int dim, const double* nodes, const int32_t* elems, int64_t e,
+                            const int32_t* n, const double* lo, const double* hi, int* c0, int* c1) {
+    const int k = dim + 1;
+    for (int c = 0; c < 3; ++c) { c0[c] = 0; c1[c] = 0; }
+    for (int c = 0; c < dim; ++c) {
+        double mn = nodes[(int64_t)elems[e * k] * dim + c], mx = mn;
+        for (int i = 1; i < k; ++i) {
+            double v = nodes[(int64_t)elems[e * k + i] * dim + c];
+            mn = v < mn ? v : mn;   /* np.min / np.max (no NaN in valid meshes) */
+            mx = v > mx ? v : mx;
+        }
+        c0[c] = axis_cell(mn, lo[c], hi[c], n[c]);
+        c1[c] = axis_cell(mx, lo[c], hi[c], n[c]);
+    }
+}
+
+int64_t tto_grid_build(int dim, const double* nodes, const int32_t* elems, int64_t E,
+                       const int32_t* gdims, const double* glo, const double* ghi,
+                       int64_t* cell_start, int32_t* cell_elems) {
+    const int32_t n[3] = {gdims[0], gdims[1], dim == 3 ? gdims[2] : 1};
+    const int64_t ncell = (int64_t)n[0] * n[1] * n[2];
+    if (!cell_elems) {
+        for (int64_t c = 0; c <= ncell; ++c) cell_start[c] = 0;
+        for (int64_t e = 0; e < E; ++e) {
+            int c0[3], c1[3];
+            elem_cell_range(dim, nodes, elems, e, n, glo, ghi, c0, c1);
+            for (int ix = c0[0]; ix <= c1[0]; ++ix)
+                for (int iy = c0[1]; iy <= c1[1]; ++iy)
+                    for (int iz = c0[2]; iz <= c1[2]; ++iz)
+                        ++cell_start[((int64_t)ix * n[1] + iy) * n[2] + iz + 1];
+        }
+        for (int64_t c = 0; c < ncell; ++c) cell_start[c + 1] += cell_start[c];
+        return cell_start[ncell];
+    }
+    int64_t* cur = (int64_t*)malloc(sizeof(int64_t) * (size_t)(ncell > 0 ? ncell : 1));
+    for (int64_t c = 0; c < ncell; ++c) cur[c] = cell_start[c];
+    for (int64_t e = 0; e < E; ++e) {
+        int c0[3], c1[3];
+        elem_cell_range(dim, nodes, elems, e, n, glo, ghi, c0, c1);
+        for (int ix = c0[0]; ix <= c1[0]; ++ix)
+            for (int iy = c0[1]; iy <= c1[1]; ++iy)
+                for (int iz = c0[2]; iz <= c1[2]; ++iz)
+                    cell_elems[cur[((int64_t)ix * n[1] + iy) * n[2] + iz]++] = (int32_t)e;
+    }
+    free(cur);
+    return cell_start[ncell];
 }

@@ -34,7 +34,9 @@ def lib():
         _lib = C.CDLL(str(build()))
         _lib.tto_mc_load_mesh.restype = C.c_int64
         _lib.tto_mc_load_mesh.argtypes = [C.c_int] + [C.c_void_p] * 3 + [C.c_int64] * 3 + \
-            [C.c_void_p] * 11 + [C.c_double, C.c_void_p, C.c_int]
+            [C.c_void_p] * 11 + [C.c_double, C.c_void_p, C.c_void_p, C.c_int]
+        _lib.tto_grid_build.restype = C.c_int64
+        _lib.tto_grid_build.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_int64] + [C.c_void_p] * 5
     return _lib
 
 
@@ -42,10 +44,40 @@ def _p(a):
     return a.ctypes.data_as(C.c_void_p)
 
 
+class Grid:
+    """The oracle's uniform-grid locator (``tt_oracle.Grid``'s arrays) with the CSR built
+    by the C counting sort (locate.py:42-70) -- seconds instead of minutes at 10M
+    elements.  Geometry (binv, origin, centroids) is the numpy restatement's."""
+
+    def __init__(self, nodes, elems, dims=None):
+        import tt_oracle as O
+        self.nodes = np.ascontiguousarray(nodes, np.float64)
+        self.elems = np.ascontiguousarray(elems, np.int32)
+        self.dim = self.nodes.shape[1]
+        self.dims = tuple(dims) if dims is not None else O.grid_dims(len(self.elems), self.dim)
+        if len(self.dims) == 2:
+            self.dims = (self.dims[0], self.dims[1], 1)
+        self.lo, self.hi = O.bbox(self.nodes)
+        self.binv, self.origin = O.bary_inverse(self.nodes, self.elems)
+        self.centroids = O.centroids(self.nodes, self.elems)
+        ncell = self.dims[0] * self.dims[1] * self.dims[2]
+        self.cell_start = np.empty(ncell + 1, np.int64)
+        gd = np.array(self.dims, np.int32)
+        lo, hi = np.zeros(3), np.ones(3)
+        lo[:self.dim], hi[:self.dim] = self.lo, self.hi
+        args = (self.dim, _p(self.nodes), _p(self.elems), len(self.elems), _p(gd), _p(lo), _p(hi),
+                _p(self.cell_start))
+        total = lib().tto_grid_build(*args, None)
+        self.cell_elems = np.empty(total, np.int32)
+        lib().tto_grid_build(*args, _p(self.cell_elems))
+
+
 def mc_load_mesh(grid, coeffs, t_nodes, t_elems, t_measure, lam, e_lo=0, e_hi=None,
-                 threads=None, eps=1e-12):
+                 threads=None, eps=1e-12, ids=None):
     """Element contributions (e_hi-e_lo, k) of a mesh-backed source; ``grid`` is an
-    oracle ``tt_oracle.Grid``.  Returns (contrib, n_outside)."""
+    oracle ``tt_oracle.Grid`` (or ``Grid`` above).  Returns (contrib, n_outside);
+    ``ids`` (e_hi-e_lo, N) int32, when given, receives every sample's source element
+    (located, or snapped when outside)."""
     d = grid.dim
     k = d + 1
     e_hi = len(t_elems) if e_hi is None else e_hi
@@ -64,7 +96,7 @@ def mc_load_mesh(grid, coeffs, t_nodes, t_elems, t_measure, lam, e_lo=0, e_hi=No
                                    len(lam), _p(a["lam"]), _p(a["s_elems"]), _p(a["coeffs"]),
                                    _p(a["dims"]), _p(a["lo"]), _p(a["hi"]), _p(a["cs"]), _p(a["ce"]),
                                    _p(a["binv"]), _p(a["origin"]), _p(a["cent"]), eps, _p(out),
-                                   int(threads or os.cpu_count() or 1))
+                                   None if ids is None else _p(ids), int(threads or os.cpu_count() or 1))
     if n_out < 0:
         raise FloatingPointError("SourceEvalFailed: non-finite source value")
     return out, int(n_out)

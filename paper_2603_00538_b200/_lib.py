@@ -47,7 +47,7 @@ def wrec_stride(dim: int) -> int:
 class tt_mesh_t(C.Structure):
     _fields_ = [("dim", C.c_int32), ("reserved", C.c_int32), ("n_nodes", C.c_int64),
                 ("n_elems", C.c_int64), ("nodes", C.c_void_p), ("elems", C.c_void_p),
-                ("measure", C.c_void_p)]
+                ("measure", C.c_void_p), ("gid", C.c_void_p)]
 
 
 class tt_grid_t(C.Structure):
@@ -228,9 +228,9 @@ def status_word() -> torch.Tensor:
     return torch.zeros(1, dtype=torch.int32, device=device())
 
 
-def mesh_desc(dim, n_nodes, n_elems, nodes, elems, measure=None) -> tt_mesh_t:
+def mesh_desc(dim, n_nodes, n_elems, nodes, elems, measure=None, gid=None) -> tt_mesh_t:
     return tt_mesh_t(dim, 0, n_nodes, n_elems, ptr(nodes).value, ptr(elems).value,
-                     ptr(measure).value)
+                     ptr(measure).value, ptr(gid).value)
 
 
 if os.environ.get("TT_B200_EAGER_LOAD"):

@@ -389,177 +389,6 @@ __global__ void __launch_bounds__(BLOCK, MINB) pcg_kernel(PcgArgs a) {
     }
 }
 
-// Chronopoulos-Gear Jacobi PCG (the same Krylov iterates as fem.py:131-152 in exact
-// arithmetic; both inner products of an iteration come from ONE reduction), one grid
-// barrier per iteration.  Loop top (after the barrier): residual test / best iterate on
-// the current r, then beta = g_new/g, alpha = g_new/(delta - beta g_new/alpha_old) and
-// for own rows  s = w + beta s, p = u + beta p, x += alpha p, r -= alpha s, u = dinv r;
-// the SpMV w = A u gathers u at neighbour rows by recomputing it from the previous
-// iteration's r, s, w (double-buffered, so no block races the writers), and the block
-// partials of (r,u), (w,u), (r,r) feed the next barrier.
-struct Cg1Args {
-    int64_t n;
-    const int64_t* __restrict__ rp;
-    const int32_t* __restrict__ ci;
-    const double* __restrict__ v;
-    const double* __restrict__ b;
-    double tol;
-    int64_t maxiter;
-    double* x;
-    double* best_x;
-    double* r[2];
-    double* s[2];
-    double* w[2];
-    double* p;
-    double* dinv;
-    double* part;   // 3 * gridDim.x partial slots
-    tt_pcg_result_t* res;
-};
-
-template <int BLOCK, int MINB>
-__global__ void __launch_bounds__(BLOCK, MINB) pcg_cg1_kernel(Cg1Args a) {
-    cg::grid_group grid = cg::this_grid();
-    __shared__ double sh[3 * 32];
-    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
-    const int nb = gridDim.x;
-    double* partG = a.part;
-    double* partD = a.part + nb;
-    double* partR = a.part + 2 * nb;
-    const int64_t n = a.n;
-    constexpr int kRowsPerWarp = 32 / kRowG;
-    const int64_t warp_id = tid >> 5, nwarps = nthreads >> 5;
-    const int lane = threadIdx.x & 31;
-    const int sub = lane % kRowG;
-
-    // init: dinv, x = 0, p = 0, s_old = 0 (so iteration 0 gives p = u0, s = w0), r0 = b
-    for (int64_t i = tid; i < n; i += nthreads) {
-        double d = 0.0;
-        for (int64_t q = a.rp[i]; q < a.rp[i + 1]; ++q)
-            if (a.ci[q] == i) d = a.v[q];
-        a.dinv[i] = 1.0 / d;
-        a.x[i] = 0.0;
-        a.best_x[i] = 0.0;
-        a.p[i] = 0.0;
-        a.r[0][i] = a.b[i];
-        a.s[0][i] = 0.0;
-    }
-    grid.sync();
-    // w0 = A u0 with u0 = dinv b; partials (r0,u0), (w0,u0), (r0,r0)
-    {
-        double pg = 0.0, pd = 0.0, pr = 0.0;
-        for (int64_t w0 = warp_id * kRowsPerWarp; w0 < n; w0 += nwarps * kRowsPerWarp) {
-            const int64_t i = w0 + lane / kRowG;
-            double acc = 0.0;
-            if (i < n) {
-                const double* __restrict__ dv = a.dinv;
-                const double* __restrict__ bb = a.b;
-                acc = row_dot(a.rp[i], a.rp[i + 1], sub, a.ci, a.v, [&](int c) { return dv[c] * bb[c]; });
-            }
-#pragma unroll
-            for (int off = kRowG / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-            if (i < n && sub == 0) {
-                const double ri = a.b[i], ui = a.dinv[i] * ri;
-                a.w[0][i] = acc;
-                pg += ri * ui;
-                pd += acc * ui;
-                pr += ri * ri;
-            }
-        }
-        {
-            double v[3] = {pg, pd, pr};
-            block_sums<3>(v, sh);
-            if (threadIdx.x == 0) { partG[blockIdx.x] = v[0]; partD[blockIdx.x] = v[1]; partR[blockIdx.x] = v[2]; }
-        }
-    }
-    grid.sync();
-    double tot[3];
-    grid_totals<3>(partG, sh, tot);  // partD, partR follow partG
-    double gamma = tot[0];
-    double delta = tot[1];
-    const double bnorm = sqrt(tot[2]);
-    if (bnorm == 0.0) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
-            a.res->iterations = 0; a.res->residual = 0.0; a.res->best_residual = 0.0;
-            a.res->converged = 1; a.res->zero_rhs = 1;
-        }
-        return;
-    }
-    double best = bnorm / bnorm;  // ||r0|| / ||b||  (fem.py:136)
-    double res = best;
-    double alpha = gamma / delta, beta = 0.0;
-    int cur = 0;
-    for (int64_t it = 0; it < a.maxiter; ++it) {
-        const int nxt = cur ^ 1;
-        const double* __restrict__ r_o = a.r[cur];
-        const double* __restrict__ s_o = a.s[cur];
-        const double* __restrict__ w_o = a.w[cur];
-        double* r_n = a.r[nxt];
-        double* s_n = a.s[nxt];
-        double* w_n = a.w[nxt];
-        double pg = 0.0, pd = 0.0, pr = 0.0;
-        for (int64_t w0 = warp_id * kRowsPerWarp; w0 < n; w0 += nwarps * kRowsPerWarp) {
-            const int64_t i = w0 + lane / kRowG;
-            double acc = 0.0;
-            if (i < n) {
-                const double* __restrict__ dv = a.dinv;
-                acc = row_dot(a.rp[i], a.rp[i + 1], sub, a.ci, a.v, [&](int c) {
-                    return dv[c] * (r_o[c] - alpha * (w_o[c] + beta * s_o[c]));
-                });
-            }
-#pragma unroll
-            for (int off = kRowG / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-            if (i < n && sub == 0) {
-                const double si = w_o[i] + beta * s_o[i];
-                const double ri = r_o[i] - alpha * si;
-                const double ui = a.dinv[i] * ri;
-                s_n[i] = si;
-                r_n[i] = ri;
-                w_n[i] = acc;
-                pg += ri * ui;
-                pd += acc * ui;
-                pr += ri * ri;
-            }
-        }
-        // x, p for own rows (p = u_old + beta p, x += alpha p): u_old = dinv r_old
-        for (int64_t i = tid; i < n; i += nthreads) {
-            const double pi = a.dinv[i] * r_o[i] + beta * a.p[i];
-            a.p[i] = pi;
-            a.x[i] += alpha * pi;
-        }
-        {
-            double v[3] = {pg, pd, pr};
-            block_sums<3>(v, sh);
-            if (threadIdx.x == 0) { partG[blockIdx.x] = v[0]; partD[blockIdx.x] = v[1]; partR[blockIdx.x] = v[2]; }
-        }
-        grid.sync();
-        cur = nxt;
-        grid_totals<3>(partG, sh, tot);
-        const double g_new = tot[0];
-        const double d_new = tot[1];
-        res = sqrt(tot[2]) / bnorm;
-        if (res < best) {
-            best = res;
-            for (int64_t i = tid; i < n; i += nthreads) a.best_x[i] = a.x[i];
-        }
-        if (res <= a.tol) {
-            if (blockIdx.x == 0 && threadIdx.x == 0) {
-                a.res->iterations = it + 1; a.res->residual = res; a.res->best_residual = best;
-                a.res->converged = 1; a.res->zero_rhs = 0;
-            }
-            return;
-        }
-        beta = g_new / gamma;
-        alpha = g_new / (d_new - beta * g_new / alpha);
-        gamma = g_new;
-        delta = d_new;
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        a.res->iterations = a.maxiter; a.res->residual = res; a.res->best_residual = best;
-        a.res->converged = 0; a.res->zero_rhs = 0;
-    }
-}
-
 // ---------------------------------------------------------------- ELL variant of the PCG
 // Fixed-width rows (width W = 16: every row of these P1 mass matrices has <= 16 entries,
 // padding = (row, 0.0)), diagonal stored separately.  4 lanes per row; lane `sub` owns
@@ -607,16 +436,6 @@ struct EllArgs {
     int64_t slab_rows;  // SLAB: rows per block held in shared memory (the rest read from L2)
 };
 
-template <class Col>
-__device__ __forceinline__ double ell_row16(const int32_t* __restrict__ ec, const double* __restrict__ ev,
-                                           int64_t i, int sub, Col col) {
-    const int4 c = __ldg(reinterpret_cast<const int4*>(ec + i * 16) + sub);
-    const double2 a0 = __ldg(reinterpret_cast<const double2*>(ev + i * 16 + 4 * sub));
-    const double2 a1 = __ldg(reinterpret_cast<const double2*>(ev + i * 16 + 4 * sub) + 1);
-    const double x0 = col(c.x), x1 = col(c.y), x2 = col(c.z), x3 = col(c.w);
-    return fma(a1.y, x3, fma(a1.x, x2, fma(a0.y, x1, a0.x * x0)));
-}
-
 // W/8 lanes per row (W = 16: 2 lanes; W = 8, the 2-D matrices: 1 lane): lane `sub` owns
 // entries [8 sub, 8 sub + 8) -> 16 independent gathers in flight per lane and half the
 // rows-per-group dependency chain of the 4-lane layout
@@ -624,16 +443,9 @@ template <int W, class Col>
 __device__ __forceinline__ double ell_row8(const int32_t* __restrict__ ec, const double* __restrict__ ev,
                                            int64_t i, int sub, Col col) {
     const int4* cq = reinterpret_cast<const int4*>(ec + i * W) + 2 * sub;
-#ifdef TT_ELL_STREAM
-    // matrix rows stream through L2 evict-first, keeping the PCG vectors L2-resident
-    const int4 c0 = __ldcs(cq), c1 = __ldcs(cq + 1);
-    const double2* vq = reinterpret_cast<const double2*>(ev + i * W + 8 * sub);
-    const double2 a0 = __ldcs(vq), a1 = __ldcs(vq + 1), a2 = __ldcs(vq + 2), a3 = __ldcs(vq + 3);
-#else
     const int4 c0 = __ldg(cq), c1 = __ldg(cq + 1);
     const double2* vq = reinterpret_cast<const double2*>(ev + i * W + 8 * sub);
     const double2 a0 = __ldg(vq), a1 = __ldg(vq + 1), a2 = __ldg(vq + 2), a3 = __ldg(vq + 3);
-#endif
     const double x0 = col(c0.x), x1 = col(c0.y), x2 = col(c0.z), x3 = col(c0.w);
     const double x4 = col(c1.x), x5 = col(c1.y), x6 = col(c1.z), x7 = col(c1.w);
     const double s0 = fma(a1.y, x3, fma(a1.x, x2, fma(a0.y, x1, a0.x * x0)));
@@ -667,10 +479,10 @@ __device__ __forceinline__ double slab_row(const uint4* __restrict__ ch, int64_t
     return s0 + s1;
 }
 
-template <int BLOCK, int MINB, int LPR, bool CONTIG = false, bool SLAB = false, int W = 16>
+// W/8 lanes per row; every block owns a contiguous row range (neighbour gathers hit its L1).
+template <int BLOCK, int MINB, int W, bool SLAB>
 __global__ void __launch_bounds__(BLOCK, MINB) pcg_ell_kernel(EllArgs a) {
-    static_assert(!SLAB || (LPR == W / 8 && CONTIG), "the slab layout is W/8 lanes per row, contiguous rows");
-    static_assert(LPR == W / 8 || (W == 16 && LPR == 4), "lanes per row");
+    constexpr int LPR = W / 8;
     cg::grid_group grid = cg::this_grid();
     __shared__ double sh[3 * 32];
     extern __shared__ uint4 slab[];  // SLAB: (rows of this block) x 2 chunks x 5 uint4
@@ -735,7 +547,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) pcg_ell_kernel(EllArgs a) {
     double res = best;
     double beta = 0.0;
     constexpr int RPW = 32 / LPR;  // rows per warp
-    const int64_t group = tid / LPR, ngroups = nthreads / LPR;
+    const int64_t group = tid / LPR;
     const int sub = threadIdx.x & (LPR - 1);
     int xc = 0, xbi = 0;  // current / best iterate buffers (settle_iterates)
     double* p_old = a.p0;
@@ -743,22 +555,19 @@ __global__ void __launch_bounds__(BLOCK, MINB) pcg_ell_kernel(EllArgs a) {
     for (int64_t it = 0; it < a.maxiter; ++it) {
         PCG_MARK(it, 0);
         double pap = 0.0;
-        // rows are processed by 4-lane groups; the loop trip count is uniform per warp
-        // CONTIG: every block owns a contiguous row range (neighbour gathers hit its L1)
-        const int64_t rpb = CONTIG ? (n + nb - 1) / nb : 0;
-        const int64_t r_end = CONTIG ? min(n, (blockIdx.x + 1) * rpb) : n;
-        const int64_t g_first = CONTIG ? blockIdx.x * rpb + (threadIdx.x / LPR & ~(RPW - 1)) : (group & ~(int64_t)(RPW - 1));
-        const int64_t g_step = CONTIG ? BLOCK / LPR : ngroups;
-        for (int64_t i0 = g_first; i0 < (CONTIG ? blockIdx.x * rpb + rpb : n); i0 += g_step) {
+        // rows are processed by LPR-lane groups; the loop trip count is uniform per warp
+        const int64_t rpb = (n + nb - 1) / nb;
+        const int64_t r_end = min(n, (blockIdx.x + 1) * rpb);
+        const int64_t g_first = blockIdx.x * rpb + (threadIdx.x / LPR & ~(RPW - 1));
+        for (int64_t i0 = g_first; i0 < blockIdx.x * rpb + rpb; i0 += BLOCK / LPR) {
             const int64_t i = i0 + (group & (RPW - 1));
             double s = 0.0;
             if (i < r_end) {
                 const double* __restrict__ z = a.z;
                 const double* __restrict__ po = p_old;
                 const auto col = [&](int c) { return z[c] + beta * po[c]; };
-                const int64_t li = i - blockIdx.x * rpb;  // (CONTIG) row within the block
+                const int64_t li = i - blockIdx.x * rpb;  // row within the block
                 if (SLAB && li < a.slab_rows) s = slab_row(slab + (li * LPR + sub) * 5, i, z, po, beta);
-                else if constexpr (LPR == 4) s = ell_row16(a.ec, a.ev, i, sub, col);
                 else s = ell_row8<W>(a.ec, a.ev, i, sub, col);
             }
 #pragma unroll
@@ -868,26 +677,12 @@ __global__ void sum_parts_kernel(int nparts, const double* __restrict__ part, do
 }
 
 template <int BLOCK, int MINB>
-static int cg1_launch(Cg1Args& a, int64_t n, cudaStream_t st) {
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg_cg1_kernel<BLOCK, MINB>, BLOCK, 0);
-    if (per_sm < 1) per_sm = 1;
-    int64_t maxb = (int64_t)sm_count() * per_sm;
-    int64_t need = (n * kRowG + BLOCK - 1) / BLOCK;
-    if (need < 1) need = 1;
-    int blocks = (int)(need < maxb ? need : maxb);
-    if (blocks > 148 * 32) blocks = 148 * 32;
-    void* args[] = {&a};
-    cudaError_t e = cudaLaunchCooperativeKernel((void*)pcg_cg1_kernel<BLOCK, MINB>, dim3(blocks),
-                                                dim3(BLOCK), args, 0, st);
-    return cuda_status(e, "pcg_cg1_kernel (cooperative launch)");
-}
-
-template <int BLOCK, int MINB>
 static int pcg_launch(PcgArgs& a, int64_t n, cudaStream_t st) {
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg_kernel<BLOCK, MINB>, BLOCK, 0);
-    if (per_sm < 1) per_sm = 1;
+    static const int per_sm = [] {
+        int per = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, pcg_kernel<BLOCK, MINB>, BLOCK, 0);
+        return per < 1 ? 1 : per;
+    }();
     int64_t maxb = (int64_t)sm_count() * per_sm;
     int64_t need = (n * kRowG + BLOCK - 1) / BLOCK;
     if (need < 1) need = 1;
@@ -959,20 +754,6 @@ extern "C" int tt_pcg(int64_t n, const int64_t* rp, const int32_t* ci, const dou
         set_error("tt_pcg: bad size");
         return TT_ERR_INVALID_PARAMETER;
     }
-    // algorithm: 0 (default) the textbook recurrence of fem.py:131-152, two barriers per
-    //            iteration; 1 Chronopoulos-Gear, one barrier but 4 gathers per nonzero
-    //            (measured slower on B200: a grid barrier costs ~1.2 us, the gathers more)
-    static int algo = [] { const char* v = getenv("TT_PCG_ALGO"); return v ? atoi(v) : 0; }();
-    if (algo == 1) {
-        Cg1Args c;
-        c.n = n; c.rp = rp; c.ci = ci; c.v = v; c.b = b; c.tol = tol; c.maxiter = maxiter;
-        c.x = x; c.best_x = best_x;
-        c.r[0] = work; c.r[1] = work + n; c.s[0] = work + 2 * n; c.s[1] = work + 3 * n;
-        c.w[0] = work + 4 * n; c.w[1] = work + 5 * n; c.p = work + 6 * n; c.dinv = work + 7 * n;
-        c.part = work + 8 * n;
-        c.res = result;
-        return cg1_launch<512, 2>(c, n, as_stream(stream));
-    }
     PcgArgs a;
     a.n = n; a.rp = rp; a.ci = ci; a.v = v; a.b = b; a.tol = tol; a.maxiter = maxiter;
     a.x = x; a.best_x = best_x;
@@ -980,11 +761,8 @@ extern "C" int tt_pcg(int64_t n, const int64_t* rp, const int32_t* ci, const dou
     a.dinv = work + 5 * n;
     a.part = work + 6 * n;
     a.res = result;
-    // block shape: 2 x 512 threads per SM by default (measured best of 256x4 / 512x2 / 1024x1)
-    static int variant = [] { const char* v = getenv("TT_PCG_VARIANT"); return v ? atoi(v) : 1; }();
-    if (variant == 0) return pcg_launch<256, 4>(a, n, as_stream(stream));
-    if (variant == 1) return pcg_launch<512, 2>(a, n, as_stream(stream));
-    return pcg_launch<1024, 1>(a, n, as_stream(stream));
+    // block shape: 2 x 512 threads per SM (measured best of 256x4 / 512x2 / 1024x1)
+    return pcg_launch<512, 2>(a, n, as_stream(stream));
 }
 
 extern "C" int tt_spmv(int64_t n, const int64_t* rp, const int32_t* ci, const double* v,
@@ -1037,6 +815,12 @@ extern "C" int tt_csr_to_ell(int64_t n, const int64_t* rp, const int32_t* ci, co
     return launch_check("csr_to_ell_kernel");
 }
 
+static int blocks_per_sm(const void* fn, int block, size_t smem) {
+    int per = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, block, smem);
+    return per < 1 ? 1 : per;
+}
+
 static bool ell_args(EllArgs& a, int64_t n, int width, const int32_t* ell_cols, const double* ell_vals,
                      const double* diag, const double* b, double tol, int64_t maxiter, double* x,
                      double* best_x, double* work, tt_pcg_result_t* result, const char* who) {
@@ -1060,25 +844,15 @@ extern "C" int tt_pcg_ell(int64_t n, int width, const int32_t* ell_cols, const d
     EllArgs a;
     if (!ell_args(a, n, width, ell_cols, ell_vals, diag, b, tol, maxiter, x, best_x, work, result, "tt_pcg_ell"))
         return TT_ERR_INVALID_PARAMETER;
-    // SpMV shape (W = 16): lanes per row (TT_PCG_ELL_LPR = 2 | 4) and contiguous per-block
-    // row ranges (TT_PCG_ELL_CONTIG = 1 | 0).  Measured on the C2 mass matrix (175,616 rows,
-    // 23 iterations): 2 lanes + contiguous 0.357 ms, 4 lanes + contiguous 0.373 ms,
-    // 4 lanes + grid-stride 0.377 ms, 2 lanes + grid-stride 0.404 ms.  W = 8: 1 lane per row.
-    static const int lpr_env = [] {
-        const char* v = getenv("TT_PCG_ELL_LPR");
-        return (v && atoi(v) == 4) ? 4 : 2;
-    }();
-    static const bool contig = [] {
-        const char* v = getenv("TT_PCG_ELL_CONTIG");
-        return !(v && atoi(v) == 0);
-    }();
-    const int lpr = width == 8 ? 1 : lpr_env;
-    const void* fn = width == 8 ? (const void*)pcg_ell_kernel<512, 2, 1, true, false, 8>
-                   : lpr == 4 ? (contig ? (const void*)pcg_ell_kernel<512, 2, 4, true> : (const void*)pcg_ell_kernel<512, 2, 4>)
-                              : (contig ? (const void*)pcg_ell_kernel<512, 2, 2, true> : (const void*)pcg_ell_kernel<512, 2, 2>);
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 512, 0);
-    if (per_sm < 1) per_sm = 1;
+    // SpMV shape: W/8 lanes per row, every block a contiguous row range.  Measured on the C2
+    // mass matrix (175,616 rows, 23 iterations): 2 lanes + contiguous 0.357 ms, 4 lanes +
+    // contiguous 0.373 ms, 4 lanes + grid-stride 0.377 ms, 2 lanes + grid-stride 0.404 ms.
+    const int lpr = width / 8;
+    const void* fn = width == 8 ? (const void*)pcg_ell_kernel<512, 2, 8, false>
+                                : (const void*)pcg_ell_kernel<512, 2, 16, false>;
+    static const int per8 = blocks_per_sm((const void*)pcg_ell_kernel<512, 2, 8, false>, 512, 0);
+    static const int per16 = blocks_per_sm((const void*)pcg_ell_kernel<512, 2, 16, false>, 512, 0);
+    const int per_sm = width == 8 ? per8 : per16;
     int64_t maxb = (int64_t)sm_count() * per_sm;
     int64_t need = (n * lpr + 511) / 512;
     if (need < 1) need = 1;
@@ -1097,21 +871,17 @@ extern "C" int tt_pcg_ell_slab(int64_t n, int width, const int32_t* ell_cols, co
                   "tt_pcg_ell_slab"))
         return TT_ERR_INVALID_PARAMETER;
     const int lpr = width / 8;  // lanes per row = 80-byte chunks per row
-    const void* fn = width == 8 ? (const void*)pcg_ell_kernel<512, 2, 1, true, true, 8>
-                                : (const void*)pcg_ell_kernel<512, 2, 2, true, true, 16>;
+    const void* fn = width == 8 ? (const void*)pcg_ell_kernel<512, 2, 8, true>
+                                : (const void*)pcg_ell_kernel<512, 2, 16, true>;
     int dev = 0, max_optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     const int sms = sm_count();
-    // rows that must be slab-resident for the slab to pay (TT_PCG_SLAB_MIN_FRAC, default 1/2):
-    // the rest of a block's rows stream from L2/HBM as in tt_pcg_ell, with the L1 the slab
-    // took.  Measured per 3-D solve, slab vs L2 kernel: 59 % on chip (357,911 rows) 0.565 vs
-    // 0.691 ms; 40 % (531,441) 1.20 vs 1.04; 28 % (753,571) 1.83 vs 1.25; C1 (2-D, 85 %)
-    // 0.36 vs 0.43
-    static const double min_frac = [] {
-        const char* v = getenv("TT_PCG_SLAB_MIN_FRAC");
-        return v ? atof(v) : 0.5;
-    }();
+    // rows that must be slab-resident for the slab to pay (1/2): the rest of a block's rows
+    // stream from L2/HBM as in tt_pcg_ell, with the L1 the slab took.  Measured per 3-D
+    // solve, slab vs L2 kernel: 59 % on chip (357,911 rows) 0.565 vs 0.691 ms; 40 %
+    // (531,441) 1.20 vs 1.04; 28 % (753,571) 1.83 vs 1.25; C1 (2-D, 85 %) 0.36 vs 0.43
+    constexpr double min_frac = 0.5;
     // 2 blocks per SM (the 2 x 512 shape of tt_pcg_ell), else 1 with twice the rows.  With
     // 2 per SM the block count and row ranges are tt_pcg_ell's, so the partial sums -- and
     // the iterates -- are bitwise the same

@@ -151,7 +151,14 @@ struct TargetDev {
     const double* __restrict__ nodes;
     const int32_t* __restrict__ elems;
     const double* __restrict__ measure;
+    const int32_t* __restrict__ gid;  // optional global element ids (Philox counters)
 };
+
+// Philox stream counter of element e: its global id (a rank's partition mesh numbers its
+// elements locally; tt_mesh_t.gid maps them back), so streams are partition independent
+__device__ __forceinline__ int64_t stream_id(const int32_t* __restrict__ gid, int64_t e) {
+    return gid ? (int64_t)__ldg(gid + e) : e;
+}
 
 struct PlanDev {
     int64_t n;
@@ -206,7 +213,7 @@ __global__ void __launch_bounds__(256) mc_load_kernel(TargetDev t, int64_t e_lo,
 #pragma unroll
                     for (int i = 0; i < K; ++i) lam[i] = __ldg(plan.lam + j * K + i);
                 } else {
-                    philox_lambda<D>(plan.seed, e, j, lam);
+                    philox_lambda<D>(plan.seed, stream_id(t.gid, e), j, lam);
                 }
                 double x[D];
                 map_point<D>(lam, v, x);
@@ -237,7 +244,8 @@ __global__ void __launch_bounds__(256) mc_load_kernel(TargetDev t, int64_t e_lo,
 }
 
 template <int D, int PLAN>
-__device__ __forceinline__ void plan_lambda(const PlanDev& plan, int64_t e, int64_t j, double* lam) {
+__device__ __forceinline__ void plan_lambda(const PlanDev& plan, const int32_t* gid, int64_t e, int64_t j,
+                                            double* lam) {
     constexpr int K = D + 1;
     if constexpr (PLAN == TT_PLAN_SHARED) {
         if constexpr (D == 3) {
@@ -249,7 +257,7 @@ __device__ __forceinline__ void plan_lambda(const PlanDev& plan, int64_t e, int6
             for (int i = 0; i < K; ++i) lam[i] = __ldg(plan.lam + j * K + i);
         }
     } else {
-        philox_lambda<D>(plan.seed, e, j, lam);
+        philox_lambda<D>(plan.seed, stream_id(gid, e), j, lam);
     }
 }
 
@@ -302,9 +310,20 @@ __device__ __forceinline__ int seed_slot_nearest(const double* lam) {
 // many steps individual samples need; the assignment is a deterministic function of the
 // data, so results are bitwise reproducible.  Identical ids/lambdas as the reference scan
 // (certified walk, see locate_walk in tt_common.cuh).
-template <int D, int PLAN, int G, bool SPEC, int MINB, bool FW = false, int BLOCK = 256,
-          bool SMEMV = false, bool RL = false, bool SLOT = false, bool DEFER = false>
-__global__ void __launch_bounds__(BLOCK, MINB) mc_mesh_kernel(TargetDev t, int64_t e_lo, int64_t e_hi,
+//
+// Launch shape: 128-thread blocks, 5 resident per SM at <= 96 registers,
+// each element's vertices and walk seeds in shared memory, one wave of blocks (a
+// persistent tile loop).  Walk steps read the compact 80 B float record (wrec) and
+// evaluate f from the element's gradient record (egrad), loaded speculatively with it.
+//   SLOT  (shared plans, N <= kSlotCap): per-block table of each sample's nearest walk
+//         anchor (N bytes of dynamic shared memory), built once per block.
+//   DEFER (pairs whose seeds saw outside anchors): an outside sample's nearest-element
+//         search is parked and run warp-cooperatively at the end of the tile.
+constexpr int kMcBlock = 128;
+constexpr int kMcMinBlocks = 5;
+
+template <int D, int PLAN, int G, bool SLOT, bool DEFER>
+__global__ void __launch_bounds__(kMcBlock, kMcMinBlocks) mc_mesh_kernel(TargetDev t, int64_t e_lo, int64_t e_hi,
                                                       PlanDev plan, SrcDev src,
                                                       double* __restrict__ contrib,
                                                       double* __restrict__ b,
@@ -312,6 +331,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) mc_mesh_kernel(TargetDev t, int64
                                                       int32_t* __restrict__ status) {
     constexpr int K = D + 1;
     constexpr int EPW = 32 / G;
+    constexpr int NW = kMcBlock / 32;
     constexpr double EPS = 1e-12;
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
@@ -323,20 +343,21 @@ __global__ void __launch_bounds__(BLOCK, MINB) mc_mesh_kernel(TargetDev t, int64
     const int64_t n_el = e_hi - e_lo;
     const int64_t N = plan.n;
     const GridDev& g = src.grid;
-    const bool walk = g.walk && src.seeds;
+    const bool walk = g.walk && src.seeds && g.wrec;
     int flags = 0;
-    // SLOT (shared plans, N <= kSlotCap, walk on): the seed slot depends on the sample
-    // index only -> one table per block, built once (the grid is one wave of blocks)
-    constexpr bool USE_SLOT = SLOT && SMEMV && PLAN == TT_PLAN_SHARED;
+    constexpr bool USE_SLOT = SLOT && PLAN == TT_PLAN_SHARED;
     extern __shared__ int8_t s_slot[];  // N bytes (launch: dynamic shared memory)
     if constexpr (USE_SLOT) {
-        for (int64_t j = threadIdx.x; j < N; j += BLOCK) {
+        for (int64_t j = threadIdx.x; j < N; j += kMcBlock) {
             double lj[K];
-            plan_lambda<D, PLAN>(plan, 0, j, lj);
+            plan_lambda<D, PLAN>(plan, t.gid, 0, j, lj);
             s_slot[j] = (int8_t)seed_slot_nearest<D>(lj);
         }
         __syncthreads();
     }
+    __shared__ double s_v[NW][EPW][K * D];
+    __shared__ int s_seed[NW][EPW][kSeeds];
+    const int wib = threadIdx.x >> 5, gib = lane / G;
 
     for (int64_t tile = warp; tile * EPW < n_el; tile += nwarps) {
         const int64_t le = tile * EPW + lane / G;
@@ -345,36 +366,22 @@ __global__ void __launch_bounds__(BLOCK, MINB) mc_mesh_kernel(TargetDev t, int64
         double acc[K];
 #pragma unroll
         for (int i = 0; i < K; ++i) acc[i] = 0.0;
-        if constexpr (SMEMV) __syncwarp();
-        // SMEMV: the element's vertices and walk seeds live in shared memory (read at each
-        // sample start) instead of 24 + 5 registers -> more resident warps per SM
-        constexpr int NW = BLOCK / 32;
-        __shared__ double s_v[SMEMV ? NW : 1][SMEMV ? EPW : 1][SMEMV ? K * D : 1];
-        __shared__ int s_seed[SMEMV ? NW : 1][SMEMV ? EPW : 1][SMEMV ? kSeeds : 1];
-        const int wib = threadIdx.x >> 5, gib = lane / G;
-        double v[SMEMV ? 1 : K][D];
-        int seed[SMEMV ? 1 : K + 1];
-        if constexpr (SMEMV) {
-            if (active) {
-                for (int q = sub_lane; q < K * D; q += G)
-                    s_v[wib][gib][q] = __ldg(t.nodes + (int64_t)__ldg(t.elems + e * K + q / D) * D + q % D);
-                if (walk)
-                    for (int q = sub_lane; q < (USE_SLOT ? kSeeds : K + 1); q += G)
-                        s_seed[wib][gib][q] = __ldg(src.seeds + e * kSeeds + q);
-            }
-            __syncwarp();
-        } else if (active) {
-            load_elem<D>(t, e, v);
-            if (walk) {
-#pragma unroll
-                for (int i = 0; i <= K; ++i) seed[i] = __ldg(src.seeds + e * kSeeds + i);
-            }
+        __syncwarp();
+        if (active) {
+            for (int q = sub_lane; q < K * D; q += G)
+                s_v[wib][gib][q] = __ldg(t.nodes + (int64_t)__ldg(t.elems + e * K + q / D) * D + q % D);
+            if (walk)
+                for (int q = sub_lane; q < (USE_SLOT ? kSeeds : K + 1); q += G)
+                    s_seed[wib][gib][q] = __ldg(src.seeds + e * kSeeds + q);
         }
-        // RL (shared plans): lambda_j is re-read from the L1-resident plan table when the
-        // sample completes instead of being held in 8 registers across the walk
+        __syncwarp();
+        const auto vertices = [&](double (*vv)[D]) {
+#pragma unroll
+            for (int q = 0; q < K * D; ++q) vv[q / D][q % D] = s_v[wib][gib][q];
+        };
         int next = 0;
         int jcur = 0;
-        int pend_j = -1;  // FW: this lane's outside sample whose snap is deferred to tile end
+        int pend_j = -1;  // DEFER: this lane's outside sample whose snap runs at tile end
         bool busy = false;
         double x[D], lam[K];
         int cur = -1, steps = 0;
@@ -384,35 +391,16 @@ __global__ void __launch_bounds__(BLOCK, MINB) mc_mesh_kernel(TargetDev t, int64
             if (want) {
                 const int j = next + __popc(m & lt);
                 if (j < N) {
-                    plan_lambda<D, PLAN>(plan, e, j, lam);
-                    if constexpr (SMEMV) {
-                        double vv[K][D];
-#pragma unroll
-                        for (int q = 0; q < K * D; ++q) vv[q / D][q % D] = s_v[wib][gib][q];
-                        if constexpr (FW) map_point_fma<D>(lam, vv, x);
-                        else map_point<D>(lam, vv, x);
-                    } else {
-                        if constexpr (FW) map_point_fma<D>(lam, v, x);
-                        else map_point<D>(lam, v, x);
-                    }
+                    plan_lambda<D, PLAN>(plan, t.gid, e, j, lam);
+                    double vv[K][D];
+                    vertices(vv);
+                    map_point_fma<D>(lam, vv, x);
                     cur = -1;
                     if (walk) {
-                        int imax = 0;
-                        double lmax = lam[0];
-                        if constexpr (SMEMV) {
-                            int slot;
-                            if constexpr (USE_SLOT) slot = s_slot[j];
-                            else slot = seed_slot<K>(lam);
-                            cur = s_seed[wib][gib][slot];
-                        } else {
-#pragma unroll
-                            for (int i = 1; i < K; ++i)
-                                if (lam[i] > lmax) { lmax = lam[i]; imax = i; }
-                            cur = seed[0];
-#pragma unroll
-                            for (int i = 0; i < K; ++i)
-                                if (lmax > 0.45 && imax == i) cur = seed[1 + i];
-                        }
+                        int slot;
+                        if constexpr (USE_SLOT) slot = s_slot[j];
+                        else slot = seed_slot<K>(lam);
+                        cur = s_seed[wib][gib][slot];
                     }
                     steps = 0;
                     jcur = j;
@@ -430,134 +418,82 @@ __global__ void __launch_bounds__(BLOCK, MINB) mc_mesh_kernel(TargetDev t, int64
             if (!busy) continue;
             double l[K];
             int hit = -1;
-            int fb = -1;  // FW: element whose float test fell in its uncertainty band
+            int fb = -1;  // element whose float test fell in its uncertainty band
             bool done = false;
             bool fw_hit = false;
             double fw_f = 0.0;
-            double2 pc0 = make_double2(0.0, 0.0), pc1 = make_double2(0.0, 0.0);
-            if constexpr (FW) {
-                if (cur >= 0 && steps < 12) {
-                    // compact float walk step: exact ids via a margin that bounds the float
-                    // evaluation error (tt_grid.cu walk_prep_kernel); f from the element's
-                    // gradient record: f = c_last + g . (x - o), accurate to a few ulps
-                    WRec<D> w;
-                    load_wrec<D>(g.wrec, cur, w);
-                    if (SPEC && src.egrad) {  // speculative: the gradient record of the element tested
-                        const double2* q = reinterpret_cast<const double2*>(src.egrad + (int64_t)cur * 4);
-                        pc0 = __ldg(q);
-                        pc1 = __ldg(q + 1);
-                    }
-                    double r[D];
-                    float rf[D];
-#pragma unroll
-                    for (int c = 0; c < D; ++c) { r[c] = x[c] - w.o[c]; rf[c] = __double2float_rn(r[c]); }
-                    float lf[K];
-#pragma unroll
-                    for (int i = 0; i < D; ++i) {
-                        float a = w.b[i][0] * rf[0];
-#pragma unroll
-                        for (int c = 1; c < D; ++c) a = fmaf(w.b[i][c], rf[c], a);
-                        lf[i] = a;
-                    }
-                    float last = 1.0f - lf[0] - lf[1];
-                    if constexpr (D == 3) last -= lf[2];
-                    lf[D] = last;
-                    int imin = 0;
-                    float lmin = lf[0];
-#pragma unroll
-                    for (int i = 1; i <= D; ++i)
-                        if (lf[i] < lmin) { lmin = lf[i]; imin = i; }
-                    if (lmin >= w.tau) {
-                        hit = cur;
-                        done = true;
-                        fw_hit = true;
-                        if (!SPEC) {  // load the gradient record of the hit only
-                            const double2* q = reinterpret_cast<const double2*>(src.egrad + (int64_t)cur * 4);
-                            pc0 = __ldg(q);
-                            pc1 = __ldg(q + 1);
-                        }
-                        const double gv[4] = {pc0.x, pc0.y, pc1.x, pc1.y};
-                        double f = gv[D];
-#pragma unroll
-                        for (int c = 0; c < D; ++c) f = fma(gv[c], r[c], f);
-                        fw_f = f;
-                    } else if (lmin > -w.tau) {
-                        fb = cur;  // within the uncertainty band of a facet: exact double walk
-                        cur = -1;
-                    } else {
-                        int nb = w.nbr[0];
-#pragma unroll
-                        for (int i = 1; i <= D; ++i)
-                            if (imin == i) nb = w.nbr[i];
-                        cur = nb;
-                        ++steps;
-                        TT_STAT(3, 1);
-                    }
-                } else {
-                    cur = -1;
+            if (cur >= 0 && steps < 12) {
+                // compact float walk step: exact ids via a margin that bounds the float
+                // evaluation error (tt_grid.cu walk_prep_kernel); f from the element's
+                // gradient record: f = c_last + g . (x - o), accurate to a few ulps
+                WRec<D> w;
+                load_wrec<D>(g.wrec, cur, w);
+                double2 pc0 = make_double2(0.0, 0.0), pc1 = make_double2(0.0, 0.0);
+                if (src.egrad) {  // speculative: the gradient record of the element tested
+                    const double2* q = reinterpret_cast<const double2*>(src.egrad + (int64_t)cur * 4);
+                    pc0 = __ldg(q);
+                    pc1 = __ldg(q + 1);
                 }
-            } else if (cur >= 0 && steps < 12) {
-                Rec<D> r;
-                load_rec<D>(g.rec, cur, r);
-                RecTail<D> tl;
-                load_tail<D>(g.rec, cur, tl);
-                if constexpr (SPEC) {
-                    // speculative: the coefficient record of the element being tested
-                    if (src.ecoef) {
-                        const double2* q = reinterpret_cast<const double2*>(src.ecoef + (int64_t)cur * 4);
-                        pc0 = __ldg(q);
-                        pc1 = __ldg(q + 1);
-                    }
+                double r[D];
+                float rf[D];
+#pragma unroll
+                for (int c = 0; c < D; ++c) { r[c] = x[c] - w.o[c]; rf[c] = __double2float_rn(r[c]); }
+                float lf[K];
+#pragma unroll
+                for (int i = 0; i < D; ++i) {
+                    float a = w.b[i][0] * rf[0];
+#pragma unroll
+                    for (int c = 1; c < D; ++c) a = fmaf(w.b[i][c], rf[c], a);
+                    lf[i] = a;
                 }
-                bary_from_rec<D>(r, x, l);
+                float last = 1.0f - lf[0] - lf[1];
+                if constexpr (D == 3) last -= lf[2];
+                lf[D] = last;
                 int imin = 0;
-                double lmin = l[0];
+                float lmin = lf[0];
 #pragma unroll
                 for (int i = 1; i <= D; ++i)
-                    if (l[i] < lmin) { lmin = l[i]; imin = i; }
-                if (lmin >= (double)tl.tau) {
+                    if (lf[i] < lmin) { lmin = lf[i]; imin = i; }
+                if (lmin >= w.tau) {
                     hit = cur;
                     done = true;
-                } else if (lmin >= -EPS) {
-                    cur = -1;  // inside within the slack, not certified: reference scan
+                    fw_hit = true;
+                    const double gv[4] = {pc0.x, pc0.y, pc1.x, pc1.y};
+                    double f = gv[D];
+#pragma unroll
+                    for (int c = 0; c < D; ++c) f = fma(gv[c], r[c], f);
+                    fw_f = f;
+                } else if (lmin > -w.tau) {
+                    fb = cur;  // within the uncertainty band of a facet: exact double walk
+                    cur = -1;
                 } else {
-                    int nb = tl.nbr[0];
+                    int nb = w.nbr[0];
 #pragma unroll
                     for (int i = 1; i <= D; ++i)
-                        if (imin == i) nb = tl.nbr[i];
+                        if (imin == i) nb = w.nbr[i];
                     cur = nb;
                     ++steps;
+                    TT_STAT(3, 1);
                 }
             } else {
                 cur = -1;
             }
             if (!done && cur < 0) {
-                // exact reference scan (+ snap / strict), rare; the float-walk path mapped
-                // the point with FMA, so recompute it exactly first (montecarlo.py:123-124)
-                if constexpr (FW) {
-                    if constexpr (RL && PLAN == TT_PLAN_SHARED) plan_lambda<D, PLAN>(plan, e, jcur, lam);
-                    if constexpr (SMEMV) {
-                        double vv[K][D];
-#pragma unroll
-                        for (int q = 0; q < K * D; ++q) vv[q / D][q % D] = s_v[wib][gib][q];
-                        map_point<D>(lam, vv, x);
-                    } else {
-                        map_point<D>(lam, v, x);
-                    }
+                // exact localisation (rare): the walk mapped the point with FMA, so recompute
+                // it in the reference's op order first (montecarlo.py:123-124); then the
+                // double certified walk from the band element (one diverged lane, ~1
+                // dependent record load) or the reference cell scan
+                {
+                    double vv[K][D];
+                    vertices(vv);
+                    map_point<D>(lam, vv, x);
                 }
-                if constexpr (FW) {
-                    // double certified walk from the band element (then the reference scan),
-                    // out of line: one diverged lane, ~1 dependent record load instead of
-                    // the ~14-candidate scan chain
-                    hit = fb >= 0 ? locate_walk<D>(g, x, EPS, fb, l) : locate_point<D>(g, x, EPS, l);
-                } else {
-                    hit = locate_point<D>(g, x, EPS, l);
-                }
+                hit = fb >= 0 ? locate_walk<D>(g, x, EPS, fb, l) : locate_point<D>(g, x, EPS, l);
                 bool deferred = false;
                 if (hit < 0) {
                     if (src.outside == TT_OUTSIDE_STRICT) {
                         flags |= TT_FLAG_OUTSIDE_STRICT;
-                    } else if (FW && DEFER && ids_out == nullptr && pend_j < 0) {
+                    } else if (DEFER && ids_out == nullptr && pend_j < 0) {
                         // the nearest-element ring search runs at the end of the tile with
                         // the whole warp (nearest_element_warp) instead of on this one lane
                         pend_j = jcur;
@@ -584,32 +520,15 @@ __global__ void __launch_bounds__(BLOCK, MINB) mc_mesh_kernel(TargetDev t, int64
                 if (!fw_hit) TT_STAT(4, 1);
                 if (ids_out) ids_out[le * N + jcur] = hit;
                 double f = 0.0;
-                if (FW && fw_hit) {
-                    f = fw_f;
-                } else if (hit >= 0 && (contrib || b)) {
-                    if (SPEC && !FW && src.ecoef && hit == cur) {
-                        const double c[4] = {pc0.x, pc0.y, pc1.x, pc1.y};
-                        f = mul(c[0], l[0]);
-#pragma unroll
-                        for (int i = 1; i < K; ++i) f = add(f, mul(c[i], l[i]));
-                    } else {
-                        f = p1_eval<D>(src, hit, l);
-                    }
-                }
+                if (fw_hit) f = fw_f;
+                else if (hit >= 0 && (contrib || b)) f = p1_eval<D>(src, hit, l);
                 if (!isfinite(f)) flags |= TT_FLAG_NONFINITE;
-                if constexpr (RL && PLAN == TT_PLAN_SHARED) {
-                    double lt[K];
-                    plan_lambda<D, PLAN>(plan, e, jcur, lt);
 #pragma unroll
-                    for (int i = 0; i < K; ++i) acc[i] = fma(f, lt[i], acc[i]);
-                } else {
-#pragma unroll
-                    for (int i = 0; i < K; ++i) acc[i] = fma(f, lam[i], acc[i]);
-                }
+                for (int i = 0; i < K; ++i) acc[i] = fma(f, lam[i], acc[i]);
                 busy = false;
             }
         }
-        if constexpr (FW && DEFER) {
+        if constexpr (DEFER) {
             // deferred snaps (outside points; rare): one warp-cooperative nearest-element
             // search per pending lane, in lane order, then the owner adds f * lambda_j
             unsigned pm = __ballot_sync(FULL, pend_j >= 0);
@@ -619,15 +538,10 @@ __global__ void __launch_bounds__(BLOCK, MINB) mc_mesh_kernel(TargetDev t, int64
                 double xe[D] = {};
                 double lj[K];
                 if (lane == sl) {
-                    plan_lambda<D, PLAN>(plan, e, pend_j, lj);
-                    if constexpr (SMEMV) {
-                        double vv[K][D];
-#pragma unroll
-                        for (int q = 0; q < K * D; ++q) vv[q / D][q % D] = s_v[wib][gib][q];
-                        map_point<D>(lj, vv, xe);
-                    } else {
-                        map_point<D>(lj, v, xe);
-                    }
+                    plan_lambda<D, PLAN>(plan, t.gid, e, pend_j, lj);
+                    double vv[K][D];
+                    vertices(vv);
+                    map_point<D>(lj, vv, xe);
                 }
 #pragma unroll
                 for (int c = 0; c < D; ++c) xe[c] = __shfl_sync(FULL, xe[c], sl);
@@ -674,7 +588,7 @@ __global__ void map_points_kernel(TargetDev t, int64_t e_lo, int64_t n_el, int p
     if (plan_kind == TT_PLAN_SHARED) {
         for (int c = 0; c < K; ++c) lam[c] = plan.lam[j * K + c];
     } else {
-        philox_lambda<D>(plan.seed, e, j, lam);
+        philox_lambda<D>(plan.seed, stream_id(t.gid, e), j, lam);
     }
     double x[D];
     map_point<D>(lam, v, x);
@@ -866,123 +780,106 @@ static SrcDev to_src(const tt_source_t& s) {
     return d;
 }
 
-template <int D, int PLAN, int SRC, int G>
-static int launch_mc(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_plan_t* p,
-                     const tt_source_t* s, double* contrib, double* b, int32_t* status,
-                     cudaStream_t st) {
-    TargetDev td{t->nodes, t->elems, t->measure};
-    PlanDev pd{p->n_samples, p->lam, p->seed};
-    SrcDev sd = to_src(*s);
+// Resident blocks per SM of a kernel at a block size, queried once per kernel instance
+// (every caller passes the same kernel/block/dynamic-smem triple).
+template <class Kernel>
+static int blocks_per_sm(Kernel kernel, int block, size_t smem) {
+    int per = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, block, smem);
+    return per < 1 ? 1 : per;
+}
+
+// Lanes per element for the fused mesh kernel.  Measured on C2 (ms per load): N = 32 / 48
+// G = 4 0.694 / 0.927 vs G = 2 0.744 / 1.053; N = 64 G = 4 best (G = 8 +5 %); N = 128
+// G = 4 ~ G = 8; N = 256 G = 16 3.76 vs G = 8 3.87; N = 512 G = 16 6.94 vs G = 32 7.35;
+// N = 1024 G = 16 13.41 vs 13.68.  Other sources: ~16 samples per lane.
+static int lanes_per_element(int src_kind, int64_t N) {
+    if (src_kind == TT_SRC_MESH) return N < 32 ? 2 : N < 128 ? 4 : N < 256 ? 8 : N < 2048 ? 16 : 32;
+    const int64_t g = N / 16;
+    return g < 8 ? 4 : g < 16 ? 8 : g < 32 ? 16 : 32;
+}
+
+// The fused mesh-backed load (and, with ids != NULL, the id sink of tt_mc_cache_ids: the
+// same kernel instance, so cached ids are exactly the ids every load walks to).
+template <int D, int PLAN, int G>
+static int launch_mesh(const TargetDev& td, int64_t e_lo, int64_t e_hi, const PlanDev& pd,
+                       const SrcDev& sd, bool defer, double* contrib, double* b, int32_t* ids,
+                       int32_t* status, cudaStream_t st) {
     constexpr int EPW = 32 / G;
     const int64_t tiles = (e_hi - e_lo + EPW - 1) / EPW;
-    const int block = 256;
-    int64_t blocks = (tiles + 7) / 8;
-    int per_sm = 0;
-    if constexpr (SRC == TT_SRC_MESH) {
-        // variant: bit0 = speculative coefficient prefetch, bit1 = 3 blocks/SM register target,
-        // bit2 = compact float walk + gradient evaluation (needs grid.wrec and elem_grad)
-        static int variant = [] { const char* v = getenv("TT_MC_VARIANT"); return v ? atoi(v) : 21; }();
-        auto launch = [&](auto kernel) {
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, 0);
-            if (per_sm < 1) per_sm = 1;
-            const int64_t cap = (int64_t)sm_count() * per_sm * 16;
-            if (blocks > cap) blocks = cap;
-            if (blocks < 1) blocks = 1;
-            kernel<<<(unsigned)blocks, block, 0, st>>>(td, e_lo, e_hi, pd, sd, contrib, b, nullptr, status);
-        };
-        if ((variant & 4) && sd.grid.wrec && sd.egrad && sd.grid.walk && sd.seeds) {
-            if (variant & 16) {
-                // 128-thread blocks, vertices/seeds in shared memory, 5 (or 6) blocks per SM
-                // grid = TT_MC_WAVES waves of resident blocks.  Measured on C2: one wave (the
-                // per-block seed-slot table is built once) beats 16 waves by 0.08 ms at N = 64;
-                // 32-lane groups (N >= 512) keep 16 waves (+1 % at N = 1024)
-                static const int waves_env = [] { const char* v = getenv("TT_MC_WAVES"); return v ? atoi(v) : 0; }();
-                const int waves = waves_env > 0 ? waves_env : (G >= 32 ? 16 : 1);
-                const bool slot = PLAN == TT_PLAN_SHARED && p->n_samples <= kSlotCap;
-                const size_t dyn_smem = slot ? (size_t)((p->n_samples + 15) / 16 * 16) : 0;
-                auto launch128 = [&](auto kernel) {
-                    int per = 0;
-                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, 128, 0);
-                    if (per < 1) per = 1;
-                    int64_t nb = (tiles + 3) / 4;
-                    const int64_t cap = (int64_t)sm_count() * per * waves;
-                    if (nb > cap) nb = cap;
-                    if (nb < 1) nb = 1;
-                    // dynamic shared memory = the seed-slot table (N bytes, SLOT kernels only):
-                    // every byte of shared memory is L1 the walk's records lose (measured:
-                    // +20 KB/block costs 0.056 ms at C2)
-                    kernel<<<(unsigned)nb, 128, dyn_smem, st>>>(td, e_lo, e_hi, pd, sd, contrib, b, nullptr, status);
-                };
-                // DEFER (source hint: the walk seeds saw outside points): the kernel variant
-                // whose outside samples are snapped warp-cooperatively at tile end.  It costs
-                // registers (C2: 1.12 -> 1.22 ms), so matching meshes run the plain variant.
-                const bool defer = (s->hints & TT_HINT_DEFER_SNAP) != 0;
-                if (slot) {
-                    if (defer) launch128(mc_mesh_kernel<D, PLAN, G, true, 5, true, 128, true, false, true, true>);
-                    else launch128(mc_mesh_kernel<D, PLAN, G, true, 5, true, 128, true, false, true>);
-                } else {
-                    if (defer) launch128(mc_mesh_kernel<D, PLAN, G, true, 5, true, 128, true, false, false, true>);
-                    else launch128(mc_mesh_kernel<D, PLAN, G, true, 5, true, 128, true>);
-                }
-                return launch_check("mc_mesh_kernel (float walk, smem)");
-            }
-            if (variant & 8) launch(mc_mesh_kernel<D, PLAN, G, true, 3, true>);
-            else launch(mc_mesh_kernel<D, PLAN, G, true, 2, true>);
-            return launch_check("mc_mesh_kernel (float walk)");
+    // one wave of blocks (the per-block seed-slot table is built once; measured 0.08 ms
+    // better than 16 waves at C2, N = 64); 32-lane groups (N >= 512) keep 16 waves (+1 %)
+    const int waves = G >= 32 ? 16 : 1;
+    const bool slot = PLAN == TT_PLAN_SHARED && pd.n <= kSlotCap;
+    // dynamic shared memory = the seed-slot table (N bytes, SLOT kernels only): every byte
+    // of shared memory is L1 the walk's records lose (+20 KB/block costs 0.056 ms at C2)
+    const size_t smem = slot ? (size_t)((pd.n + 15) / 16 * 16) : 0;
+    auto go = [&](auto kernel) {
+        static const int per = blocks_per_sm(kernel, kMcBlock, 0);
+        constexpr int kWarps = kMcBlock / 32;  // a warp works one tile at a time
+        int64_t nb = (tiles + kWarps - 1) / kWarps;
+        const int64_t cap = (int64_t)sm_count() * per * waves;
+        nb = nb > cap ? cap : nb < 1 ? 1 : nb;
+        kernel<<<(unsigned)nb, kMcBlock, smem, st>>>(td, e_lo, e_hi, pd, sd, contrib, b, ids, status);
+    };
+    // DEFER costs registers (C2: 1.12 -> 1.22 ms), so only pairs known to snap run it
+    if constexpr (PLAN == TT_PLAN_SHARED) {
+        if (slot) {
+            if (defer) go(mc_mesh_kernel<D, PLAN, G, true, true>);
+            else go(mc_mesh_kernel<D, PLAN, G, true, false>);
+            return launch_check("mc_mesh_kernel");
         }
-        switch (variant & 3) {
-            case 0: launch(mc_mesh_kernel<D, PLAN, G, false, 2>); break;
-            case 1: launch(mc_mesh_kernel<D, PLAN, G, true, 2>); break;
-            case 2: launch(mc_mesh_kernel<D, PLAN, G, false, 3>); break;
-            default: launch(mc_mesh_kernel<D, PLAN, G, true, 3>); break;
-        }
-        return launch_check("mc_mesh_kernel");
     }
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mc_load_kernel<D, PLAN, SRC, G>, block, 0);
-    if (per_sm < 1) per_sm = 1;
-    const int64_t cap = (int64_t)sm_count() * per_sm * 16;
-    if (blocks > cap) blocks = cap;
-    if (blocks < 1) blocks = 1;
-    mc_load_kernel<D, PLAN, SRC, G><<<(unsigned)blocks, block, 0, st>>>(td, e_lo, e_hi, pd, sd,
-                                                                        s->expr, contrib, b, status);
-    return launch_check("mc_load_kernel");
+    if (defer) go(mc_mesh_kernel<D, PLAN, G, false, true>);
+    else go(mc_mesh_kernel<D, PLAN, G, false, false>);
+    return launch_check("mc_mesh_kernel");
+}
+
+template <int D, int PLAN, int SRC, int G>
+static int launch_mc(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_plan_t* p,
+                     const tt_source_t* s, double* contrib, double* b, int32_t* ids,
+                     int32_t* status, cudaStream_t st) {
+    TargetDev td{t->nodes, t->elems, t->measure, t->gid};
+    PlanDev pd{p->n_samples, p->lam, p->seed};
+    SrcDev sd = to_src(*s);
+    if constexpr (SRC == TT_SRC_MESH) {
+        return launch_mesh<D, PLAN, G>(td, e_lo, e_hi, pd, sd, (s->hints & TT_HINT_DEFER_SNAP) != 0,
+                                       contrib, b, ids, status, st);
+    } else {
+        constexpr int EPW = 32 / G;
+        const int64_t tiles = (e_hi - e_lo + EPW - 1) / EPW;
+        static const int per = blocks_per_sm(mc_load_kernel<D, PLAN, SRC, G>, 256, 0);
+        int64_t blocks = (tiles + 7) / 8;
+        const int64_t cap = (int64_t)sm_count() * per * 16;
+        blocks = blocks > cap ? cap : blocks < 1 ? 1 : blocks;
+        mc_load_kernel<D, PLAN, SRC, G><<<(unsigned)blocks, 256, 0, st>>>(td, e_lo, e_hi, pd, sd,
+                                                                          s->expr, contrib, b, status);
+        return launch_check("mc_load_kernel");
+    }
 }
 
 template <int D, int PLAN, int SRC>
 static int dispatch_g(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_plan_t* p,
-                      const tt_source_t* s, double* contrib, double* b, int32_t* status,
-                      cudaStream_t st) {
-    // lanes per element G.  Measured on C2 (fused mesh kernel, ms per load): N = 32 / 48
-    // G = 4 0.694 / 0.927 vs G = 2 0.744 / 1.053; N = 64 G = 4 best (G = 8 +5 %);
-    // N = 128 G = 4 ~ G = 8; N = 256 G = 16 3.76 vs G = 8 3.87; N = 512 G = 16 6.94 vs
-    // G = 32 7.35; N = 1024 G = 16 13.41 vs 13.68.  TT_MC_SPL=<samples per lane> restores
-    // the plain N / spl rule for experiments.
-    const int64_t N = p->n_samples;
-    static int spl = [] { const char* v = getenv("TT_MC_SPL"); return v ? atoi(v) : 0; }();
-    int G;
-    if (spl > 0 || SRC != TT_SRC_MESH) {  // other sources: ~16 samples per lane
-        const int64_t gsel = N / (spl > 0 ? spl : 16);
-        G = gsel < 4 ? 2 : gsel < 8 ? 4 : gsel < 16 ? 8 : gsel < 32 ? 16 : 32;
-    } else {
-        G = N < 32 ? 2 : N < 128 ? 4 : N < 256 ? 8 : N < 2048 ? 16 : 32;
-    }
+                      const tt_source_t* s, double* contrib, double* b, int32_t* ids,
+                      int32_t* status, cudaStream_t st) {
+    const int G = lanes_per_element(SRC, p->n_samples);
     if constexpr (SRC == TT_SRC_MESH)
-        if (G == 2) return launch_mc<D, PLAN, SRC, 2>(t, e_lo, e_hi, p, s, contrib, b, status, st);
-    if (G <= 4) return launch_mc<D, PLAN, SRC, 4>(t, e_lo, e_hi, p, s, contrib, b, status, st);
-    if (G == 8) return launch_mc<D, PLAN, SRC, 8>(t, e_lo, e_hi, p, s, contrib, b, status, st);
-    if (G == 16) return launch_mc<D, PLAN, SRC, 16>(t, e_lo, e_hi, p, s, contrib, b, status, st);
-    return launch_mc<D, PLAN, SRC, 32>(t, e_lo, e_hi, p, s, contrib, b, status, st);
+        if (G == 2) return launch_mc<D, PLAN, SRC, 2>(t, e_lo, e_hi, p, s, contrib, b, ids, status, st);
+    if (G == 4) return launch_mc<D, PLAN, SRC, 4>(t, e_lo, e_hi, p, s, contrib, b, ids, status, st);
+    if (G == 8) return launch_mc<D, PLAN, SRC, 8>(t, e_lo, e_hi, p, s, contrib, b, ids, status, st);
+    if (G == 16) return launch_mc<D, PLAN, SRC, 16>(t, e_lo, e_hi, p, s, contrib, b, ids, status, st);
+    return launch_mc<D, PLAN, SRC, 32>(t, e_lo, e_hi, p, s, contrib, b, ids, status, st);
 }
 
 template <int D, int PLAN>
 static int dispatch_src(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_plan_t* p,
-                        const tt_source_t* s, double* contrib, double* b, int32_t* status,
-                        cudaStream_t st) {
+                        const tt_source_t* s, double* contrib, double* b, int32_t* ids,
+                        int32_t* status, cudaStream_t st) {
     switch (s->kind) {
-        case TT_SRC_EXPR: return dispatch_g<D, PLAN, TT_SRC_EXPR>(t, e_lo, e_hi, p, s, contrib, b, status, st);
-        case TT_SRC_MESH: return dispatch_g<D, PLAN, TT_SRC_MESH>(t, e_lo, e_hi, p, s, contrib, b, status, st);
-        case TT_SRC_VALUES: return dispatch_g<D, PLAN, TT_SRC_VALUES>(t, e_lo, e_hi, p, s, contrib, b, status, st);
-        case TT_SRC_CACHED: return dispatch_g<D, PLAN, TT_SRC_CACHED>(t, e_lo, e_hi, p, s, contrib, b, status, st);
+        case TT_SRC_EXPR: return dispatch_g<D, PLAN, TT_SRC_EXPR>(t, e_lo, e_hi, p, s, contrib, b, ids, status, st);
+        case TT_SRC_MESH: return dispatch_g<D, PLAN, TT_SRC_MESH>(t, e_lo, e_hi, p, s, contrib, b, ids, status, st);
+        case TT_SRC_VALUES: return dispatch_g<D, PLAN, TT_SRC_VALUES>(t, e_lo, e_hi, p, s, contrib, b, ids, status, st);
+        case TT_SRC_CACHED: return dispatch_g<D, PLAN, TT_SRC_CACHED>(t, e_lo, e_hi, p, s, contrib, b, ids, status, st);
     }
     set_error("tt_mc_load: unknown source kind %d", s->kind);
     return TT_ERR_INVALID_PARAMETER;
@@ -990,10 +887,10 @@ static int dispatch_src(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt
 
 template <int D>
 static int dispatch_plan(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_plan_t* p,
-                         const tt_source_t* s, double* contrib, double* b, int32_t* status,
-                         cudaStream_t st) {
-    if (p->kind == TT_PLAN_SHARED) return dispatch_src<D, TT_PLAN_SHARED>(t, e_lo, e_hi, p, s, contrib, b, status, st);
-    if (p->kind == TT_PLAN_PHILOX) return dispatch_src<D, TT_PLAN_PHILOX>(t, e_lo, e_hi, p, s, contrib, b, status, st);
+                         const tt_source_t* s, double* contrib, double* b, int32_t* ids,
+                         int32_t* status, cudaStream_t st) {
+    if (p->kind == TT_PLAN_SHARED) return dispatch_src<D, TT_PLAN_SHARED>(t, e_lo, e_hi, p, s, contrib, b, ids, status, st);
+    if (p->kind == TT_PLAN_PHILOX) return dispatch_src<D, TT_PLAN_PHILOX>(t, e_lo, e_hi, p, s, contrib, b, ids, status, st);
     set_error("tt_mc_load: unknown plan kind %d", p->kind);
     return TT_ERR_INVALID_PARAMETER;
 }
@@ -1054,52 +951,28 @@ extern "C" int tt_mc_load(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const 
     int st = check_source(s, t->dim);
     if (st) return st;
     if (e_hi == e_lo) return TT_OK;
-    if (t->dim == 2) return dispatch_plan<2>(t, e_lo, e_hi, p, s, contrib, b, status, as_stream(stream));
-    return dispatch_plan<3>(t, e_lo, e_hi, p, s, contrib, b, status, as_stream(stream));
+    if (t->dim == 2) return dispatch_plan<2>(t, e_lo, e_hi, p, s, contrib, b, nullptr, status, as_stream(stream));
+    return dispatch_plan<3>(t, e_lo, e_hi, p, s, contrib, b, nullptr, status, as_stream(stream));
 }
 
 extern "C" int tt_mc_cache_ids(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_plan_t* p,
                                const tt_grid_t* g, const int32_t* seeds, int32_t* ids, void* stream) {
     if (!t || !p || !g || p->dim != t->dim || g->dim != t->dim || e_lo < 0 || e_hi > t->n_elems ||
-        e_lo > e_hi) {
+        e_lo > e_hi || !ids || (p->kind == TT_PLAN_SHARED && !p->lam)) {
         set_error("tt_mc_cache_ids: bad arguments");
         return TT_ERR_INVALID_PARAMETER;
     }
     if ((e_hi - e_lo) * p->n_samples == 0) return TT_OK;
-    // the fused mesh kernel with an id sink and no accumulation: the very code path the
-    // load uses, so cached ids are the ids every load sees (transfer.py:74-82)
-    TargetDev td{t->nodes, t->elems, t->measure};
-    PlanDev pd{p->n_samples, p->lam, p->seed};
-    SrcDev sd{};
-    sd.kind = TT_SRC_MESH;
-    sd.outside = TT_OUTSIDE_SNAP;
-    sd.grid = to_dev(*g);
-    sd.seeds = seeds;
-    auto s = as_stream(stream);
-    const int64_t tiles = (e_hi - e_lo + 3) / 4;
-    const unsigned nb = grid_for(tiles * 32, 256);
-    // the float-walk kernel when the grid carries compact walk records (the default load
-    // path), else the double walk; either way the ids are the reference scan's
-    const bool fw = g->wrec && g->walk && seeds;
-    const unsigned nb128 = grid_for(tiles * 32, 128);  // same launch shape as the default load
-    if (t->dim == 2) {
-        if (p->kind == TT_PLAN_SHARED) {
-            if (fw) mc_mesh_kernel<2, TT_PLAN_SHARED, 8, true, 5, true, 128, true><<<nb128, 128, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
-            else mc_mesh_kernel<2, TT_PLAN_SHARED, 8, false, 2><<<nb, 256, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
-        } else {
-            if (fw) mc_mesh_kernel<2, TT_PLAN_PHILOX, 8, true, 5, true, 128, true><<<nb128, 128, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
-            else mc_mesh_kernel<2, TT_PLAN_PHILOX, 8, false, 2><<<nb, 256, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
-        }
-    } else {
-        if (p->kind == TT_PLAN_SHARED) {
-            if (fw) mc_mesh_kernel<3, TT_PLAN_SHARED, 8, true, 5, true, 128, true><<<nb128, 128, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
-            else mc_mesh_kernel<3, TT_PLAN_SHARED, 8, false, 2><<<nb, 256, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
-        } else {
-            if (fw) mc_mesh_kernel<3, TT_PLAN_PHILOX, 8, true, 5, true, 128, true><<<nb128, 128, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
-            else mc_mesh_kernel<3, TT_PLAN_PHILOX, 8, false, 2><<<nb, 256, 0, s>>>(td, e_lo, e_hi, pd, sd, nullptr, nullptr, ids, nullptr);
-        }
-    }
-    return launch_check("mc_mesh_kernel (cache ids)");
+    // the fused load kernel itself (same instance the load launches for this N) with an id
+    // sink and no accumulation, so cached ids are the ids every load sees (transfer.py:74-82)
+    tt_source_t s{};
+    s.kind = TT_SRC_MESH;
+    s.outside = TT_OUTSIDE_SNAP;
+    s.dim = t->dim;
+    s.grid = *g;
+    s.seeds = seeds;
+    if (t->dim == 2) return dispatch_plan<2>(t, e_lo, e_hi, p, &s, nullptr, nullptr, ids, nullptr, as_stream(stream));
+    return dispatch_plan<3>(t, e_lo, e_hi, p, &s, nullptr, nullptr, ids, nullptr, as_stream(stream));
 }
 
 extern "C" int tt_map_points(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_plan_t* p,
@@ -1110,7 +983,7 @@ extern "C" int tt_map_points(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, con
     }
     int64_t total = (e_hi - e_lo) * p->n_samples;
     if (total == 0) return TT_OK;
-    TargetDev td{t->nodes, t->elems, t->measure};
+    TargetDev td{t->nodes, t->elems, t->measure, t->gid};
     PlanDev pd{p->n_samples, p->lam, p->seed};
     auto s = as_stream(stream);
     if (t->dim == 2)

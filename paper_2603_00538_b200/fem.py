@@ -218,29 +218,30 @@ def assemble_mass_matrix(mesh, rule: QuadratureRule | None = None) -> SparseSymM
     return SparseSymMatrix(mesh.n_nodes, row_ptr, cols, vals)
 
 
-#: "ell" (default when every row has <= 16 entries: the shared-memory slab PCG when the rows
-#: fit, else the L2-streaming ELL PCG), "ell_l2" (never the slab) or "csr"
-_PCG_PATH = __import__("os").environ.get("TT_PCG_PATH", "ell")
-
-
 class PcgResult:
     __slots__ = ("iterations", "residual", "best_residual", "converged", "zero_rhs")
 
 
 def pcg_device(M: SparseSymMatrix, b: torch.Tensor, tol: float = 1e-12,
                maxiter: int | None = None, x: torch.Tensor | None = None,
-               best_x: torch.Tensor | None = None):
-    """Launch the single-kernel PCG; returns (x, best_x, result tensor) without syncing."""
+               best_x: torch.Tensor | None = None, path: str = "auto"):
+    """Launch the single-kernel PCG; returns (x, best_x, result tensor) without syncing.
+
+    ``path``: "auto" -- the ELL matrix (every row <= 16 entries) with its rows held in
+    shared memory when they fit (the slab kernel), else streamed from L2/HBM; "ell_l2"
+    never uses the slab; "csr" the CSR kernel.  All paths run the same recurrence."""
     n = M.n
     maxiter = 10 * n if maxiter is None else int(maxiter)
     work, res = M.workspace()
     x = x if x is not None else torch.empty(n, dtype=torch.float64, device=b.device)
     best_x = best_x if best_x is not None else torch.empty(n, dtype=torch.float64, device=b.device)
-    ell = M.ell() if _PCG_PATH != "csr" else None
+    if path not in ("auto", "ell_l2", "csr"):
+        raise ValueError(f"unknown PCG path {path!r}")
+    ell = M.ell() if path != "csr" else None
     if ell is not None:
         args = (n, ell[3], _lib.ptr(ell[0]), _lib.ptr(ell[1]), _lib.ptr(ell[2]), _lib.ptr(b), float(tol),
                 maxiter, _lib.ptr(x), _lib.ptr(best_x), _lib.ptr(work), _lib.ptr(res), _lib.stream_handle())
-        if _PCG_PATH == "ell" and getattr(M, "_slab_ok", False):
+        if path == "auto" and getattr(M, "_slab_ok", False):
             # rows held in shared memory when they fit (TT_ERR_CAPACITY: nothing launched)
             if _lib.call_status("tt_pcg_ell_slab", *args) == 0:
                 return x, best_x, res
@@ -280,16 +281,18 @@ def decode_result(res: torch.Tensor, status: torch.Tensor | None = None):
     return out, int(np.frombuffer(raw[res.numel() * 8:res.numel() * 8 + 4], dtype=np.int32)[0])
 
 
-def cg_solve(M: SparseSymMatrix, b, tol: float = 1e-12, maxiter: int | None = None):
+def cg_solve(M: SparseSymMatrix, b, tol: float = 1e-12, maxiter: int | None = None, *,
+             path: str = "auto"):
     """Jacobi-preconditioned CG for ``M x = b`` (fem.py:113-152): stops when the
     recurrence residual ||r||/||b|| <= tol; raises ``NoConvergence`` carrying the best
-    iterate after ``maxiter`` (default 10 n) iterations; b = 0 returns zeros."""
+    iterate after ``maxiter`` (default 10 n) iterations; b = 0 returns zeros.
+    ``path`` (extension): the device kernel, see ``pcg_device``."""
     was_np = not isinstance(b, torch.Tensor)
     bd = torch.as_tensor(np.asarray(b, dtype=np.float64) if was_np else b,
                          device=M.vals_dev.device, dtype=torch.float64).contiguous()
     if bd.shape != (M.n,):
         raise DimensionMismatch(f"rhs length {tuple(bd.shape)} for {M.n}x{M.n} matrix")
-    x, best_x, res = pcg_device(M, bd, tol, maxiter)
+    x, best_x, res = pcg_device(M, bd, tol, maxiter, path=path)
     return finish_solve(x, best_x, res, was_np)
 
 

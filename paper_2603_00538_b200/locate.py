@@ -12,6 +12,7 @@ int(sqrt(E))`` cells (locate.py:38-41); d = 3 uses ``int(cbrt(E))`` per axis.
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 from functools import cached_property
 
 import numpy as np
@@ -56,7 +57,11 @@ class UniformGridLocator:
         self.cell_start_dev = cell_start
         self.cell_elems_dev = cell_elems
         self.walk = walk
-        self._seeds = {}
+        #: kernel variant for outside samples (performance only): None = decided once per
+        #: target from its walk seeds (an anchor outside the source mesh -> outside samples
+        #: are snapped warp-cooperatively at tile end), True / False = forced
+        self.defer_snaps = None
+        self._seeds = weakref.WeakKeyDictionary()
 
     @property
     def nx(self):
@@ -128,33 +133,37 @@ class UniformGridLocator:
     def seeds_for(self, target) -> torch.Tensor:
         """Walk starts per target element (E, 16): source elements containing the
         element's 16 anchor points -- centroid c, the points (v_i + c)/2, k-means anchors
-        (tt_seed_elements; cached per target, meshes are immutable)."""
-        key = id(target)
-        hit = self._seeds.get(key)
-        if hit is not None and hit[0] is target:
-            return hit[1]
+        (tt_seed_elements; cached per target while it lives, meshes are immutable)."""
+        hit = self._seeds.get(target)
+        if hit is not None:
+            return hit[0]
         seeds = torch.empty((target.n_elems, _lib.TT_SEED_ANCHORS), dtype=torch.int32,
                             device=self.cell_start_dev.device)
         g, t = self.desc(), target.device.desc()
         st = _lib.status_word()
         _lib.call("tt_seed_elements", C.byref(g), C.byref(t), 0, target.n_elems, _lib.ptr(seeds),
                   _lib.ptr(st), _lib.stream_handle())
-        # one-time read (setup): anchors outside the source mesh mean outside samples occur
-        # -> the fused kernel variant with warp-cooperative snaps (a hint only); otherwise
-        # unknown until the first load reports whether it snapped
-        snap_prone = True if int(st.item()) & _lib.TT_FLAG_SNAPPED else None
-        self._seeds[key] = (target, seeds, snap_prone)
+        # one-time read (setup): an anchor outside the source mesh means outside samples
+        # occur -> the kernel variant with warp-cooperative snaps.  Decided here, before any
+        # load, so every load of this (target, locator) pair runs the same kernel and is
+        # bitwise reproducible
+        self._seeds[target] = (seeds, bool(int(st.item()) & _lib.TT_FLAG_SNAPPED))
         return seeds
 
-    def snap_prone(self, target):
-        """True / False: loads of ``target`` through this locator do / do not snap outside
-        samples; None: not known yet (no anchor was outside, no load has run)."""
+    def snap_prone(self, target) -> bool:
+        """Whether loads of ``target`` run the deferred (warp-cooperative) snap variant:
+        ``defer_snaps`` when set, else whether a walk-seed anchor lay outside."""
+        if self.defer_snaps is not None:
+            return bool(self.defer_snaps)
         self.seeds_for(target)
-        return self._seeds[id(target)][2]
+        return self._seeds[target][1]
 
-    def set_snap_prone(self, target, value: bool):
-        t, seeds, _ = self._seeds[id(target)]
-        self._seeds[id(target)] = (t, seeds, bool(value))
+    def release(self, target=None):
+        """Drop the cached walk seeds of ``target`` (all targets when None)."""
+        if target is None:
+            self._seeds.clear()
+        else:
+            self._seeds.pop(target, None)
 
     @cached_property
     def cell_start(self) -> np.ndarray:

@@ -70,8 +70,12 @@ class AnalyticField:
         dim = pts.shape[-1]
         desc = self.desc(dim)
         if desc is None:
-            p = np.asarray(points, dtype=np.float64)
-            return np.asarray(self.fn(*(p[..., c] for c in range(dim))), dtype=np.float64)
+            # an untraceable numpy callable is the user's host black box: hand it host
+            # points (device tensors in -> device values out, as for traced fields)
+            on_dev = isinstance(points, torch.Tensor)
+            p = points.detach().cpu().numpy() if on_dev else pts
+            f = np.asarray(self.fn(*(p[..., c] for c in range(dim))), dtype=np.float64)
+            return torch.from_numpy(np.ascontiguousarray(f)).to(points.device) if on_dev else f
         return _eval_points(desc, points, dim, keep=(), host_fallback=False)
 
 
@@ -106,7 +110,7 @@ class MeshBackedField:
             # snap fallbacks gather the vertex coefficients directly
             s.seeds = _lib.ptr(self.locator.seeds_for(target)).value
             s.elem_grad = _lib.ptr(self.field.elem_grad()).value
-            if self.locator.snap_prone(target) is True:
+            if self.locator.snap_prone(target):
                 s.hints |= _lib.TT_HINT_DEFER_SNAP
         else:
             s.elem_coeffs = _lib.ptr(self.field.elem_coeffs()).value
@@ -286,6 +290,24 @@ def map_points(target, plan: SamplePlan, e_lo: int = 0, e_hi: int | None = None)
     return pts
 
 
+def sample_source_elements(target, locator: UniformGridLocator, plan: SamplePlan, e_lo: int = 0,
+                           e_hi: int | None = None, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Source element of every sample (e_hi - e_lo, N) int32 on the device: located, or the
+    nearest element when outside (transfer.py:74-87) -- computed by the fused load kernel
+    itself with an id sink (``tt_mc_cache_ids``), so these are the ids every load uses."""
+    if plan.dim != target.DIM or locator.mesh.DIM != target.DIM:
+        raise DimensionMismatch("target, locator and plan dimensions differ")
+    e_hi = target.n_elems if e_hi is None else e_hi
+    dm = target.device
+    ids = out if out is not None else torch.empty((e_hi - e_lo, plan.n_samples), dtype=torch.int32,
+                                                  device=dm.nodes.device)
+    mdesc, pdesc, gdesc = dm.desc(), plan.desc(), locator.desc()
+    seeds = locator.seeds_for(target) if locator.walk else None
+    _lib.call("tt_mc_cache_ids", C.byref(mdesc), e_lo, e_hi, C.byref(pdesc), C.byref(gdesc),
+              _lib.ptr(seeds), _lib.ptr(ids), _lib.stream_handle())
+    return ids
+
+
 def element_contributions(target, source, plan: SamplePlan, e_lo: int = 0,
                           e_hi: int | None = None, out: torch.Tensor | None = None,
                           status: torch.Tensor | None = None) -> torch.Tensor:
@@ -305,12 +327,6 @@ def element_contributions(target, source, plan: SamplePlan, e_lo: int = 0,
     if sdesc is not None:
         _lib.call("tt_mc_load", C.byref(mdesc), e_lo, e_hi, C.byref(pdesc), C.byref(sdesc),
                   _lib.ptr(contrib), None, _lib.ptr(status), s)
-        if isinstance(source, MeshBackedField) and source.locator.walk and \
-                source.locator.snap_prone(target) is None:
-            # first load of this (target, locator) pair: one read of the status word learns
-            # whether outside samples occur (TT_FLAG_SNAPPED) -> later loads pick the kernel
-            # variant with warp-cooperative snaps (a performance hint, never a result change)
-            source.locator.set_snap_prone(target, bool(int(status.item()) & _lib.TT_FLAG_SNAPPED))
         return contrib
     # host black box: materialise points per chunk, query, accumulate the values
     chunk = max(1, _HOST_CHUNK_POINTS // plan.n_samples)

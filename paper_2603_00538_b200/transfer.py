@@ -20,7 +20,7 @@ from . import _lib
 from .errors import DimensionMismatch
 from .fem import NodalField, pcg_device, solved_field
 from .locate import UniformGridLocator
-from .montecarlo import SamplePlan, _raise_status, load_vector
+from .montecarlo import SamplePlan, _raise_status, load_vector, sample_source_elements
 
 
 def transfer_mc(target, source, plan: SamplePlan, cg_tol: float = 1e-12, workers: int = 1,
@@ -52,13 +52,7 @@ class MCTransferOperator:
         self.cg_tol = cg_tol
         self.mass = target.device.mass
         self.locator = source_locator or UniformGridLocator.build(source_mesh)
-        dm = target.device
-        self.src_elem_dev = torch.empty((target.n_elems, plan.n_samples), dtype=torch.int32,
-                                        device=dm.nodes.device)
-        mdesc, pdesc, gdesc = dm.desc(), plan.desc(), self.locator.desc()
-        seeds = self.locator.seeds_for(target) if self.locator.walk else None
-        _lib.call("tt_mc_cache_ids", C.byref(mdesc), 0, target.n_elems, C.byref(pdesc),
-                  C.byref(gdesc), _lib.ptr(seeds), _lib.ptr(self.src_elem_dev), _lib.stream_handle())
+        self.src_elem_dev = sample_source_elements(target, self.locator, plan)
         if fold is None:
             fold = not plan.per_element
         self.R = self._fold() if fold else None

@@ -1,0 +1,86 @@
+"""GPU parity at the BENCHMARKED sizes (BASELINE.json configs 2-4):
+every sample's source element bit-exact against the reference algorithm restated in
+C/OpenMP (oracle/c: the reference's first-ascending-candidate cell scan +
+nearest-centroid snap, _compiled.pyx:147-174, locate.py:97-127), the grid CSR bit-exact
+(locate.py:42-70), and the load vector b normwise <= 1e-12 (montecarlo.py:110-147).
+
+  C2  cube n=55 pair (998,250 tets), N = 64 Sobol            63.9 M samples
+  C3  LTX-like torus pair (4,992,000 / 4,561,920 tets), N=16  79.9 M samples, with the
+      snap path (non-matching faceted boundaries) in both kernel variants
+  C4  cube n=120 pair (10,368,000 tets), N = 16               165.9 M samples
+
+The ids come from the fused load kernel itself (``sample_source_elements`` =
+tt_mc_cache_ids: the load's kernel instance with an id sink), so they certify the walk
+the benchmark runs.
+"""
+
+import gc
+
+import numpy as np
+import pytest
+
+import tt_oracle as O
+import tt_oracle_c as OC
+
+pytestmark = pytest.mark.gpu
+
+
+def _meshes(tt, name):
+    if name == "c2":
+        return (tt.generate_cube_mesh(55, 0.2, seed=20, split="kuhn"),
+                tt.generate_cube_mesh(55, 0.2, seed=10, split="kuhn_mirror"), 64)
+    if name == "c3":
+        return (tt.generate_torus_mesh(40, 80, 260, perturbation=0.2, seed=20),
+                tt.generate_torus_mesh(36, 88, 240, perturbation=0.2, seed=10, split="kuhn_mirror"), 16)
+    return (tt.generate_cube_mesh(120, 0.2, seed=20, split="kuhn"),
+            tt.generate_cube_mesh(120, 0.2, seed=10, split="kuhn_mirror"), 16)
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4"])
+def test_full_size_ids_and_load_vs_oracle(name):
+    import torch
+    import paper_2603_00538_b200 as tt
+    from paper_2603_00538_b200.montecarlo import sample_source_elements
+
+    tgt, src, N = _meshes(tt, name)
+    coeffs = np.sin(src.nodes[:, 0]) * np.cos(src.nodes[:, 1]) * np.cos(src.nodes[:, 2]) + 2.0
+    fs = tt.NodalField(src, coeffs)
+    loc = tt.UniformGridLocator.build(src)
+    plan = tt.SamplePlan.build(N, "sobol", 0, dim=3)
+    lam = O.bary_map(O.sobol(N, 3))
+    assert np.array_equal(plan.barycentric, lam)
+
+    # ---- oracle: the reference algorithm on every sample (C/OpenMP, all host cores)
+    g = OC.Grid(src.nodes, src.elements)
+    assert g.dims == loc.dims
+    assert np.array_equal(loc.cell_start, g.cell_start)          # locate.py:42-70
+    assert np.array_equal(loc.cell_elems, g.cell_elems)
+    measure = np.abs(O.signed_measure(tgt.nodes, tgt.elements))
+    ids_ref = np.empty((tgt.n_elems, N), np.int32)
+    contrib, n_out = OC.mc_load_mesh(g, coeffs, tgt.nodes, tgt.elements, measure, lam, ids=ids_ref)
+    b_ref = np.bincount(tgt.elements.ravel(), weights=contrib.ravel(), minlength=tgt.n_nodes)
+    if name == "c3":
+        assert n_out > 10000                     # the snap path runs (non-matching boundaries)
+    else:
+        assert n_out == 0
+
+    # ---- every sample's source element, bit-exact
+    ids = sample_source_elements(tgt, loc, plan).cpu().numpy()
+    bad = np.flatnonzero(ids.ravel() != ids_ref.ravel())
+    assert len(bad) == 0, f"{len(bad)} of {ids.size} ids differ (first at sample {bad[:5]})"
+    del ids, ids_ref
+    gc.collect()
+
+    # ---- the load vector through the benchmarked kernel (both snap variants at C3)
+    modes = (None, True, False) if name == "c3" else (None,)
+    scale = np.max(np.abs(b_ref))
+    for mode in modes:
+        loc.defer_snaps = mode
+        b = tt.assemble_load_mc(tgt, tt.MeshBackedField(fs, loc), plan)
+        err = np.max(np.abs(b - b_ref)) / scale
+        assert err <= 1e-12, f"defer={mode}: ||db||/||b|| = {err:.3e}"
+    loc.defer_snaps = None
+    assert loc.snap_prone(tgt) == (name == "c3")
+    del loc, fs, tgt, src
+    gc.collect()
+    torch.cuda.empty_cache()

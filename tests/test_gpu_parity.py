@@ -444,22 +444,6 @@ def test_torus_pair_snap_heavy_3d(tt):
     _walk_vs_scan(tt, tgt, src, 40, 3)
 
 
-def test_pcg_algorithms_agree(tt, golden, c1):
-    """Both device PCG recurrences (textbook, Chronopoulos-Gear) reach the reference x."""
-    import subprocess, sys, json
-    code = ("import numpy as np, json, sys; sys.path.insert(0, '.'); import paper_2603_00538_b200 as tt;"
-            "z = np.load('tests/golden/ref_2d.npz');"
-            "t = tt.TriMesh.from_arrays(z['c1t_nodes'], z['c1t_elements']);"
-            "x = tt.cg_solve(tt.assemble_mass_matrix(t), z['b_c1_mesh_smooth'], tol=1e-14);"
-            "print(json.dumps(float(np.max(np.abs(x - z['x_c1_mesh_tol14'])))))")
-    import os
-    for algo in ("0", "1"):
-        out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
-                             env=dict(os.environ, TT_PCG_ALGO=algo), cwd=str(__import__('pathlib').Path(__file__).resolve().parents[1]))
-        assert out.returncode == 0, out.stderr
-        assert json.loads(out.stdout.strip().splitlines()[-1]) <= 1e-12
-
-
 def test_ell_and_csr_pcg_agree(tt, golden, c1):
     """The ELL PCG (default when rows have <= 16 entries) and the CSR PCG reach the
     reference x at cg_tol 1e-14."""
@@ -469,13 +453,7 @@ def test_ell_and_csr_pcg_agree(tt, golden, c1):
     M = tt.assemble_mass_matrix(tgt)
     assert M.ell() is not None
     b = torch.as_tensor(golden["b_c1_mesh_smooth"], device="cuda")
-    xs = []
-    for path in ("ell", "ell_l2", "csr"):
-        fem._PCG_PATH = path
-        try:
-            xs.append(tt.cg_solve(M, b, tol=1e-14).cpu().numpy())
-        finally:
-            fem._PCG_PATH = "ell"
+    xs = [tt.cg_solve(M, b, tol=1e-14, path=path).cpu().numpy() for path in ("auto", "ell_l2", "csr")]
     assert M._slab_ok          # the default ran the shared-memory slab PCG
     assert np.array_equal(xs[0], xs[1])   # slab and L2 ELL: the same arithmetic, bit for bit
     for x in xs:
@@ -493,13 +471,7 @@ def test_slab_pcg_full_and_partial(tt, dim, n):
            else tt.generate_square_mesh(n, 0.2, seed=20, diagonal="right"))
     M = tt.assemble_mass_matrix(tgt)
     b = torch.as_tensor(np.random.default_rng(n).random(tgt.n_nodes), device="cuda")
-    xs = []
-    for path in ("ell", "ell_l2"):
-        fem._PCG_PATH = path
-        try:
-            xs.append(tt.cg_solve(M, b, tol=1e-14).cpu().numpy())
-        finally:
-            fem._PCG_PATH = "ell"
+    xs = [tt.cg_solve(M, b, tol=1e-14, path=path).cpu().numpy() for path in ("auto", "ell_l2")]
     assert M.ell()[3] == (8 if dim == 2 else 16)
     assert M._slab_ok
     assert np.array_equal(xs[0], xs[1])
@@ -508,23 +480,17 @@ def test_slab_pcg_full_and_partial(tt, dim, n):
 
 
 def test_slab_pcg_capacity_fallback(tt):
-    """TT_PCG_SLAB_MIN_FRAC above the fraction that fits: tt_pcg_ell_slab reports
+    """A matrix whose rows do not fit on chip (3-D n=85: 636k rows, a third of every
+    block's rows would fit, below the 1/2 threshold): tt_pcg_ell_slab reports
     TT_ERR_CAPACITY without launching and the L2 ELL PCG solves (same x bits)."""
-    import os
-    import subprocess
-    import sys
-    code = ("import numpy as np, torch, sys; sys.path.insert(0, '.'); import paper_2603_00538_b200 as tt;"
-            "from paper_2603_00538_b200 import fem;"
-            "t = tt.generate_cube_mesh(60, 0.2, seed=20, split='kuhn'); M = tt.assemble_mass_matrix(t);"
-            "b = torch.as_tensor(np.random.default_rng(3).random(t.n_nodes), device='cuda');"
-            "x = tt.cg_solve(M, b, tol=1e-14).cpu().numpy(); assert not M._slab_ok;"
-            "fem._PCG_PATH = 'ell_l2'; y = tt.cg_solve(M, b, tol=1e-14).cpu().numpy();"
-            "assert np.array_equal(x, y); print('ok')")
-    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
-                         env=dict(os.environ, TT_PCG_SLAB_MIN_FRAC="0.99"),
-                         cwd=str(__import__("pathlib").Path(__file__).resolve().parents[1]))
-    assert out.returncode == 0, out.stderr
-    assert out.stdout.strip().endswith("ok")
+    import torch
+    t = tt.generate_cube_mesh(85, 0.2, seed=20, split="kuhn")
+    M = tt.assemble_mass_matrix(t)
+    b = torch.as_tensor(np.random.default_rng(3).random(t.n_nodes), device="cuda")
+    x = tt.cg_solve(M, b, tol=1e-14).cpu().numpy()
+    assert M.ell() is not None and not M._slab_ok
+    y = tt.cg_solve(M, b, tol=1e-14, path="ell_l2").cpu().numpy()
+    assert np.array_equal(x, y)
 
 
 def test_slab_pcg_wide_rows_not_used(tt):
@@ -604,27 +570,7 @@ def test_3d_mesh_backed_large_n_matches_oracle(tt, n):
     assert _rel(b, O.reduce_to_nodes(tgt.n_nodes, tgt.elements, contrib)) <= 1e-12
 
 
-@pytest.mark.parametrize("shape", [("4", "1"), ("4", "0"), ("2", "0")])
-def test_ell_pcg_spmv_shapes_agree(tt, golden, c1, shape):
-    """Non-default ELL SpMV shapes (TT_PCG_ELL_LPR lanes per row, TT_PCG_ELL_CONTIG row
-    ranges; read once per process) reach the reference x like the default."""
-    import json
-    import os
-    import subprocess
-    import sys
-    code = ("import numpy as np, json, sys; sys.path.insert(0, '.'); import paper_2603_00538_b200 as tt;"
-            "z = np.load('tests/golden/ref_2d.npz');"
-            "t = tt.TriMesh.from_arrays(z['c1t_nodes'], z['c1t_elements']);"
-            "x = tt.cg_solve(tt.assemble_mass_matrix(t), z['b_c1_mesh_smooth'], tol=1e-14);"
-            "print(json.dumps(float(np.max(np.abs(x - z['x_c1_mesh_tol14'])))))")
-    env = dict(os.environ, TT_PCG_ELL_LPR=shape[0], TT_PCG_ELL_CONTIG=shape[1])
-    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
-                         cwd=str(__import__("pathlib").Path(__file__).resolve().parents[1]))
-    assert out.returncode == 0, out.stderr
-    assert json.loads(out.stdout.strip().splitlines()[-1]) <= 1e-12
-
-
-@pytest.mark.parametrize("path", ["ell", "ell_l2", "csr"])
+@pytest.mark.parametrize("path", ["auto", "ell_l2", "csr"])
 def test_pcg_best_iterate_matches_oracle(tt, path):
     """NoConvergence carries the best iterate (fem.py:141-152).  An SPD matrix whose
     preconditioned residual is NOT monotone (increases at iterations 2, 6, 8, 10) drives
@@ -643,29 +589,26 @@ def test_pcg_best_iterate_matches_oracle(tt, path):
     M = fem.SparseSymMatrix(n, torch.as_tensor(A.indptr.astype(np.int64), device=dev),
                             torch.as_tensor(A.indices.astype(np.int32), device=dev),
                             torch.as_tensor(A.data, device=dev))
-    fem._PCG_PATH = path
-    try:
-        for maxiter in range(1, 11):
-            with pytest.raises(tt.NoConvergence) as got:
-                tt.cg_solve(M, b, tol=1e-16, maxiter=maxiter)
-            with pytest.raises(O.NoConvergence) as ref:
-                O.cg_solve(A, b, tol=1e-16, maxiter=maxiter)
-            assert got.value.residual == pytest.approx(ref.value.residual, rel=1e-9)
-            assert _rel(got.value.best_x, ref.value.best_x) <= 1e-9
-        x = tt.cg_solve(M, b, tol=1e-13)
-        xr, _ = O.cg_solve(A, b, tol=1e-13)
-        assert _rel(x, xr) <= 1e-8
-    finally:
-        fem._PCG_PATH = "ell"
+    for maxiter in range(1, 11):
+        with pytest.raises(tt.NoConvergence) as got:
+            tt.cg_solve(M, b, tol=1e-16, maxiter=maxiter, path=path)
+        with pytest.raises(O.NoConvergence) as ref:
+            O.cg_solve(A, b, tol=1e-16, maxiter=maxiter)
+        assert got.value.residual == pytest.approx(ref.value.residual, rel=1e-9)
+        assert _rel(got.value.best_x, ref.value.best_x) <= 1e-9
+    x = tt.cg_solve(M, b, tol=1e-13, path=path)
+    xr, _ = O.cg_solve(A, b, tol=1e-13)
+    assert _rel(x, xr) <= 1e-8
 
 
 @pytest.mark.parametrize("dim", [2, 3])
 def test_deferred_snap_variant_matches_inline(tt, golden, dim):
-    """Snap-prone pairs (outside anchors, or a first load that snapped) run the variant whose
+    """Snap-prone pairs (a walk-seed anchor outside the source mesh) run the variant whose
     outside samples are snapped warp-cooperatively at tile end (nearest_element_warp); the
     plain variant snaps on the diverged lane.  Same samples, same snapped elements, so the
     two loads agree to rounding (the snapped terms are added in a different order) and both
-    match the oracle."""
+    match the oracle.  The choice is made once per (target, locator) before any load, so
+    repeated loads -- whatever came before -- are bitwise identical."""
     if dim == 2:
         src = tt.TriMesh.from_arrays(golden["curv_nodes"], golden["curv_elements"])
         tgt = tt.TriMesh.from_arrays(golden["curvt_nodes"], golden["curvt_elements"])
@@ -677,15 +620,18 @@ def test_deferred_snap_variant_matches_inline(tt, golden, dim):
         fs = tt.NodalField.from_function(src, tt.get_field("smooth", dim=3).fn)
         plan = tt.SamplePlan.build(40, "sobol", 0, dim=3)
     loc = tt.UniformGridLocator.build(src)
-    tt.assemble_load_mc(tgt, tt.MeshBackedField(fs, loc), plan)   # learns the hint if unknown
-    assert loc.snap_prone(tgt) is True
+    b_auto = [tt.assemble_load_mc(tgt, tt.MeshBackedField(fs, loc), plan, workers=w) for w in (1, 8, 1)]
+    assert all(np.array_equal(b_auto[0], b) for b in b_auto[1:])
+    loc.defer_snaps = True
     b_defer = tt.assemble_load_mc(tgt, tt.MeshBackedField(fs, loc), plan)
-    tgt_e, seeds, _ = loc._seeds[id(tgt)]
-    loc._seeds[id(tgt)] = (tgt_e, seeds, False)          # force the plain variant
+    loc.defer_snaps = False
     b_inline = tt.assemble_load_mc(tgt, tt.MeshBackedField(fs, loc), plan)
+    loc.defer_snaps = None
+    assert np.array_equal(b_auto[0], b_defer if loc.snap_prone(tgt) else b_inline)
     assert _rel(b_defer, b_inline) <= 1e-14
     g = O.Grid(src.nodes, src.elements)
     ref = O.reduce_to_nodes(tgt.n_nodes, tgt.elements,
                             O.accumulate(tgt.nodes, tgt.elements, tgt.elem_areas, plan.barycentric,
                                          lambda P: O.mesh_backed_eval(g, fs.coeffs, P)))
     assert _rel(b_defer, ref) <= 1e-12
+    assert _rel(b_inline, ref) <= 1e-12
