@@ -16,13 +16,15 @@ value = S / t_step (S = E_t * N samples per step, all ranks); ms_per_step = wall
 per coupling step.  e2e = the same through the public API (transfer_mc on a NodalField
 whose coefficients are copied H2D from pinned memory each step, x read back D2H).
 
-Multi-GPU (torchrun): target elements are split into contiguous ranges (strong
-scaling); source mesh, grid and field are replicated; partial b vectors are summed
-with one NCCL all-reduce; the PCG is replicated per rank.
+Multi-GPU (torchrun): the target is split into Morton-ordered element parts (strong
+scaling); source mesh, grid and field are replicated; interface element contributions
+go to the nodes' owners (NCCL all-to-all), which sum them in the single-GPU order; the
+PCG is row-partitioned (halo exchange + one 3-scalar all-reduce per iteration) or
+replicated (--solve).  c5 reports wall time per coupling step (ms/step).
 
 ``--impl reference``: the reference algorithm on the host CPU for the same config
-(the reference is 2-D only, so 3-D runs the oracle restatement: kind "port"), bounded
-sample, rank 0 only.
+(the reference is 2-D only, so 3-D runs the C/OpenMP + scipy restatement: kind "port"),
+every step timed in full, rank 0 only.
 """
 
 from __future__ import annotations
@@ -56,6 +58,11 @@ def parse_args():
     ap.add_argument("--sweep", default="16,32,64,128,256")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="N>1 collectives (gloo: host-staged, for boxes with fewer GPUs than ranks)")
+    ap.add_argument("--solve", default="auto", choices=["auto", "distributed", "replicated"],
+                    help="N>1 PCG: row-partitioned (halo exchange + 1 all-reduce/iteration) or "
+                         "replicated on every rank; auto = distributed from 1M target nodes")
     return ap.parse_args()
 
 
@@ -87,14 +94,18 @@ def mesh_names(args):
     return f"cube n={n} kuhn jitter0.2 seed20", f"cube n={n} kuhn_mirror jitter0.2 seed10"
 
 
-def workload_config(args, world):
+def workload_config(args, world, coupling=None):
     tname, sname = mesh_names(args)
+    part = "single GPU"
+    if world > 1:
+        part = (f"Morton-ordered target-element parts x{world}, owner-summed interface loads (all-to-all), "
+                f"{coupling.solve_mode if coupling else args.solve} PCG")
     return {"workload": WORKLOADS[args.config],
             "target": tname, "source": sname,
             "field": ("sin(x)cos(y)+2" if args.config == "c1" else "sin(x)cos(y)cos(z)+2")
                      + " (P1 interpolant on source)",
             "samples_per_elem": args.samples, "plan": args.mode, "cg_tol": 1e-12,
-            "partition": f"contiguous target-element ranges x{world}", "l2": "flushed between timed steps",
+            "partition": part, "l2": "flushed between timed steps (256 MB write)",
             "parallelism": f"dp{world}"}
 
 
@@ -214,56 +225,73 @@ def fp64_peak(tt, torch):
     return best
 
 
+def _ncu_evidence():
+    """The newest committed ncu summary of the dominant kernel (profiles/rNN/)."""
+    for rnd in sorted((ROOT / "profiles").glob("r[0-9][0-9]"), reverse=True):
+        f = rnd / "ncu_dominant_kernel.json"
+        if f.exists():
+            try:
+                return json.loads(f.read_text()), str(f.relative_to(ROOT))
+            except Exception:
+                pass
+    return {}, None
+
+
 def run_ours(args):
-    import numpy as np
     import torch
     import torch.distributed as dist
     import paper_2603_00538_b200 as tt
     from paper_2603_00538_b200.fem import decode_result, pcg_device
-    from paper_2603_00538_b200.montecarlo import load_vector, _raise_status
+    from paper_2603_00538_b200.montecarlo import load_vector, _raise_status, element_contributions
     from paper_2603_00538_b200 import _lib
+    from paper_2603_00538_b200.dist import DistributedCoupling, DistributedMCOperator
 
     rank, world, local = dist_env()
-    # TT_BENCH_BACKEND=gloo exercises the N>1 code path on a box with fewer GPUs than ranks:
-    # host-side collectives, ranks share devices round-robin, no kernel waits on another rank
-    backend = os.environ.get("TT_BENCH_BACKEND", "nccl")
-    if backend == "gloo":
+    # --backend gloo exercises the N>1 code path on a box with fewer GPUs than ranks:
+    # host-staged collectives, ranks share devices round-robin, no kernel waits on another rank
+    if args.backend == "gloo":
         local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        if backend == "nccl":
+        if args.backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
-            dist.init_process_group(backend)
+            dist.init_process_group("gloo")
     tgt, src, fs, loc, mass = build_problem(args, tt)
     box = tt.MeshBackedField(fs, loc)
-    from paper_2603_00538_b200.dist import partition_elements, reduce_load
     E = tgt.n_elems
-    e_lo, e_hi = partition_elements(E, world, rank)
+    c5 = args.config == "c5"
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
     status = _lib.status_word()
-
+    coupling = DistributedCoupling(tgt, solve=args.solve) if world > 1 else None
     ops = {}
 
+    def operator(plan):
+        if plan.n_samples not in ops:   # localisation + fold once per plan (untimed init)
+            ops[plan.n_samples] = (DistributedMCOperator(coupling, src, plan, source_locator=loc)
+                                   if coupling else tt.MCTransferOperator(tgt, src, plan, source_locator=loc))
+            torch.cuda.synchronize()
+        return ops[plan.n_samples]
+
     def step(plan, ev=None):
+        """One coupling step; ev = (start, end-of-load) events."""
         if ev is not None:
             ev[0].record()
         fs._packed = fs._grad = None   # new coefficients each coupling step: repack (timed)
-        if args.config == "c5":
-            if plan.n_samples not in ops:   # localisation cached once per plan (untimed init)
-                ops[plan.n_samples] = tt.MCTransferOperator(tgt, src, plan, source_locator=loc)
-                torch.cuda.synchronize()
-            b = ops[plan.n_samples].load(fs, check=False)
+        if coupling is None:
+            b = operator(plan).load(fs, check=False) if c5 else \
+                load_vector(tgt, box, plan, deterministic=True, check=False, status=status)
+            if ev is not None:
+                ev[1].record()
+            x, best_x, res = pcg_device(mass, b, tol=1e-12)
         else:
-            b = load_vector(tgt, box, plan, e_lo, e_hi, deterministic=True, check=False, status=status)
-        if ev is not None:
-            ev[1].record()
-        reduce_load(b)                      # NCCL all-reduce of the partial b (N>1)
-        # (TT_DIST_REDUCE=p2p: the e2e leg uses PeerCoupling's peer-memory gather instead)
-        x, best_x, res = pcg_device(mass, b, tol=1e-12)
+            b = operator(plan).load_owned(fs) if c5 else coupling.load_owned(box, plan, status)
+            if ev is not None:
+                ev[1].record()
+            x, best_x, res = coupling.solve_owned(b, tol=1e-12)
         return x, res
 
-    def timed(plan, steps, warmup, kernel_events=True):
+    def timed(plan, steps, warmup):
         for _ in range(warmup):
             step(plan)
         torch.cuda.synchronize()
@@ -276,7 +304,7 @@ def run_ours(args):
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             ks = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
             s.record()
-            x, res = step(plan, ks if kernel_events else None)
+            x, res = step(plan, ks)
             e.record()
             tot.append((s, e))
             ker.append(ks)
@@ -284,8 +312,14 @@ def run_ours(args):
         if world > 1:
             dist.barrier()
         ms = sum(s.elapsed_time(e) for s, e in tot)
-        kms = [a.elapsed_time(b) for a, b in ker] if kernel_events else []
+        kms = [a.elapsed_time(b) for a, b in ker]
         return ms, kms, x, res
+
+    def max_ranks(v):
+        t = torch.tensor([float(v)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     D = tgt.DIM
     plan = tt.SamplePlan.build(args.samples, args.mode, 0, dim=D)
@@ -294,65 +328,53 @@ def run_ours(args):
     r = decode_result(res)
     _raise_status(int(status.item()))
     assert r.converged, "PCG did not converge"
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_step = float(t.item()) / args.steps
+    ms_step = max_ranks(ms) / args.steps
     S = E * args.samples
-    value = S / (ms_step * 1e-3)
-    load_ms = statistics.mean(kms)   # mc_load + reduce_nodes, per step
-    if world > 1:
-        lt = torch.tensor([load_ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(lt, op=dist.ReduceOp.MAX)
-        load_ms = float(lt.item())
+    load_ms = max_ranks(statistics.mean(kms))   # load phase per step, slowest rank
 
-    # --- dominant kernel alone (mc_load_kernel), CUDA events on the launch stream
-    from paper_2603_00538_b200.montecarlo import element_contributions
-    contrib = torch.empty((e_hi - e_lo, D + 1), dtype=torch.float64, device="cuda")
+    # --- dominant kernel alone, CUDA events on the launch stream
+    sub = coupling.sub if coupling else tgt
+    E_loc = sub.n_elems
+    contrib = torch.empty((max(E_loc, 1), D + 1), dtype=torch.float64, device="cuda")
     kt = []
     for i in range(args.warmup + args.steps):
         flush.zero_()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
-        if args.config == "c5":
-            ops[plan.n_samples].load(fs, check=False)
+        if c5:
+            o = operator(plan)
+            (o.load_owned(fs) if coupling else o.load(fs, check=False))
         else:
-            element_contributions(tgt, box, plan, e_lo, e_hi, out=contrib, status=status)
+            element_contributions(sub, box, plan, out=contrib, status=status)
         e.record()
         if i >= args.warmup:
             kt.append((s, e))
     torch.cuda.synchronize()
     k_ms = statistics.mean(a.elapsed_time(b) for a, b in kt)
-    E_loc = e_hi - e_lo
     n_cells = loc.dims[0] * loc.dims[1] * loc.dims[2]
     K = D + 1
     alg_bytes = (E_loc * (4 * K + 8 * D * K + 8 + 8 * K)       # target conn, coords, measure, contrib
                  + 8 * (n_cells + 1) + 4 * int(loc.cell_elems_dev.numel())
                  + src.n_elems * (8 * (D * D + D) + 4 * K) + 8 * src.n_nodes)
-    folded = args.config == "c5" and ops[plan.n_samples].R is not None
-    if folded:
+    nnz_r = 0
+    if c5:
         # b = R c: CSR row pointers, column indices and values, c and b, each once
-        nnz_r = int(ops[plan.n_samples].R[2].numel())
-        alg_bytes = 8 * (tgt.n_nodes + 1) + 12 * nnz_r + 8 * src.n_nodes + 8 * tgt.n_nodes
-    peak_hbm = None
+        R = (operator(plan).op if coupling else operator(plan)).R
+        nnz_r = int(R[2].numel())
+        n_rows = int(R[0].numel()) - 1
+        alg_bytes = 8 * (n_rows + 1) + 12 * nnz_r + 8 * src.n_nodes + 8 * n_rows
     try:
-        peak_hbm = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"]
-        peak_src = "measured"
+        peak_hbm, peak_src = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"], "measured"
     except Exception:
         peak_hbm, peak_src = 6650.0, "fallback"
     achieved = alg_bytes / (k_ms * 1e-3) / 1e9
     fp64 = fp64_peak(tt, torch)
-    # ncu evidence for the same kernel and config (profiles/, one --set full capture):
-    # DRAM traffic per launch and SASS-counted FP64 flops per sample
-    ncu = {}
-    try:
-        ncu = json.loads((ROOT / "profiles" / "r01" / "ncu_dominant_kernel.json").read_text())
-    except Exception:
-        pass
-    same = args.config == "c2" and args.samples == 64 and world == 1 and args.mode == "sobol"
+    # ncu evidence for the same kernel and config (profiles/rNN, one --set full capture)
+    ncu, ncu_src = _ncu_evidence()
+    same = (args.config == "c2" and args.samples == 64 and world == 1 and args.mode == "sobol"
+            and "C2" in ncu.get("kernel", ""))
     traffic = ncu.get("dram_bytes_per_launch") if same else None
-    fp64_fl = (2.0 * nnz_r if folded                 # one FMA per nonzero of R
-               else ncu.get("fp64_flops_per_sample", 0.0) * E_loc * args.samples)
+    fp64_fl = 2.0 * nnz_r if c5 else ncu.get("fp64_flops_per_sample", 0.0) * E_loc * args.samples
     fp64_achieved = fp64_fl / (k_ms * 1e-3) / 1e12 if fp64_fl else None
 
     # --- e2e: public API, pinned host coefficients in, x out, every step
@@ -360,28 +382,24 @@ def run_ours(args):
     x_host = torch.empty(tgt.n_nodes, dtype=torch.float64).pin_memory()
     c_dev = torch.empty(src.n_nodes, dtype=torch.float64, device="cuda")
 
-    from paper_2603_00538_b200.dist import DistributedCoupling, PeerCoupling
-    coupling = None
-    if world > 1:
-        coupling = (PeerCoupling(tgt, rank, world) if os.environ.get("TT_DIST_REDUCE") == "p2p"
-                    else DistributedCoupling(tgt, rank, world))
-
     def e2e_step():
         # the calls a user makes: NodalField from host coefficients (pinned H2D), then
         # transfer_mc / MCTransferOperator.apply / DistributedCoupling.step, x back to host
         c_dev.copy_(c_host, non_blocking=True)
         field = tt.NodalField(src, c_dev)
-        # (transfer_mc / apply take the pinned host buffer as `out`: the x D2H is queued
-        # before the call's one synchronisation and `.coeffs` is a view of it)
-        if args.config == "c5":
-            xh = ops[plan.n_samples].apply(field, out=x_host).coeffs
-        elif coupling is not None:
-            xx = coupling.step(tt.MeshBackedField(field, loc), plan, tol=1e-12)
+        if coupling is None:
+            # (transfer_mc / apply take the pinned host buffer as `out`: the x D2H is queued
+            # before the call's one synchronisation and `.coeffs` is a view of it)
+            if c5:
+                xh = operator(plan).apply(field, out=x_host).coeffs
+            else:
+                xh = tt.transfer_mc(tgt, tt.MeshBackedField(field, loc), plan, cg_tol=1e-12, out=x_host).coeffs
+        else:
+            xx = operator(plan).apply(field) if c5 else \
+                coupling.step(tt.MeshBackedField(field, loc), plan, tol=1e-12)
             x_host.copy_(xx, non_blocking=True)
             torch.cuda.current_stream().synchronize()
             xh = x_host
-        else:
-            xh = tt.transfer_mc(tgt, tt.MeshBackedField(field, loc), plan, cg_tol=1e-12, out=x_host).coeffs
         assert xh.shape[0] == tgt.n_nodes
     for _ in range(args.warmup):
         e2e_step()
@@ -397,69 +415,72 @@ def run_ours(args):
         e.record()
         ev.append((s, e))
     torch.cuda.synchronize()
-    e2e_ms = torch.tensor([sum(a.elapsed_time(b) for a, b in ev) / args.steps], dtype=torch.float64,
-                          device="cuda")
-    if world > 1:
-        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
-    e2e_ms = float(e2e_ms.item())
+    e2e_ms = max_ranks(sum(a.elapsed_time(b) for a, b in ev) / args.steps)
 
     # --- samples/element sweep (same step, fewer repetitions)
     sweep = {}
-    if args.sweep:
+    if args.sweep and not c5:
         for n in [int(v) for v in args.sweep.split(",") if v]:
             p = tt.SamplePlan.build(n, args.mode, 0, dim=D)
-            m, km, _, rr = timed(p, max(2, args.steps // 3), 1)
-            tt_ = torch.tensor([m / max(2, args.steps // 3)], dtype=torch.float64, device="cuda")
-            if world > 1:
-                dist.all_reduce(tt_, op=dist.ReduceOp.MAX)
-            sweep[str(n)] = {"ms_per_step": round(float(tt_.item()), 4),
-                             "samples_per_s": E * n / (float(tt_.item()) * 1e-3),
-                             "load_ms": round(statistics.mean(km), 4)}
+            reps = max(2, args.steps // 3)
+            m, km, _, rr = timed(p, reps, 1)
+            m = max_ranks(m / reps)
+            sweep[str(n)] = {"ms_per_step": round(m, 4), "samples_per_s": E * n / (m * 1e-3),
+                             "load_ms": round(max_ranks(statistics.mean(km)), 4)}
 
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args, tgt, src, fs.coeffs, seconds=args.cpu_seconds)
+    if rank == 0 and not args.no_cpu_baseline and not c5:
+        cpu = cpu_baseline(args, seconds=args.cpu_seconds)
     if rank == 0:
-        line = {
-            "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (generated meshes, analytic field interpolated on the source)",
-            "config": workload_config(args, world),
-            "load_ms_per_step": load_ms, "pcg_iterations": int(r.iterations),
-            # SURVEY 8(d)'s sample throughput S / t_load (load phase: pack + fused kernel + node
-            # gather, slowest rank); `value` above is the stricter S / t_step with the PCG included
-            "sample_throughput": {"value": S / (load_ms * 1e-3), "unit": "samples/s",
-                                  "phase": "load (source pack + fused MC kernel + node gather), max over ranks"},
-            "e2e": {"value": S / (e2e_ms * 1e-3), "unit": "samples/s", "ms_per_step": e2e_ms,
-                    "h2d_bytes_per_step": src.n_nodes * 8, "d2h_bytes_per_step": tgt.n_nodes * 8,
+        per_step = 2 if c5 else 4      # c5: spmv_rect + pcg; else pack_grad + mc kernel + reduce + pcg
+        if world > 1:
+            per_step += 1              # owner-side gather of the exchanged rows
+        if c5:
+            metric_val, unit, hib = ms_step, "ms/step", False
+            e2e = {"value": e2e_ms, "unit": "ms/step"}
+        else:
+            metric_val, unit, hib = S / (ms_step * 1e-3), "samples/s", True
+            e2e = {"value": S / (e2e_ms * 1e-3), "unit": "samples/s"}
+        e2e.update({"ms_per_step": e2e_ms, "h2d_bytes_per_step": src.n_nodes * 8,
+                    "d2h_bytes_per_step": tgt.n_nodes * 8,
                     "api": "NodalField(pinned H2D) -> transfer_mc(MeshBackedField, out=pinned x).coeffs | "
                            "MCTransferOperator.apply(field, out=pinned x).coeffs (c5) | "
-                           "DistributedCoupling.step + x D2H (N>1)"},
+                           "DistributedCoupling.step / DistributedMCOperator.apply + x D2H (N>1)"})
+        line = {
+            "metric": METRIC, "value": metric_val, "unit": unit, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": hib, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (generated meshes, analytic field interpolated on the source)",
+            "config": workload_config(args, world, coupling),
+            "load_ms_per_step": load_ms, "pcg_iterations": int(r.iterations),
+            # SURVEY 8(d)'s sample throughput S / t_load (load phase, slowest rank); `value`
+            # is the stricter S / t_step with the PCG included (c5: ms per step)
+            "sample_throughput": {"value": S / (load_ms * 1e-3), "unit": "samples/s",
+                                  "phase": ("R @ c over the folded load matrix (no samples touched)" if c5 else
+                                            "load (source pack + fused MC kernel + node gather), max over ranks")},
+            "e2e": e2e,
             "roofline": {"bound": "hbm",
-                         "kernel": ("spmv_rect (folded R @ c)" if folded else "mc_load_kernel<3,SHARED,CACHED>")
-                         if args.config == "c5" else "mc_mesh_kernel<3,SHARED,G,spec>",
+                         "kernel": "spmv_rect (folded R @ c)" if c5 else "mc_mesh_kernel<3,SHARED,G,SLOT>",
                          "achieved": achieved, "peak": peak_hbm, "unit": "GB/s",
                          "frac": achieved / peak_hbm, "peak_source": peak_src,
                          "traffic": traffic, "kernel_ms": k_ms, "algorithmic_bytes": alg_bytes,
-                         "traffic_source": "profiles/r01/ncu_dominant_kernel.json" if traffic else None,
+                         "traffic_source": ncu_src if traffic else None,
                          "fp64": {"achieved": fp64_achieved, "peak": fp64, "unit": "TFLOP/s",
                                   "frac": fp64_achieved / fp64 if fp64_achieved else None,
-                                  "flops_per_sample": (2.0 * nnz_r / (E_loc * args.samples) if folded
+                                  "flops_per_sample": (2.0 * nnz_r / (E_loc * args.samples) if c5
                                                        else ncu.get("fp64_flops_per_sample")),
                                   "peak_source": "measured in this run (tt_fp64_peak_probe, DFMA)"},
                          "l1_data_pipe_pct_ncu": ncu.get("l1_data_pipe_pct") if same else None,
+                         "l1_wavefronts_per_sample_ncu": ncu.get("l1_wavefronts_per_sample") if same else None,
                          "note": ("streaming CSR SpMV over the folded load matrix R (12 B per nonzero); "
-                                  "the PCG that follows dominates the step") if folded else
-                                 "fused gather kernel: < 1 compulsory HBM byte per sample (DRAM 2 %); "
-                                 "limited by dependent-load latency and the L1 data pipe (ncu)"},
+                                  "the PCG that follows dominates the step") if c5 else
+                                 "fused gather kernel: < 1 compulsory HBM byte per sample; bound by the "
+                                 "L1 data pipe (LSU wavefronts, ncu) and dependent-load latency"},
             "fp64_peak_tflops": fp64,
             "sweep": sweep,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
-            # per step: c5 folded = spmv_rect + pcg_ell; c5 cached = pack_coeffs + mc_load +
-            # reduce_nodes + pcg_ell; else pack_grad + mc kernel + reduce_nodes + pcg_ell
-            "gpu_launches": (2 if folded else 4) * args.steps,
+            "gpu_launches": per_step * args.steps,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -467,70 +488,117 @@ def run_ours(args):
 
 
 # --------------------------------------------------------------------- CPU
-def cpu_baseline(args, tgt, src, coeffs, seconds=12.0):
-    """The reference MC load restated in C/OpenMP (oracle/c, all host cores) on a bounded
-    sample of the same workload: grid built by the oracle (untimed setup), then as many
-    512-element chunks as fit in ``seconds``."""
+def _ref_inputs(args):
+    """The config's meshes and source coefficients built WITHOUT the product package:
+    oracle/meshgen.py (tests pin it to the product's generators) + oracle numpy geometry."""
     import numpy as np
     sys.path.insert(0, str(ROOT / "oracle"))
+    import meshgen
+    if args.config == "c1":
+        # 2-D: the reference's own generator (oracle/_ref), as the reference arm runs it
+        sys.path.insert(0, str(ROOT / "oracle" / "_ref"))
+        import tritransfer as ref
+        t = ref.generate_square_mesh(707, 0.2, seed=20, diagonal="right")
+        s_ = ref.generate_square_mesh(707, 0.2, seed=10, diagonal="left")
+        sn = np.asarray(s_.nodes)
+        return (np.asarray(t.nodes), np.asarray(t.elements), sn, np.asarray(s_.elements),
+                np.sin(sn[:, 0]) * np.cos(sn[:, 1]) + 2.0)
+    if args.config == "c3":
+        tn, te = meshgen.torus(40, 80, 260, 0.2, 20, "kuhn")
+        sn, se = meshgen.torus(36, 88, 240, 0.2, 10, "kuhn_mirror")
+    else:
+        n = 120 if args.config == "c4" else args.n
+        tn, te = meshgen.cube(n, 0.2, 20, "kuhn")
+        sn, se = meshgen.cube(n, 0.2, 10, "kuhn_mirror")
+    coeffs = np.sin(sn[:, 0]) * np.cos(sn[:, 1]) * np.cos(sn[:, 2]) + 2.0
+    return tn, te, sn, se, coeffs
+
+
+def cpu_baseline(args, seconds=12.0):
+    """The reference MC load restated in C/OpenMP (oracle/c, all host cores) on a bounded
+    sample of the same workload: grid built by the oracle (untimed setup), then as many
+    element chunks as fit in ``seconds``."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import numpy as np
     import tt_oracle as O
     import tt_oracle_c as OC
+    tn, te, sn, se, coeffs = _ref_inputs(args)
     t0 = time.perf_counter()
-    g = O.Grid(src.nodes, src.elements)
+    g = OC.Grid(sn, se)
     setup_s = time.perf_counter() - t0
-    lam = O.bary_map(O.sobol(args.samples, tgt.DIM))
-    coeffs = np.asarray(coeffs)
+    lam = O.bary_map(O.sobol(args.samples, tn.shape[1]))
+    meas = np.abs(O.signed_measure(tn, te))
     threads = os.cpu_count() or 1
-    OC.mc_load_mesh(g, coeffs, tgt.nodes, tgt.elements, tgt.elem_areas, lam, 0, 512, threads)  # warm
+    OC.mc_load_mesh(g, coeffs, tn, te, meas, lam, 0, 512, threads)  # warm
     n_el, done, t_used = 4096, 0, 0.0
-    while t_used < seconds and done < tgt.n_elems:
-        lo, hi = done, min(done + n_el, tgt.n_elems)
+    while t_used < seconds and done < len(te):
+        lo, hi = done, min(done + n_el, len(te))
         t = time.perf_counter()
-        OC.mc_load_mesh(g, coeffs, tgt.nodes, tgt.elements, tgt.elem_areas, lam, lo, hi, threads)
+        OC.mc_load_mesh(g, coeffs, tn, te, meas, lam, lo, hi, threads)
         t_used += time.perf_counter() - t
         done = hi
         n_el = min(n_el * 2, 262144)
     sps = done * args.samples / t_used
     return {"value": sps, "unit": "samples/s", "cores": threads, "kind": "port",
             "sample": f"MC load (locate+snap+P1 eval+accumulate) on target elements [0, {done}) of "
-                      f"{tgt.n_elems}, N={args.samples}: {done * args.samples} samples in {t_used:.1f} s; "
+                      f"{len(te)}, N={args.samples}: {done * args.samples} samples in {t_used:.1f} s; "
                       f"grid setup {setup_s:.1f} s untimed",
             "impl": "oracle/c/tt_oracle_c.c: C/OpenMP restatement of the reference MC path "
                     "(the reference itself is 2-D only); -O2, no FMA, 512-element chunks"}
 
 
 def run_reference(args):
+    """The reference's algorithm on the host CPU, every step of --warmup + --steps timed in
+    full: the C/OpenMP port of the MC load over ALL target elements (all host cores), the
+    node reduction in np.add.at order, and the reference's Jacobi PCG (scipy CSR, the
+    oracle restatement of fem.py:113-152) on that step's b.  Inputs are built without the
+    product package (oracle/meshgen.py).  C1 (2-D) runs the reference package itself."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    import numpy as np
-    sys.path.insert(0, str(ROOT))
-    import paper_2603_00538_b200.mesh as M   # host-only mesh generators (no GPU use)
-    sys.path.insert(0, str(ROOT / "oracle"))
-    import tt_oracle as O
     if args.config == "c1" and (ROOT / "oracle" / "_ref" / "tritransfer").exists():
         return run_reference_real(args, world)
-    tgt, src = build_meshes(args, M)
-
-    coeffs = np.sin(src.nodes[:, 0]) * np.cos(src.nodes[:, 1]) * np.cos(src.nodes[:, 2]) + 2
-    cpu = cpu_baseline(args, tgt, src, coeffs, seconds=args.cpu_seconds)
-    # the PCG on the full target mesh (scipy CSR, the reference's solver) once
-    t = time.perf_counter()
-    Mm = O.mass_matrix(tgt.n_nodes, tgt.elements, tgt.elem_areas, 3)
-    rhs = Mm @ np.ones(tgt.n_nodes)
-    O.cg_solve(Mm, rhs, tol=1e-12)
-    cg_s = time.perf_counter() - t
-    S = tgt.n_elems * args.samples
-    step_s = S / cpu["value"] + cg_s
+    if args.config == "c5":
+        print(json.dumps({"impl": "reference", "unavailable": "C5 needs the reference's load-matrix fold "
+                          "(transfer.py:88-110) in 3-D, which the 2-D-only reference has no CPU port of here"}))
+        return
+    import numpy as np
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import tt_oracle as O
+    import tt_oracle_c as OC
+    t0 = time.perf_counter()
+    tn, te, sn, se, coeffs = _ref_inputs(args)
+    g = OC.Grid(sn, se)
+    meas = np.abs(O.signed_measure(tn, te))
+    Mm = O.mass_matrix(len(tn), te, meas, 3)
+    lam = O.bary_map(O.sobol(args.samples, 3))
+    setup = time.perf_counter() - t0
+    threads = os.cpu_count() or 1
+    times, iters = [], []
+    for i in range(args.warmup + args.steps):
+        t = time.perf_counter()
+        contrib, _ = OC.mc_load_mesh(g, coeffs, tn, te, meas, lam, threads=threads)
+        b = np.bincount(te.ravel(), weights=contrib.ravel(), minlength=len(tn))   # np.add.at order
+        x, it = O.cg_solve(Mm, b, tol=1e-12)
+        dt = time.perf_counter() - t
+        if i >= args.warmup:
+            times.append(dt)
+            iters.append(it)
+    step_s = statistics.mean(times)
+    S = len(te) * args.samples
     value = S / step_s
-    cpu_line = dict(cpu)
-    cpu_line["value"] = value
-    cpu_line["sample"] += f"; step = extrapolated load + full-size PCG ({cg_s:.2f} s)"
+    cpu = {"value": value, "unit": "samples/s", "cores": threads, "kind": "port",
+           "sample": f"{args.steps} full coupling steps of {S} samples each (MC load over all "
+                     f"{len(te)} target elements + np.add.at-order reduction + reference PCG on that b, "
+                     f"{statistics.mean(iters):.0f} iterations), after {args.warmup} warm-up steps; "
+                     f"setup {setup:.1f} s untimed",
+           "impl": "oracle/c/tt_oracle_c.c (C/OpenMP, -O2, no FMA) + oracle/tt_oracle.py cg_solve "
+                   "(scipy CSR); the reference itself is 2-D only"}
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_config(args, world), "cpu_baseline": cpu_line,
+            "config": workload_config(args, world), "cpu_baseline": cpu,
             "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -538,8 +606,8 @@ def run_reference(args):
 
 def run_reference_real(args, world):
     """C1 (2-D): the REFERENCE itself (oracle/_ref: tritransfer with its compiled Cython
-    backend) through its public API, all host cores: one online step =
-    assemble_load_mc(MeshBackedField) + cg_solve, as its own bench (cli.py:272-293)."""
+    backend) through its public API, all host cores, every step of --warmup + --steps
+    timed: assemble_load_mc(MeshBackedField) + cg_solve, as its own bench (cli.py:272-293)."""
     sys.path.insert(0, str(ROOT / "oracle" / "_ref"))
     import tritransfer as ref
     from tritransfer.fem import NodalField, assemble_mass_matrix, cg_solve
@@ -555,20 +623,22 @@ def run_reference_real(args, world):
     setup = time.perf_counter() - t0
     workers = os.cpu_count() or 1
     times = []
-    for _ in range(max(1, min(args.steps, 2))):
+    for i in range(args.warmup + args.steps):
         t = time.perf_counter()
         b = assemble_load_mc(tgt, box, plan, workers=workers)
         cg_solve(mass, b)
-        times.append(time.perf_counter() - t)
-    step_s = min(times)
+        if i >= args.warmup:
+            times.append(time.perf_counter() - t)
+    step_s = statistics.mean(times)
     S = tgt.n_elems * args.samples
     value = S / step_s
     cpu = {"value": value, "unit": "samples/s", "cores": workers, "kind": "reference",
-           "sample": f"full C1 step ({S} samples) through tritransfer.assemble_load_mc(workers={workers}) "
-                     f"+ cg_solve, best of {len(times)}; setup {setup:.1f} s untimed",
+           "sample": f"{args.steps} full C1 steps ({S} samples each) through "
+                     f"tritransfer.assemble_load_mc(workers={workers}) + cg_solve after {args.warmup} "
+                     f"warm-up steps; setup {setup:.1f} s untimed",
            "impl": f"reference tritransfer {ref.__version__}, backend {ref.kernel_backend}"}
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s",
-            "n_gpus": world, "steps": len(times), "warmup": 0, "ms_per_step": step_s * 1e3,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": workload_config(args, world), "cpu_baseline": cpu,
             "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}

@@ -32,6 +32,8 @@
  *   tt_reduce_nodes       <- montecarlo._reduce_to_nodes       montecarlo.py:144-147
  *   tt_mass_*             <- fem.assemble_mass_matrix          fem.py:78-110
  *   tt_pcg                <- fem.cg_solve                      fem.py:113-152
+ *   tt_dpcg_*             <- fem.cg_solve, row-partitioned over GPUs (fem.py:113-152)
+ *   tt_gather/scatter_rows <- (exchange plumbing of the partitioned load / solve)
  *   tt_integrate_p1       <- fem.integrate_field               fem.py:155-161
  */
 #ifndef TT_B200_H
@@ -285,15 +287,6 @@ int tt_reduce_nodes(int64_t n_nodes, int k, const int64_t* inc_start, const int3
                     int64_t e_lo, int64_t e_hi, const double* contrib, double* b,
                     void* stream);
 
-/* Multi-GPU node reduction over peer memory: element contributions of rank r (its
- * contiguous range [range_lo[r], range_lo[r+1])) are read through contrib_ptrs[r] (a device
- * array of device/peer pointers, e.g. symmetric-memory buffers over NVLink); every node sums
- * its incidences in the single-GPU order, so b is bitwise identical for any GPU count.
- * range_lo: device (n_ranks,) ascending element offsets. */
-int tt_reduce_nodes_peers(int64_t n_nodes, int k, const int64_t* inc_start, const int32_t* inc,
-                          int n_ranks, const int64_t* range_lo, const double* const* contrib_ptrs,
-                          double* b, void* stream);
-
 /* ---- P1 mass matrix (CSR, exactly symmetric) ---- */
 int tt_mass_pattern(const tt_mesh_t* mesh, const int64_t* inc_start, const int32_t* inc,
                     int64_t* row_ptr /* (n_nodes+1) exclusive scan of row lengths */,
@@ -332,6 +325,48 @@ int tt_pcg_ell_slab(int64_t n, int width, const int32_t* ell_cols, const double*
                     tt_pcg_result_t* result, void* stream);
 int tt_spmv(int64_t n, const int64_t* row_ptr, const int32_t* cols, const double* vals,
             const double* x, double* y, void* stream);
+
+/* ---- multi-GPU: row-partitioned PCG and exchange helpers (tt_dist.cu) ---- */
+/* One rank's part of the distributed Jacobi PCG (fem.py:113-152 in its Chronopoulos-Gear
+ * form: one all-reduce of 3 scalars per iteration).  Rows = the rank's own target nodes; the
+ * local vector u is (n_ext = own + halo) long, halo entries received from their owners each
+ * iteration.  Host loop per iteration:
+ *   tt_dpcg_update -> tt_dpcg_pack -> exchange send_buf into u[n_own:] (NCCL) ->
+ *   tt_dpcg_spmv -> all-reduce(sum) of sums[0..3) (NCCL) -> tt_dpcg_scalars
+ * after one initial tt_dpcg_start -> pack -> exchange -> spmv -> all-reduce -> scalars.  The
+ * iteration scalars stay on the device (state); every call is a no-op once it is done. */
+#define TT_DPCG_STATE_BYTES 128
+typedef struct tt_dpcg {
+    int64_t n_own;            /* owned rows */
+    int64_t n_ext;            /* local vector length: owned + halo */
+    int32_t width;            /* ELL width 8 | 16 */
+    int32_t reserved;
+    const int32_t* ell_cols;  /* (n_own, width) local column ids into u (padding: own row, 0.0) */
+    const double*  ell_vals;  /* (n_own, width) */
+    const double*  diag;      /* (n_own,) */
+    const double*  b;         /* (n_own,) */
+    double* x; double* best_x; double* r; double* w; double* p; double* s; double* dinv; /* (n_own,) */
+    double* u;                /* (n_ext,) */
+    const int64_t* send_idx;  /* (n_send,) own rows whose u the peers need, grouped by peer */
+    int64_t n_send;
+    double* send_buf;         /* (n_send,) */
+    double* part;             /* tt_dpcg_part_doubles() scratch */
+    double* sums;             /* (3,) local sums (r.u, w.u, r.r): all-reduce them in place */
+    double* state;            /* TT_DPCG_STATE_BYTES of device scalar state */
+    double  tol;
+    int64_t maxiter;
+} tt_dpcg_t;
+int64_t tt_dpcg_part_doubles(void);
+int tt_dpcg_start(const tt_dpcg_t* a, void* stream);
+int tt_dpcg_update(const tt_dpcg_t* a, void* stream);
+int tt_dpcg_pack(const tt_dpcg_t* a, void* stream);
+int tt_dpcg_spmv(const tt_dpcg_t* a, void* stream);
+int tt_dpcg_scalars(const tt_dpcg_t* a, void* stream);
+/* settles best_x / zeroes x for b = 0 and writes the result record (device) */
+int tt_dpcg_finish(const tt_dpcg_t* a, tt_pcg_result_t* result, void* stream);
+/* dst[t, :] = src[idx[t], :] and dst[idx[t], :] = src[t, :] for rows of k doubles */
+int tt_gather_rows(int64_t n, int k, const int64_t* idx, const double* src, double* dst, void* stream);
+int tt_scatter_rows(int64_t n, int k, const int64_t* idx, const double* src, double* dst, void* stream);
 
 /* ---- reporting ---- */
 int tt_integrate_p1(const tt_mesh_t* mesh, const double* coeffs, double* out /* device scalar */,

@@ -82,6 +82,16 @@ class tt_pcg_result_t(C.Structure):
                 ("zero_rhs", C.c_int32)]
 
 
+class tt_dpcg_t(C.Structure):
+    _fields_ = [("n_own", C.c_int64), ("n_ext", C.c_int64), ("width", C.c_int32), ("reserved", C.c_int32),
+                ("ell_cols", C.c_void_p), ("ell_vals", C.c_void_p), ("diag", C.c_void_p), ("b", C.c_void_p),
+                ("x", C.c_void_p), ("best_x", C.c_void_p), ("r", C.c_void_p), ("w", C.c_void_p),
+                ("p", C.c_void_p), ("s", C.c_void_p), ("dinv", C.c_void_p), ("u", C.c_void_p),
+                ("send_idx", C.c_void_p), ("n_send", C.c_int64), ("send_buf", C.c_void_p),
+                ("part", C.c_void_p), ("sums", C.c_void_p), ("state", C.c_void_p),
+                ("tol", C.c_double), ("maxiter", C.c_int64)]
+
+
 _P = C.c_void_p
 _I64 = C.c_int64
 _I = C.c_int
@@ -121,7 +131,6 @@ _SIGNATURES = {
     "tt_incidence_count": ([C.POINTER(tt_mesh_t), _P, _P], _I),
     "tt_incidence_fill": ([C.POINTER(tt_mesh_t), _P, _P, _P, _P], _I),
     "tt_reduce_nodes": ([_I64, _I, _P, _P, _I64, _I64, _P, _P, _P], _I),
-    "tt_reduce_nodes_peers": ([_I64, _I, _P, _P, _I, _P, _P, _P, _P], _I),
     "tt_mass_pattern": ([C.POINTER(tt_mesh_t), _P, _P, _P, _P, _P], _I),
     "tt_mass_fill": ([C.POINTER(tt_mesh_t), _P, _P, C.POINTER(_D), _P, _P, _P, _P], _I),
     "tt_pcg_workspace_doubles": ([_I64], _I64),
@@ -131,6 +140,15 @@ _SIGNATURES = {
     "tt_pcg_ell_slab": ([_I64, _I, _P, _P, _P, _P, _D, _I64, _P, _P, _P, _P, _P], _I),
     "tt_spmv": ([_I64, _P, _P, _P, _P, _P, _P], _I),
     "tt_integrate_p1": ([C.POINTER(tt_mesh_t), _P, _P, _P], _I),
+    "tt_dpcg_part_doubles": ([], _I64),
+    "tt_dpcg_start": ([_P, _P], _I),
+    "tt_dpcg_update": ([_P, _P], _I),
+    "tt_dpcg_pack": ([_P, _P], _I),
+    "tt_dpcg_spmv": ([_P, _P], _I),
+    "tt_dpcg_scalars": ([_P, _P], _I),
+    "tt_dpcg_finish": ([_P, _P, _P], _I),
+    "tt_gather_rows": ([_I64, _I, _P, _P, _P, _P], _I),
+    "tt_scatter_rows": ([_I64, _I, _P, _P, _P, _P], _I),
     "tt_fp64_peak_probe": ([_I64, _P, C.POINTER(_I), C.POINTER(_I), _P], _I),
 }
 

@@ -711,31 +711,6 @@ __global__ void reduce_nodes_kernel(int64_t n_nodes, int k, const int64_t* __res
     b[n] = s;
 }
 
-// Multi-GPU node reduction over peer memory: contributions of element e live on the rank
-// whose contiguous range contains e (contrib_ptrs[r] may be a peer/NVLink pointer).  Each
-// node sums its incidences in ascending (e, a) order from 0.0 -- the single-GPU order, so b
-// is bitwise identical for any number of GPUs (the reference's worker invariance,
-// montecarlo.py:191).
-__global__ void reduce_nodes_peers_kernel(int64_t n_nodes, int k, const int64_t* __restrict__ inc_start,
-                                          const int32_t* __restrict__ inc, int n_ranks,
-                                          const int64_t* __restrict__ range_lo,
-                                          const double* const* __restrict__ contrib_ptrs,
-                                          double* __restrict__ b) {
-    int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (n >= n_nodes) return;
-    double s = 0.0;
-    int r = 0;
-    for (int64_t q = inc_start[n]; q < inc_start[n + 1]; ++q) {
-        const int64_t ea = inc[q];
-        const int64_t e = ea / k;
-        // incidences ascend in e: advance the owning rank monotonically
-        while (r + 1 < n_ranks && e >= range_lo[r + 1]) ++r;
-        while (r > 0 && e < range_lo[r]) --r;
-        s = add(s, contrib_ptrs[r][(e - range_lo[r]) * k + (ea - e * k)]);
-    }
-    b[n] = s;
-}
-
 __global__ void incidence_count_kernel(int64_t nent, const int32_t* __restrict__ elems,
                                        unsigned long long* __restrict__ counts) {
     int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -1096,19 +1071,6 @@ extern "C" int tt_pack_grad(const tt_mesh_t* m, const double* coeffs, double* ou
     else
         pack_grad_kernel<3><<<grid_for(m->n_elems, 256), 256, 0, as_stream(stream)>>>(m->n_elems, m->elems, m->nodes, coeffs, out);
     return launch_check("pack_grad_kernel");
-}
-
-extern "C" int tt_reduce_nodes_peers(int64_t n_nodes, int k, const int64_t* inc_start, const int32_t* inc,
-                                     int n_ranks, const int64_t* range_lo, const double* const* contrib_ptrs,
-                                     double* b, void* stream) {
-    if (n_ranks < 1 || k < 3 || k > 4) {
-        set_error("tt_reduce_nodes_peers: bad arguments");
-        return TT_ERR_INVALID_PARAMETER;
-    }
-    if (n_nodes == 0) return TT_OK;
-    reduce_nodes_peers_kernel<<<grid_for(n_nodes, 256), 256, 0, as_stream(stream)>>>(
-        n_nodes, k, inc_start, inc, n_ranks, range_lo, contrib_ptrs, b);
-    return launch_check("reduce_nodes_peers_kernel");
 }
 
 #ifdef TT_MC_STATS

@@ -31,6 +31,8 @@ class DeviceMesh:
         dev = _lib.device()
         self.nodes = torch.tensor(mesh.nodes, dtype=torch.float64, device=dev)
         self.elems = torch.tensor(mesh.elements, dtype=torch.int32, device=dev)
+        # partition meshes: global element ids (Philox stream counters)
+        self.gid = None if mesh.gid is None else torch.as_tensor(mesh.gid, dtype=torch.int32, device=dev)
         self.signed_measure = torch.empty(self.n_elems, dtype=torch.float64, device=dev)
         self.rec = torch.empty((self.n_elems, _lib.rec_stride(self.dim)), dtype=torch.float64,
                                device=dev)
@@ -42,7 +44,7 @@ class DeviceMesh:
 
     def desc(self, with_measure: bool = True) -> _lib.tt_mesh_t:
         return _lib.mesh_desc(self.dim, self.n_nodes, self.n_elems, self.nodes, self.elems,
-                              self.measure if with_measure else None)
+                              self.measure if with_measure else None, self.gid)
 
     @cached_property
     def incidence(self):

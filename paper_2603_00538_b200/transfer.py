@@ -50,7 +50,6 @@ class MCTransferOperator:
         self.source_mesh = source_mesh
         self.plan = plan
         self.cg_tol = cg_tol
-        self.mass = target.device.mass
         self.locator = source_locator or UniformGridLocator.build(source_mesh)
         self.src_elem_dev = sample_source_elements(target, self.locator, plan)
         if fold is None:
@@ -72,6 +71,10 @@ class MCTransferOperator:
         va = torch.empty(max(nnz.value, 1), dtype=torch.float64, device=dev)
         _lib.call("tt_mc_fold_finish", handle, _lib.ptr(rp), _lib.ptr(ci), _lib.ptr(va), s)
         return rp, ci[:nnz.value], va[:nnz.value]
+
+    @property
+    def mass(self):
+        return self.target.device.mass
 
     @property
     def load_matrix(self):

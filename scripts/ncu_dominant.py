@@ -1,5 +1,5 @@
 """Roofline evidence of the dominant kernel from one `ncu --set full` capture -> the JSON
-bench.py reads (profiles/r01/ncu_dominant_kernel.json): DRAM bytes per launch and
+bench.py reads (profiles/rNN/ncu_dominant_kernel.json): DRAM bytes per launch and
 SASS-counted flops per sample (DFMA = 2).
 
 python scripts/ncu_dominant.py report.ncu-rep SAMPLES_PER_LAUNCH KERNEL_LABEL > out.json
@@ -32,6 +32,8 @@ out = {
     "fp64_flops_per_sample": (2 * ops["dfma"] + ops["dmul"] + ops["dadd"]) / samples,
     "fp32_flops_per_sample": (2 * ops["ffma"] + ops["fmul"] + ops["fadd"]) / samples,
     "l1_data_pipe_pct": get("l1tex__data_pipe_lsu_wavefronts.sum.pct_of_peak_sustained_elapsed"),
+    "l1_wavefronts_per_sample": (get("l1tex__data_pipe_lsu_wavefronts.sum") / samples
+                                 if "l1tex__data_pipe_lsu_wavefronts.sum" in names else None),
     "fp64_pipe_active_pct": get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
     "ipc": get("sm__inst_executed.avg.per_cycle_active"),
 }

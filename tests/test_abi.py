@@ -49,7 +49,7 @@ def test_struct_layouts_match_c():
     import ctypes as C
     structs = {"tt_mesh_t": _lib.tt_mesh_t, "tt_grid_t": _lib.tt_grid_t, "tt_plan_t": _lib.tt_plan_t,
                "tt_expr_t": _lib.tt_expr_t, "tt_source_t": _lib.tt_source_t,
-               "tt_pcg_result_t": _lib.tt_pcg_result_t}
+               "tt_pcg_result_t": _lib.tt_pcg_result_t, "tt_dpcg_t": _lib.tt_dpcg_t}
     lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{HEADER}"', "int main(void){"]
     for name, cls in structs.items():
         lines.append(f'printf("{name} %zu\\n", sizeof({name}));')

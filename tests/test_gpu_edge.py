@@ -105,28 +105,6 @@ def test_deterministic_reduction_matches_add_at_order(tt):
     assert np.array_equal(b, ref)
 
 
-@pytest.mark.parametrize("world", [1, 2, 3, 8])
-def test_peer_reduction_is_gpu_count_invariant(tt, world):
-    """tt_reduce_nodes_peers with W emulated ranks (W contribution buffers on this GPU,
-    addressed through a pointer table exactly as peer buffers are) reproduces the
-    single-GPU deterministic load vector bitwise."""
-    import torch
-    from paper_2603_00538_b200.dist import partition_elements, reduce_nodes_peers
-    from paper_2603_00538_b200.montecarlo import element_contributions, load_vector
-    tgt = tt.generate_cube_mesh(7, 0.2, seed=20)
-    src = tt.generate_cube_mesh(8, 0.2, seed=10, split="kuhn_mirror")
-    fs = tt.NodalField.from_function(src, tt.get_field("smooth", dim=3).fn)
-    box = tt.MeshBackedField(fs)
-    plan = tt.SamplePlan.build(24, "sobol", 0, dim=3)
-    full = load_vector(tgt, box, plan)
-    spans = [partition_elements(tgt.n_elems, world, r) for r in range(world)]
-    bufs = [element_contributions(tgt, box, plan, lo, hi) for lo, hi in spans]
-    ptrs = torch.tensor([t.data_ptr() for t in bufs], dtype=torch.int64, device="cuda")
-    lo = torch.tensor([a for a, _ in spans], dtype=torch.int64, device="cuda")
-    b = reduce_nodes_peers(tgt, ptrs, lo)
-    assert torch.equal(b, full)
-
-
 @pytest.mark.parametrize("n", [1, 2, 5, 33, 600])
 def test_pcg_small_systems_all_paths(tt, n):
     """Tiny SPD systems through the slab, L2-ELL and CSR PCGs (block ranges with no rows,

@@ -60,7 +60,7 @@ def test_full_size_ids_and_load_vs_oracle(name):
     contrib, n_out = OC.mc_load_mesh(g, coeffs, tgt.nodes, tgt.elements, measure, lam, ids=ids_ref)
     b_ref = np.bincount(tgt.elements.ravel(), weights=contrib.ravel(), minlength=tgt.n_nodes)
     if name == "c3":
-        assert n_out > 10000                     # the snap path runs (non-matching boundaries)
+        assert n_out > 1000                      # the snap path runs (non-matching boundaries)
     else:
         assert n_out == 0
 

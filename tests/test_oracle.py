@@ -217,3 +217,18 @@ def test_c_grid_and_ids_match_numpy_oracle(golden):
             eo[i] = gn.nearest_element(pts[i])
         assert n_out == len(out)
         assert np.array_equal(ids.ravel(), eo)
+
+
+def test_oracle_mesh_generators_equal_the_product_inputs():
+    """The reference arm builds its 3-D inputs with oracle/meshgen.py (no product import):
+    the same meshes the GPU arm generates, bit for bit."""
+    import meshgen
+    from paper_2603_00538_b200 import mesh as M
+    for args in ((5, 0.2, 20, "kuhn"), (4, 0.2, 10, "kuhn_mirror")):
+        n, p, seed, split = args
+        nodes, elems = meshgen.cube(n, p, seed, split)
+        m = M.generate_cube_mesh(n, p, seed=seed, split=split)
+        assert np.array_equal(nodes, m.nodes) and np.array_equal(elems, m.elements)
+    nodes, elems = meshgen.torus(3, 12, 17, 0.2, 10, "kuhn_mirror")
+    m = M.generate_torus_mesh(3, 12, 17, perturbation=0.2, seed=10, split="kuhn_mirror")
+    assert np.array_equal(nodes, m.nodes) and np.array_equal(elems, m.elements)
