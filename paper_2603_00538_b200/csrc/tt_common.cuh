@@ -154,36 +154,46 @@ TT_D void load_tail(const double* __restrict__ rec, int64_t e, RecTail<D>& t) {
     if constexpr (D == 3) t.nbr[3] = __ldg(reinterpret_cast<const int*>(q + 1));
 }
 
-// Compact walk record: origin (double), binv (float), tau_f (float), nbr (int32).
+// 256-bit non-coherent global load (sm_100: one LDG.E.ENL2.256 per lane); p 32-byte aligned.
+TT_D void ldg256(const void* p, uint64_t (&v)[4]) {
+    asm("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];"
+        : "=l"(v[0]), "=l"(v[1]), "=l"(v[2]), "=l"(v[3]) : "l"(p));
+}
+
+TT_D float lo_f(uint64_t w) { return __int_as_float((int)(uint32_t)w); }
+TT_D float hi_f(uint64_t w) { return __int_as_float((int)(uint32_t)(w >> 32)); }
+
+// Compact walk record, 64 B (one half line, two 256-bit loads), stride TT_WREC_STRIDE:
+//   3-D: origin o (3 doubles), binv as float (9), float tau_f; neighbours in grid.wnbr
+//   2-D: origin o (2 doubles), binv as float (4) | tau_f, int32 nbr[3], pad
 template <int D>
 struct WRec {
     double o[D];
     float b[D][D];
     float tau;
-    int nbr[D + 1];
 };
 
 template <int D>
-TT_D void load_wrec(const double* __restrict__ wrec, int64_t e, WRec<D>& w) {
+TT_D void load_wrec(const double* __restrict__ wrec, int64_t e, WRec<D>& w, int* nbr2 = nullptr) {
+    uint64_t a[4], c[4];
+    ldg256(wrec + e * 8, a);
+    ldg256(wrec + e * 8 + 4, c);
     if constexpr (D == 2) {
-        const int4* q = reinterpret_cast<const int4*>(wrec + e * 6);
-        const int4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
-        w.o[0] = __hiloint2double(a.y, a.x); w.o[1] = __hiloint2double(a.w, a.z);
-        w.b[0][0] = __int_as_float(b.x); w.b[0][1] = __int_as_float(b.y);
-        w.b[1][0] = __int_as_float(b.z); w.b[1][1] = __int_as_float(b.w);
-        w.tau = __int_as_float(c.x);
-        w.nbr[0] = c.y; w.nbr[1] = c.z; w.nbr[2] = c.w;
+        w.o[0] = __longlong_as_double((long long)a[0]); w.o[1] = __longlong_as_double((long long)a[1]);
+        w.b[0][0] = lo_f(a[2]); w.b[0][1] = hi_f(a[2]);
+        w.b[1][0] = lo_f(a[3]); w.b[1][1] = hi_f(a[3]);
+        w.tau = lo_f(c[0]);
+        if (nbr2) {
+            nbr2[0] = (int)(c[0] >> 32); nbr2[1] = (int)(uint32_t)c[1]; nbr2[2] = (int)(c[1] >> 32);
+        }
     } else {
-        const int4* q = reinterpret_cast<const int4*>(wrec + e * 10);
-        const int4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2), d = __ldg(q + 3), f = __ldg(q + 4);
-        w.o[0] = __hiloint2double(a.y, a.x); w.o[1] = __hiloint2double(a.w, a.z);
-        w.o[2] = __hiloint2double(b.y, b.x);
-        w.b[0][0] = __int_as_float(b.z); w.b[0][1] = __int_as_float(b.w);
-        w.b[0][2] = __int_as_float(c.x); w.b[1][0] = __int_as_float(c.y);
-        w.b[1][1] = __int_as_float(c.z); w.b[1][2] = __int_as_float(c.w);
-        w.b[2][0] = __int_as_float(d.x); w.b[2][1] = __int_as_float(d.y);
-        w.b[2][2] = __int_as_float(d.z); w.tau = __int_as_float(d.w);
-        w.nbr[0] = f.x; w.nbr[1] = f.y; w.nbr[2] = f.z; w.nbr[3] = f.w;
+        w.o[0] = __longlong_as_double((long long)a[0]); w.o[1] = __longlong_as_double((long long)a[1]);
+        w.o[2] = __longlong_as_double((long long)a[2]);
+        w.b[0][0] = lo_f(a[3]); w.b[0][1] = hi_f(a[3]);
+        w.b[0][2] = lo_f(c[0]); w.b[1][0] = hi_f(c[0]);
+        w.b[1][1] = lo_f(c[1]); w.b[1][2] = hi_f(c[1]);
+        w.b[2][0] = lo_f(c[2]); w.b[2][1] = hi_f(c[2]);
+        w.b[2][2] = lo_f(c[3]); w.tau = hi_f(c[3]);
     }
 }
 
@@ -197,6 +207,7 @@ struct GridDev {
     const double* __restrict__ rec;
     const double* __restrict__ centroids;
     const double* __restrict__ wrec;
+    const int32_t* __restrict__ wnbr;  // 3-D facet neighbours of the walk (E, 4)
 };
 
 inline GridDev to_dev(const tt_grid_t& g) {
@@ -207,6 +218,7 @@ inline GridDev to_dev(const tt_grid_t& g) {
     d.cell_start = g.cell_start; d.cell_elems = g.cell_elems;
     d.rec = g.rec; d.centroids = g.centroids;
     d.wrec = g.wrec;
+    d.wnbr = g.wnbr;
     return d;
 }
 

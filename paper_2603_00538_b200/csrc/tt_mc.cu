@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(kMcBlock, kMcMinBlocks) mc_mesh_kernel(TargetD
     const int64_t n_el = e_hi - e_lo;
     const int64_t N = plan.n;
     const GridDev& g = src.grid;
-    const bool walk = g.walk && src.seeds && g.wrec;
+    const bool walk = g.walk && src.seeds && g.wrec && (D == 2 || g.wnbr);
     int flags = 0;
     constexpr bool USE_SLOT = SLOT && PLAN == TT_PLAN_SHARED;
     extern __shared__ int8_t s_slot[];  // N bytes (launch: dynamic shared memory)
@@ -427,13 +427,10 @@ __global__ void __launch_bounds__(kMcBlock, kMcMinBlocks) mc_mesh_kernel(TargetD
                 // evaluation error (tt_grid.cu walk_prep_kernel); f from the element's
                 // gradient record: f = c_last + g . (x - o), accurate to a few ulps
                 WRec<D> w;
-                load_wrec<D>(g.wrec, cur, w);
-                double2 pc0 = make_double2(0.0, 0.0), pc1 = make_double2(0.0, 0.0);
-                if (src.egrad) {  // speculative: the gradient record of the element tested
-                    const double2* q = reinterpret_cast<const double2*>(src.egrad + (int64_t)cur * 4);
-                    pc0 = __ldg(q);
-                    pc1 = __ldg(q + 1);
-                }
+                int nb2[3];
+                load_wrec<D>(g.wrec, cur, w, D == 2 ? nb2 : nullptr);
+                uint64_t gq[4] = {0, 0, 0, 0};
+                if (src.egrad) ldg256(src.egrad + (int64_t)cur * 4, gq);  // speculative: gradient record
                 double r[D];
                 float rf[D];
 #pragma unroll
@@ -458,7 +455,9 @@ __global__ void __launch_bounds__(kMcBlock, kMcMinBlocks) mc_mesh_kernel(TargetD
                     hit = cur;
                     done = true;
                     fw_hit = true;
-                    const double gv[4] = {pc0.x, pc0.y, pc1.x, pc1.y};
+                    double gv[4];
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) gv[c] = __longlong_as_double((long long)gq[c]);
                     double f = gv[D];
 #pragma unroll
                     for (int c = 0; c < D; ++c) f = fma(gv[c], r[c], f);
@@ -467,10 +466,17 @@ __global__ void __launch_bounds__(kMcBlock, kMcMinBlocks) mc_mesh_kernel(TargetD
                     fb = cur;  // within the uncertainty band of a facet: exact double walk
                     cur = -1;
                 } else {
-                    int nb = w.nbr[0];
+                    int nbr[K];
+                    if constexpr (D == 2) {
+                        nbr[0] = nb2[0]; nbr[1] = nb2[1]; nbr[2] = nb2[2];
+                    } else {
+                        const int4 q = __ldg(reinterpret_cast<const int4*>(g.wnbr) + cur);
+                        nbr[0] = q.x; nbr[1] = q.y; nbr[2] = q.z; nbr[3] = q.w;
+                    }
+                    int nb = nbr[0];
 #pragma unroll
                     for (int i = 1; i <= D; ++i)
-                        if (imin == i) nb = w.nbr[i];
+                        if (imin == i) nb = nbr[i];
                     cur = nb;
                     ++steps;
                     TT_STAT(3, 1);

@@ -128,6 +128,7 @@ class UniformGridLocator:
         g.centroids = _lib.ptr(dm.centroids).value
         if self.walk and getattr(dm, "wrec", None) is not None:
             g.wrec = _lib.ptr(dm.wrec).value
+            g.wnbr = _lib.ptr(dm.wnbr).value
         return g
 
     def seeds_for(self, target) -> torch.Tensor:
@@ -143,16 +144,20 @@ class UniformGridLocator:
         st = _lib.status_word()
         _lib.call("tt_seed_elements", C.byref(g), C.byref(t), 0, target.n_elems, _lib.ptr(seeds),
                   _lib.ptr(st), _lib.stream_handle())
-        # one-time read (setup): an anchor outside the source mesh means outside samples
-        # occur -> the kernel variant with warp-cooperative snaps.  Decided here, before any
-        # load, so every load of this (target, locator) pair runs the same kernel and is
-        # bitwise reproducible
-        self._seeds[target] = (seeds, bool(int(st.item()) & _lib.TT_FLAG_SNAPPED))
+        # one-time setup probe: an anchor or a target vertex outside the source mesh (the
+        # reference scan) means outside samples occur -> the kernel variant with
+        # warp-cooperative snaps.  Decided here, before any load, as a function of the mesh
+        # pair only, so every load of this (target, locator) pair runs the same kernel and
+        # is bitwise reproducible
+        elem, _ = self.locate_many(target.device.nodes)
+        outside = bool(int(st.item()) & _lib.TT_FLAG_SNAPPED) or bool((elem < 0).any().item())
+        self._seeds[target] = (seeds, outside)
         return seeds
 
     def snap_prone(self, target) -> bool:
         """Whether loads of ``target`` run the deferred (warp-cooperative) snap variant:
-        ``defer_snaps`` when set, else whether a walk-seed anchor lay outside."""
+        ``defer_snaps`` when set, else whether a walk-seed anchor or a target vertex lies
+        outside the source mesh."""
         if self.defer_snaps is not None:
             return bool(self.defer_snaps)
         self.seeds_for(target)
@@ -238,10 +243,14 @@ def _walk_prep(mesh):
     inc_start, inc = dm.incidence
     status = _lib.status_word()
     desc = dm.desc()
+    # 64 B records read with 256-bit loads (torch allocations are 512-byte aligned)
     dm.wrec = torch.empty((mesh.n_elems, _lib.wrec_stride(mesh.DIM)), dtype=torch.float64,
                           device=dm.nodes.device)
+    dm.wnbr = (torch.empty((mesh.n_elems, 4), dtype=torch.int32, device=dm.nodes.device)
+               if mesh.DIM == 3 else None)
     _lib.call("tt_grid_walk_prep", C.byref(desc), _lib.ptr(inc_start), _lib.ptr(inc), EPS_LOC,
-              _lib.ptr(dm.rec), _lib.ptr(dm.wrec), _lib.ptr(status), _lib.stream_handle())
+              _lib.ptr(dm.rec), _lib.ptr(dm.wrec), _lib.ptr(dm.wnbr), _lib.ptr(status),
+              _lib.stream_handle())
     if int(status.item()) & _lib.TT_FLAG_NONMANIFOLD:
         raise NonManifold("a facet is shared by more than two elements")
     dm.walk_ready = True
