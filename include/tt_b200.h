@@ -35,6 +35,8 @@
  *   tt_dpcg_*             <- fem.cg_solve, row-partitioned over GPUs (fem.py:113-152)
  *   tt_gather/scatter_rows <- (exchange plumbing of the partitioned load / solve)
  *   tt_integrate_p1       <- fem.integrate_field               fem.py:155-161
+ *   tt_supermesh_integrals <- metrics.supermesh_l2/mass_error  metrics.py:35-74 (2-D, with
+ *                            the intersect.py clip done on the device)
  */
 #ifndef TT_B200_H
 #define TT_B200_H
@@ -373,6 +375,15 @@ int tt_scatter_rows(int64_t n, int k, const int64_t* idx, const double* src, dou
 /* ---- reporting ---- */
 int tt_integrate_p1(const tt_mesh_t* mesh, const double* coeffs, double* out /* device scalar */,
                     void* stream);
+
+/* Supermesh integrals of two P1 fields on triangle meshes (metrics.py:35-74 over the
+ * intersection polygons of intersect.py:60-80, clipped on the device): per target element
+ * (E_t, 6) = [int (fs-ft)^2, int fs^2, int fs, int ft, covered area, covered / |t|] and the
+ * totals (6,) = column sums (fixed order), last = min covered fraction.  Polygons of area
+ * <= sliver_rel |t| are dropped (intersect.py:21). */
+int tt_supermesh_integrals(const tt_mesh_t* target, const double* t_coeffs, const tt_mesh_t* source,
+                           const double* s_coeffs, const tt_grid_t* src_grid, double sliver_rel,
+                           double* per_elem, double* totals, void* stream);
 
 /* ---- measurement helpers ---- */
 int tt_fp64_peak_probe(int64_t iters, double* sink /* (blocks*threads) */, int* blocks_out,

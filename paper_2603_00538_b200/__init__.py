@@ -7,7 +7,7 @@ every numeric step running in hand-written sm_100a CUDA (libtt_b200.so) and no C
 fallback.  Extends the reference (2-D triangles) to 3-D tetrahedra.
 """
 
-from .errors import (DegenerateElement, DeviceUnavailable, DimensionMismatch, EmptyMesh,
+from .errors import (CoverageGap, DegenerateElement, DeviceUnavailable, DimensionMismatch, EmptyMesh,
                      InvalidDensity, InvalidParameter, MeshMismatch, NoConvergence,
                      NonManifold, ParseError, SourceEvalFailed, TransferError,
                      ZeroDenominator)
@@ -20,7 +20,8 @@ from .montecarlo import (AnalyticField, MeshBackedField, SamplePlan, assemble_lo
                          assemble_load_mc_weighted, bary_map, importance_weights)
 from .fields import NAMED_FIELDS, get_field, parse_field
 from .transfer import MCTransferOperator, transfer_mc
-from .metrics import ErrorReport, dof_l2_error, mass_error, mesh_mass_error
+from .metrics import (ErrorReport, IntersectionSet, dof_l2_error, find_intersections, mass_error,
+                      mesh_mass_error, supermesh_l2_error, supermesh_mass_error)
 
 kernel_backend = "cuda-sm_100a"
 
@@ -33,7 +34,8 @@ __all__ = [
     "assemble_load_mc_weighted", "importance_weights", "bary_map",
     "NAMED_FIELDS", "get_field", "parse_field",
     "MCTransferOperator", "transfer_mc",
-    "ErrorReport", "dof_l2_error", "mesh_mass_error", "mass_error",
+    "ErrorReport", "dof_l2_error", "mesh_mass_error", "mass_error", "IntersectionSet",
+    "find_intersections", "supermesh_l2_error", "supermesh_mass_error", "CoverageGap",
     "kernel_backend",
 ]
 

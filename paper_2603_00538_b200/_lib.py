@@ -140,6 +140,8 @@ _SIGNATURES = {
     "tt_pcg_ell_slab": ([_I64, _I, _P, _P, _P, _P, _D, _I64, _P, _P, _P, _P, _P], _I),
     "tt_spmv": ([_I64, _P, _P, _P, _P, _P, _P], _I),
     "tt_integrate_p1": ([C.POINTER(tt_mesh_t), _P, _P, _P], _I),
+    "tt_supermesh_integrals": ([C.POINTER(tt_mesh_t), _P, C.POINTER(tt_mesh_t), _P, C.POINTER(tt_grid_t),
+                                _D, _P, _P, _P], _I),
     "tt_dpcg_part_doubles": ([], _I64),
     "tt_dpcg_start": ([_P, _P], _I),
     "tt_dpcg_update": ([_P, _P], _I),

@@ -163,7 +163,7 @@ TT_D void ldg256(const void* p, uint64_t (&v)[4]) {
 TT_D float lo_f(uint64_t w) { return __int_as_float((int)(uint32_t)w); }
 TT_D float hi_f(uint64_t w) { return __int_as_float((int)(uint32_t)(w >> 32)); }
 
-// Compact walk record, 64 B (one half line, two 256-bit loads), stride TT_WREC_STRIDE:
+// Compact walk record, 64 B (one aligned half line), stride TT_WREC_STRIDE:
 //   3-D: origin o (3 doubles), binv as float (9), float tau_f; neighbours in grid.wnbr
 //   2-D: origin o (2 doubles), binv as float (4) | tau_f, int32 nbr[3], pad
 template <int D>
@@ -175,25 +175,26 @@ struct WRec {
 
 template <int D>
 TT_D void load_wrec(const double* __restrict__ wrec, int64_t e, WRec<D>& w, int* nbr2 = nullptr) {
-    uint64_t a[4], c[4];
-    ldg256(wrec + e * 8, a);
-    ldg256(wrec + e * 8 + 4, c);
+    // four LDG.128 of one 64-byte-aligned half line (no record straddles a line).  Measured:
+    // two 256-bit loads per test issue fewer instructions but cost MORE L1 wavefronts (1.22
+    // vs 1.12 ms at C2): a 32 B lane access takes two wavefronts of the LSU data path.
+    const int4* q = reinterpret_cast<const int4*>(wrec + e * 8);
+    const int4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
     if constexpr (D == 2) {
-        w.o[0] = __longlong_as_double((long long)a[0]); w.o[1] = __longlong_as_double((long long)a[1]);
-        w.b[0][0] = lo_f(a[2]); w.b[0][1] = hi_f(a[2]);
-        w.b[1][0] = lo_f(a[3]); w.b[1][1] = hi_f(a[3]);
-        w.tau = lo_f(c[0]);
-        if (nbr2) {
-            nbr2[0] = (int)(c[0] >> 32); nbr2[1] = (int)(uint32_t)c[1]; nbr2[2] = (int)(c[1] >> 32);
-        }
+        w.o[0] = __hiloint2double(a.y, a.x); w.o[1] = __hiloint2double(a.w, a.z);
+        w.b[0][0] = __int_as_float(b.x); w.b[0][1] = __int_as_float(b.y);
+        w.b[1][0] = __int_as_float(b.z); w.b[1][1] = __int_as_float(b.w);
+        w.tau = __int_as_float(c.x);
+        if (nbr2) { nbr2[0] = c.y; nbr2[1] = c.z; nbr2[2] = c.w; }
     } else {
-        w.o[0] = __longlong_as_double((long long)a[0]); w.o[1] = __longlong_as_double((long long)a[1]);
-        w.o[2] = __longlong_as_double((long long)a[2]);
-        w.b[0][0] = lo_f(a[3]); w.b[0][1] = hi_f(a[3]);
-        w.b[0][2] = lo_f(c[0]); w.b[1][0] = hi_f(c[0]);
-        w.b[1][1] = lo_f(c[1]); w.b[1][2] = hi_f(c[1]);
-        w.b[2][0] = lo_f(c[2]); w.b[2][1] = hi_f(c[2]);
-        w.b[2][2] = lo_f(c[3]); w.tau = hi_f(c[3]);
+        const int4 d = __ldg(q + 3);
+        w.o[0] = __hiloint2double(a.y, a.x); w.o[1] = __hiloint2double(a.w, a.z);
+        w.o[2] = __hiloint2double(b.y, b.x);
+        w.b[0][0] = __int_as_float(b.z); w.b[0][1] = __int_as_float(b.w);
+        w.b[0][2] = __int_as_float(c.x); w.b[1][0] = __int_as_float(c.y);
+        w.b[1][1] = __int_as_float(c.z); w.b[1][2] = __int_as_float(c.w);
+        w.b[2][0] = __int_as_float(d.x); w.b[2][1] = __int_as_float(d.y);
+        w.b[2][2] = __int_as_float(d.z); w.tau = __int_as_float(d.w);
     }
 }
 

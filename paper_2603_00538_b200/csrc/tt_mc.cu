@@ -355,7 +355,10 @@ __global__ void __launch_bounds__(kMcBlock, kMcMinBlocks) mc_mesh_kernel(TargetD
         }
         __syncthreads();
     }
-    __shared__ double s_v[NW][EPW][K * D];
+    // vertex rows padded to an odd number of doubles: the 8-byte reads of the warp's groups
+    // land in distinct bank pairs (12-double rows put groups 0 and 4 on the same banks)
+    constexpr int VS = (K * D) | 1;
+    __shared__ double s_v[NW][EPW][VS];
     __shared__ int s_seed[NW][EPW][kSeeds];
     const int wib = threadIdx.x >> 5, gib = lane / G;
 
@@ -429,8 +432,12 @@ __global__ void __launch_bounds__(kMcBlock, kMcMinBlocks) mc_mesh_kernel(TargetD
                 WRec<D> w;
                 int nb2[3];
                 load_wrec<D>(g.wrec, cur, w, D == 2 ? nb2 : nullptr);
-                uint64_t gq[4] = {0, 0, 0, 0};
-                if (src.egrad) ldg256(src.egrad + (int64_t)cur * 4, gq);  // speculative: gradient record
+                double2 pc0 = make_double2(0.0, 0.0), pc1 = make_double2(0.0, 0.0);
+                if (src.egrad) {  // speculative: the gradient record of the element tested
+                    const double2* q = reinterpret_cast<const double2*>(src.egrad + (int64_t)cur * 4);
+                    pc0 = __ldg(q);
+                    pc1 = __ldg(q + 1);
+                }
                 double r[D];
                 float rf[D];
 #pragma unroll
@@ -455,9 +462,7 @@ __global__ void __launch_bounds__(kMcBlock, kMcMinBlocks) mc_mesh_kernel(TargetD
                     hit = cur;
                     done = true;
                     fw_hit = true;
-                    double gv[4];
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) gv[c] = __longlong_as_double((long long)gq[c]);
+                    const double gv[4] = {pc0.x, pc0.y, pc1.x, pc1.y};
                     double f = gv[D];
 #pragma unroll
                     for (int c = 0; c < D; ++c) f = fma(gv[c], r[c], f);

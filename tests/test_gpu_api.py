@@ -211,9 +211,11 @@ def test_cli_study_commands_run(tt, tmp_path):
     assert lines[0] == "# schema: tritransfer/convergence v1"
     assert lines[1] == "h,method,n_samples,e_l2_supermesh,e_mass_supermesh"
     rows = {int(r.split(",")[2]): float(r.split(",")[4]) for r in lines[2:]}
+    l2 = {int(r.split(",")[2]): float(r.split(",")[3]) for r in lines[2:]}
     with np.load(Path(__file__).resolve().parent / "golden" / "ref_stats.npz") as z:
         for N in (400, 1600):
             assert abs(rows[N] - float(z[f"emass_n8_N{N}"])) <= 1e-11
+            assert abs(l2[N] - float(z[f"el2_n8_N{N}"])) <= 1e-10 * float(z[f"el2_n8_N{N}"])
     r = tmp_path / "r.csv"
     assert cli.main(["roundtrip", "--gen-source", "12,0.2,1,left", "--gen-target", "6,0.2,2,right",
                      "--samples", "64", "--seeds", "0", "--iterations", "3", "--out", str(r)]) == 0
@@ -265,3 +267,31 @@ def test_transfer_out_buffer(tt, small_pair):
     assert np.all(op.apply(zero, out=out2).coeffs == 0.0)          # b = 0 -> zeros in `out`
     with pytest.raises(tt.DimensionMismatch):
         tt.transfer_mc(target, tt.MeshBackedField(field), plan, out=torch.empty(3, dtype=torch.float64))
+
+
+@pytest.mark.parametrize("n", [8, 16, 32, 64])
+def test_supermesh_metrics_match_reference(tt, n):
+    """E_L2 and E_mass on the supermesh (metrics.py:35-74) for the reference's convergence
+    study (cli.py:151-191): with the REFERENCE's transferred coefficients the device
+    clip-and-integrate reproduces its E_L2 to 1e-12 relative and E_mass to 1e-14 absolute;
+    with this framework's own transfer (cg_tol 1e-14) to 1e-10 relative."""
+    from pathlib import Path
+    z = np.load(Path(__file__).resolve().parent / "golden" / "ref_stats.npz")
+    src = tt.generate_square_mesh(n, 0.2, seed=10 + n, diagonal="left")
+    tgt = tt.generate_square_mesh(n, 0.2, seed=20 + n, diagonal="right")
+    fs = tt.NodalField.from_function(src, tt.get_field("smooth").fn)
+    iset = tt.find_intersections(tgt, src)
+    cov = iset.per_target_area() / tgt.elem_areas
+    assert np.all(np.abs(cov - 1.0) <= 1e-12)
+    for N in (400, 1600):
+        ft = tt.NodalField(tgt, z[f"x_n{n}_N{N}"])
+        el2, em = float(z[f"el2_n{n}_N{N}"]), float(z[f"emass_n{n}_N{N}"])
+        assert abs(tt.supermesh_l2_error(fs, ft, iset) - el2) <= 1e-12 * el2
+        assert abs(tt.supermesh_mass_error(fs, ft, iset) - em) <= 1e-14
+        own = tt.transfer_mc(tgt, tt.MeshBackedField(fs), tt.SamplePlan.build(N, "sobol", 0), cg_tol=1e-14)
+        assert abs(tt.supermesh_l2_error(fs, own, iset) - el2) <= 1e-10 * el2
+    with pytest.raises(tt.CoverageGap):
+        shifted = tt.TriMesh.from_arrays(tgt.nodes + np.array([0.01, 0.0]), tgt.elements)
+        tt.find_intersections(shifted, src)
+    with pytest.raises(tt.DimensionMismatch):
+        tt.find_intersections(tt.generate_cube_mesh(2), tt.generate_cube_mesh(2))
