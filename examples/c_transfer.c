@@ -121,7 +121,7 @@ int main(int argc, char** argv) {
     CU(cudaMemset(status, 0, 4));
     double* wrec;
     CU(cudaMalloc((void**)&wrec, 8 * TT_WREC_STRIDE(2) * sne));
-    CK(tt_grid_walk_prep(&S, s_inc_s, s_inc, 1e-12, srec, wrec, NULL /* 2-D: neighbours in wrec */, status, st));
+    CK(tt_grid_walk_prep(&S, s_inc_s, s_inc, 1e-12, srec, wrec, status, st));
     G.walk = 1;
     G.wrec = wrec;
     int32_t* seeds;

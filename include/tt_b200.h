@@ -139,14 +139,13 @@ typedef struct tt_grid {
     const int32_t* cell_elems;  /* ascending element ids per cell */
     const double*  rec;         /* (n_elems, TT_REC_STRIDE(dim)) packed binv/origin */
     const double*  centroids;   /* (n_elems, dim) */
-    const double*  wrec;        /* optional compact walk records (n_elems, TT_WREC_STRIDE), 64 B,
-                                   64-byte aligned: origin (dim doubles), binv as float (dim*dim),
-                                   float tau_f [2-D: then int32 nbr[3]]; tt_grid_walk_prep */
-    const int32_t* wnbr;        /* 3-D walk: (n_elems, 4) facet neighbours (tt_grid_walk_prep) */
+    const double*  wrec;        /* optional compact walk records (n_elems, TT_WREC_STRIDE(dim)):
+                                   origin (dim doubles), binv as float (dim*dim), float tau_f,
+                                   int32 nbr[dim+1]; written by tt_grid_walk_prep */
 } tt_grid_t;
 
-/* compact walk record stride in doubles: 64 B, two 256-bit loads */
-#define TT_WREC_STRIDE(dim) 8
+/* compact walk record stride in doubles: 48 B (2-D), 80 B (3-D) */
+#define TT_WREC_STRIDE(dim) ((dim) == 2 ? 6 : 10)
 
 typedef struct tt_plan {
     int32_t  kind;            /* TT_PLAN_SHARED | TT_PLAN_PHILOX */
@@ -228,8 +227,7 @@ int tt_locate_many(const double* points, int64_t count, int nx, int ny,
 /* Certified facet walk: fills tau and nbr of every record from
  * the node incidence; sets TT_FLAG_NONMANIFOLD in *status for a non-manifold mesh. */
 int tt_grid_walk_prep(const tt_mesh_t* mesh, const int64_t* inc_start, const int32_t* inc,
-                      double eps, double* rec, double* wrec /* or NULL */,
-                      int32_t* wnbr /* (E, 4), 3-D with wrec, else NULL */, int32_t* status,
+                      double eps, double* rec, double* wrec /* or NULL */, int32_t* status,
                       void* stream);
 /* seeds[(e - e_lo)*TT_SEED_ANCHORS + s] = source element containing anchor point s of the
  * target element (reference scan, snapped when outside): s = 0 the centroid c, s = 1 + i the

@@ -41,7 +41,7 @@ def rec_stride(dim: int) -> int:
 
 
 def wrec_stride(dim: int) -> int:
-    return 8
+    return 6 if dim == 2 else 10
 
 
 class tt_mesh_t(C.Structure):
@@ -55,7 +55,7 @@ class tt_grid_t(C.Structure):
                 ("reserved", C.c_int32), ("lo", C.c_double * 3),
                 ("hi", C.c_double * 3), ("n_elems", C.c_int64), ("cell_start", C.c_void_p),
                 ("cell_elems", C.c_void_p), ("rec", C.c_void_p), ("centroids", C.c_void_p),
-                ("wrec", C.c_void_p), ("wnbr", C.c_void_p)]
+                ("wrec", C.c_void_p)]
 
 
 class tt_plan_t(C.Structure):
@@ -112,7 +112,7 @@ _SIGNATURES = {
     "tt_grid_fill": ([C.POINTER(tt_mesh_t), C.POINTER(tt_grid_t), _P, _P, _P], _I),
     "tt_locate": ([C.POINTER(tt_grid_t), _P, _I64, _D, _P, _P, _P], _I),
     "tt_locate_many": ([_P, _I64, _I, _I, C.POINTER(_D), _P, _P, _P, _P, _D, _P, _P, _P], _I),
-    "tt_grid_walk_prep": ([C.POINTER(tt_mesh_t), _P, _P, _D, _P, _P, _P, _P, _P], _I),
+    "tt_grid_walk_prep": ([C.POINTER(tt_mesh_t), _P, _P, _D, _P, _P, _P, _P], _I),
     "tt_seed_elements": ([C.POINTER(tt_grid_t), C.POINTER(tt_mesh_t), _I64, _I64, _P, _P, _P], _I),
     "tt_nearest": ([C.POINTER(tt_grid_t), _P, _I64, _P, _P], _I),
     "tt_snap": ([C.POINTER(tt_grid_t), _P, _I64, _P, _P, _P], _I),

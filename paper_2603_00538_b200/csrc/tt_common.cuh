@@ -154,40 +154,28 @@ TT_D void load_tail(const double* __restrict__ rec, int64_t e, RecTail<D>& t) {
     if constexpr (D == 3) t.nbr[3] = __ldg(reinterpret_cast<const int*>(q + 1));
 }
 
-// 256-bit non-coherent global load (sm_100: one LDG.E.ENL2.256 per lane); p 32-byte aligned.
-TT_D void ldg256(const void* p, uint64_t (&v)[4]) {
-    asm("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];"
-        : "=l"(v[0]), "=l"(v[1]), "=l"(v[2]), "=l"(v[3]) : "l"(p));
-}
-
-TT_D float lo_f(uint64_t w) { return __int_as_float((int)(uint32_t)w); }
-TT_D float hi_f(uint64_t w) { return __int_as_float((int)(uint32_t)(w >> 32)); }
-
-// Compact walk record, 64 B (one aligned half line), stride TT_WREC_STRIDE:
-//   3-D: origin o (3 doubles), binv as float (9), float tau_f; neighbours in grid.wnbr
-//   2-D: origin o (2 doubles), binv as float (4) | tau_f, int32 nbr[3], pad
+// Compact walk record: origin (double), binv (float), tau_f (float), nbr (int32).
 template <int D>
 struct WRec {
     double o[D];
     float b[D][D];
     float tau;
+    int nbr[D + 1];
 };
 
 template <int D>
-TT_D void load_wrec(const double* __restrict__ wrec, int64_t e, WRec<D>& w, int* nbr2 = nullptr) {
-    // four LDG.128 of one 64-byte-aligned half line (no record straddles a line).  Measured:
-    // two 256-bit loads per test issue fewer instructions but cost MORE L1 wavefronts (1.22
-    // vs 1.12 ms at C2): a 32 B lane access takes two wavefronts of the LSU data path.
-    const int4* q = reinterpret_cast<const int4*>(wrec + e * 8);
-    const int4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
+TT_D void load_wrec(const double* __restrict__ wrec, int64_t e, WRec<D>& w) {
     if constexpr (D == 2) {
+        const int4* q = reinterpret_cast<const int4*>(wrec + e * 6);
+        const int4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
         w.o[0] = __hiloint2double(a.y, a.x); w.o[1] = __hiloint2double(a.w, a.z);
         w.b[0][0] = __int_as_float(b.x); w.b[0][1] = __int_as_float(b.y);
         w.b[1][0] = __int_as_float(b.z); w.b[1][1] = __int_as_float(b.w);
         w.tau = __int_as_float(c.x);
-        if (nbr2) { nbr2[0] = c.y; nbr2[1] = c.z; nbr2[2] = c.w; }
+        w.nbr[0] = c.y; w.nbr[1] = c.z; w.nbr[2] = c.w;
     } else {
-        const int4 d = __ldg(q + 3);
+        const int4* q = reinterpret_cast<const int4*>(wrec + e * 10);
+        const int4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2), d = __ldg(q + 3), f = __ldg(q + 4);
         w.o[0] = __hiloint2double(a.y, a.x); w.o[1] = __hiloint2double(a.w, a.z);
         w.o[2] = __hiloint2double(b.y, b.x);
         w.b[0][0] = __int_as_float(b.z); w.b[0][1] = __int_as_float(b.w);
@@ -195,6 +183,7 @@ TT_D void load_wrec(const double* __restrict__ wrec, int64_t e, WRec<D>& w, int*
         w.b[1][1] = __int_as_float(c.z); w.b[1][2] = __int_as_float(c.w);
         w.b[2][0] = __int_as_float(d.x); w.b[2][1] = __int_as_float(d.y);
         w.b[2][2] = __int_as_float(d.z); w.tau = __int_as_float(d.w);
+        w.nbr[0] = f.x; w.nbr[1] = f.y; w.nbr[2] = f.z; w.nbr[3] = f.w;
     }
 }
 
@@ -208,7 +197,6 @@ struct GridDev {
     const double* __restrict__ rec;
     const double* __restrict__ centroids;
     const double* __restrict__ wrec;
-    const int32_t* __restrict__ wnbr;  // 3-D facet neighbours of the walk (E, 4)
 };
 
 inline GridDev to_dev(const tt_grid_t& g) {
@@ -219,7 +207,6 @@ inline GridDev to_dev(const tt_grid_t& g) {
     d.cell_start = g.cell_start; d.cell_elems = g.cell_elems;
     d.rec = g.rec; d.centroids = g.centroids;
     d.wrec = g.wrec;
-    d.wnbr = g.wnbr;
     return d;
 }
 

@@ -314,7 +314,7 @@ __global__ void walk_prep_kernel(int64_t E, const double* __restrict__ nodes,
                                  const int64_t* __restrict__ inc_start,
                                  const int32_t* __restrict__ inc, double eps, double dmax,
                                  double* __restrict__ rec, double* __restrict__ wrec,
-                                 int32_t* __restrict__ wnbr, int32_t* __restrict__ status) {
+                                 int32_t* __restrict__ status) {
     constexpr int K = D + 1;
     constexpr int S = (D == 2) ? 8 : 16;
     int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -399,18 +399,14 @@ __global__ void walk_prep_kernel(int64_t E, const double* __restrict__ nodes,
             }
         double tau_f = tau + 9.5367431640625e-07 * (4.0 * babs * diam * 1.0001 + 8.0);
         if (!(tau_f < 0.25)) tau_f = 2.0;
-        double* w = wrec + e * 8;                                     // 64 B record
+        constexpr int WS = (D == 2) ? 6 : 10;
+        double* w = wrec + e * WS;
         for (int c = 0; c < D; ++c) w[c] = rb[D * D + c];           // origin (double)
         float* wf = reinterpret_cast<float*>(w + D);
         for (int i = 0; i < D * D; ++i) wf[i] = __double2float_rn(rb[i]);
         wf[D * D] = __double2float_ru(tau_f);
         int* wn = reinterpret_cast<int*>(wf + D * D + 1);
-        if constexpr (D == 2) {
-            for (int i = 0; i < K; ++i) wn[i] = nbr[i];
-            wn[3] = 0; wn[4] = 0; wn[5] = 0; wn[6] = 0;                // pad to 64 B
-        } else {
-            reinterpret_cast<int4*>(wnbr)[e] = make_int4(nbr[0], nbr[1], nbr[2], nbr[3]);
-        }
+        for (int i = 0; i < K; ++i) wn[i] = nbr[i];
     }
 }
 
@@ -615,10 +611,9 @@ extern "C" int tt_snap(const tt_grid_t* g, const double* pts, int64_t K, int32_t
 }
 
 extern "C" int tt_grid_walk_prep(const tt_mesh_t* m, const int64_t* inc_start, const int32_t* inc,
-                                 double eps, double* rec, double* wrec, int32_t* wnbr, int32_t* status,
-                                 void* stream) {
-    if (!m || (m->dim != 2 && m->dim != 3) || !inc_start || !inc || !rec || (m->dim == 3 && wrec && !wnbr)) {
-        set_error("tt_grid_walk_prep: bad arguments (3-D walk records need wnbr)");
+                                 double eps, double* rec, double* wrec, int32_t* status, void* stream) {
+    if (!m || (m->dim != 2 && m->dim != 3) || !inc_start || !inc || !rec) {
+        set_error("tt_grid_walk_prep: bad arguments");
         return TT_ERR_INVALID_PARAMETER;
     }
     if (m->n_elems == 0) return TT_OK;
@@ -640,10 +635,10 @@ extern "C" int tt_grid_walk_prep(const tt_mesh_t* m, const int64_t* inc_start, c
     memcpy(&dmax, &bits, sizeof(dmax));
     if (m->dim == 2)
         walk_prep_kernel<2><<<grid_for(m->n_elems, 128), 128, 0, s>>>(m->n_elems, m->nodes, m->elems,
-                                                                      inc_start, inc, eps, dmax, rec, wrec, wnbr, status);
+                                                                      inc_start, inc, eps, dmax, rec, wrec, status);
     else
         walk_prep_kernel<3><<<grid_for(m->n_elems, 128), 128, 0, s>>>(m->n_elems, m->nodes, m->elems,
-                                                                      inc_start, inc, eps, dmax, rec, wrec, wnbr, status);
+                                                                      inc_start, inc, eps, dmax, rec, wrec, status);
     return launch_check("walk_prep_kernel");
 }
 

@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(kMcBlock, kMcMinBlocks) mc_mesh_kernel(TargetD
     const int64_t n_el = e_hi - e_lo;
     const int64_t N = plan.n;
     const GridDev& g = src.grid;
-    const bool walk = g.walk && src.seeds && g.wrec && (D == 2 || g.wnbr);
+    const bool walk = g.walk && src.seeds && g.wrec;
     int flags = 0;
     constexpr bool USE_SLOT = SLOT && PLAN == TT_PLAN_SHARED;
     extern __shared__ int8_t s_slot[];  // N bytes (launch: dynamic shared memory)
@@ -355,10 +355,7 @@ __global__ void __launch_bounds__(kMcBlock, kMcMinBlocks) mc_mesh_kernel(TargetD
         }
         __syncthreads();
     }
-    // vertex rows padded to an odd number of doubles: the 8-byte reads of the warp's groups
-    // land in distinct bank pairs (12-double rows put groups 0 and 4 on the same banks)
-    constexpr int VS = (K * D) | 1;
-    __shared__ double s_v[NW][EPW][VS];
+    __shared__ double s_v[NW][EPW][K * D];
     __shared__ int s_seed[NW][EPW][kSeeds];
     const int wib = threadIdx.x >> 5, gib = lane / G;
 
@@ -430,8 +427,7 @@ __global__ void __launch_bounds__(kMcBlock, kMcMinBlocks) mc_mesh_kernel(TargetD
                 // evaluation error (tt_grid.cu walk_prep_kernel); f from the element's
                 // gradient record: f = c_last + g . (x - o), accurate to a few ulps
                 WRec<D> w;
-                int nb2[3];
-                load_wrec<D>(g.wrec, cur, w, D == 2 ? nb2 : nullptr);
+                load_wrec<D>(g.wrec, cur, w);
                 double2 pc0 = make_double2(0.0, 0.0), pc1 = make_double2(0.0, 0.0);
                 if (src.egrad) {  // speculative: the gradient record of the element tested
                     const double2* q = reinterpret_cast<const double2*>(src.egrad + (int64_t)cur * 4);
@@ -471,17 +467,10 @@ __global__ void __launch_bounds__(kMcBlock, kMcMinBlocks) mc_mesh_kernel(TargetD
                     fb = cur;  // within the uncertainty band of a facet: exact double walk
                     cur = -1;
                 } else {
-                    int nbr[K];
-                    if constexpr (D == 2) {
-                        nbr[0] = nb2[0]; nbr[1] = nb2[1]; nbr[2] = nb2[2];
-                    } else {
-                        const int4 q = __ldg(reinterpret_cast<const int4*>(g.wnbr) + cur);
-                        nbr[0] = q.x; nbr[1] = q.y; nbr[2] = q.z; nbr[3] = q.w;
-                    }
-                    int nb = nbr[0];
+                    int nb = w.nbr[0];
 #pragma unroll
                     for (int i = 1; i <= D; ++i)
-                        if (imin == i) nb = nbr[i];
+                        if (imin == i) nb = w.nbr[i];
                     cur = nb;
                     ++steps;
                     TT_STAT(3, 1);

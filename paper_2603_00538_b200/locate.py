@@ -128,7 +128,6 @@ class UniformGridLocator:
         g.centroids = _lib.ptr(dm.centroids).value
         if self.walk and getattr(dm, "wrec", None) is not None:
             g.wrec = _lib.ptr(dm.wrec).value
-            g.wnbr = _lib.ptr(dm.wnbr).value
         return g
 
     def seeds_for(self, target) -> torch.Tensor:
@@ -243,14 +242,10 @@ def _walk_prep(mesh):
     inc_start, inc = dm.incidence
     status = _lib.status_word()
     desc = dm.desc()
-    # 64 B records read with 256-bit loads (torch allocations are 512-byte aligned)
     dm.wrec = torch.empty((mesh.n_elems, _lib.wrec_stride(mesh.DIM)), dtype=torch.float64,
                           device=dm.nodes.device)
-    dm.wnbr = (torch.empty((mesh.n_elems, 4), dtype=torch.int32, device=dm.nodes.device)
-               if mesh.DIM == 3 else None)
     _lib.call("tt_grid_walk_prep", C.byref(desc), _lib.ptr(inc_start), _lib.ptr(inc), EPS_LOC,
-              _lib.ptr(dm.rec), _lib.ptr(dm.wrec), _lib.ptr(dm.wnbr), _lib.ptr(status),
-              _lib.stream_handle())
+              _lib.ptr(dm.rec), _lib.ptr(dm.wrec), _lib.ptr(status), _lib.stream_handle())
     if int(status.item()) & _lib.TT_FLAG_NONMANIFOLD:
         raise NonManifold("a facet is shared by more than two elements")
     dm.walk_ready = True
