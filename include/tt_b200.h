@@ -23,6 +23,7 @@
  *   tt_mc_load            <- montecarlo._accumulate            montecarlo.py:110-141
  *                            (+ SourceField.__call__: AnalyticField :20-29,
  *                             MeshBackedField :49-65, NodalField.eval_in_elements fem.py:36-38)
+ *   tt_mc_load_density    <- montecarlo.assemble_load_mc_weighted montecarlo.py:165-176
  *   tt_mc_cache_ids       <- MCTransferOperator.__init__ localisation transfer.py:74-87
  *   tt_mc_fold(_finish)   <- MCTransferOperator load matrix fold  transfer.py:88-110
  *   tt_spmv_rect          <- MCTransferOperator.apply R @ c      transfer.py:112-115
@@ -253,6 +254,13 @@ int tt_mc_load(const tt_mesh_t* target, int64_t e_lo, int64_t e_hi, const tt_pla
                double* contrib /* (e_hi-e_lo, k) or NULL */,
                double* b /* (n_nodes) atomically accumulated when contrib == NULL */,
                int32_t* status, void* stream);
+
+/* importance-weighted load (montecarlo.py:165-176): contrib[e, a] = sum_j f_j / (N p_ej) lambda_ja
+ * with the caller's densities p (e_hi-e_lo, N) for a shared plan; p <= 0 sets
+ * TT_FLAG_INVALID_DENSITY, non-finite f TT_FLAG_NONFINITE */
+int tt_mc_load_density(const tt_mesh_t* target, int64_t e_lo, int64_t e_hi, const tt_plan_t* plan,
+                       const tt_source_t* src, const double* density, double* contrib,
+                       int32_t* status, void* stream);
 
 int tt_mc_cache_ids(const tt_mesh_t* target, int64_t e_lo, int64_t e_hi, const tt_plan_t* plan,
                     const tt_grid_t* grid, const int32_t* seeds /* (E_target, TT_SEED_ANCHORS) or NULL */,

@@ -120,6 +120,8 @@ _SIGNATURES = {
     "tt_eval_points": ([C.POINTER(tt_source_t), _P, _I64, _P, _P, _P], _I),
     "tt_mc_load": ([C.POINTER(tt_mesh_t), _I64, _I64, C.POINTER(tt_plan_t),
                     C.POINTER(tt_source_t), _P, _P, _P, _P], _I),
+    "tt_mc_load_density": ([C.POINTER(tt_mesh_t), _I64, _I64, C.POINTER(tt_plan_t),
+                            C.POINTER(tt_source_t), _P, _P, _P, _P], _I),
     "tt_mc_cache_ids": ([C.POINTER(tt_mesh_t), _I64, _I64, C.POINTER(tt_plan_t),
                          C.POINTER(tt_grid_t), _P, _P, _P], _I),
     "tt_pack_coeffs": ([C.POINTER(tt_mesh_t), _P, _P, _P], _I),

@@ -31,6 +31,7 @@ struct SrcDev {
     const int32_t* __restrict__ seeds;
     const double* __restrict__ ecoef;
     const double* __restrict__ egrad;
+    const double* __restrict__ density;  // importance weights p (e_hi-e_lo, N), or NULL = 1/|T|
 };
 
 template <int D>
@@ -219,6 +220,12 @@ __global__ void __launch_bounds__(256) mc_load_kernel(TargetDev t, int64_t e_lo,
                 map_point<D>(lam, v, x);
                 double f = eval_source<D, SRC>(src, expr, x, le * N + j, flags, guess);
                 if (!isfinite(f)) flags |= TT_FLAG_NONFINITE;
+                if (src.density) {
+                    // importance-weighted estimator: f / (N p) per sample (montecarlo.py:128-131)
+                    const double p = __ldg(src.density + le * N + j);
+                    if (p <= 0.0) flags |= TT_FLAG_INVALID_DENSITY;
+                    f = f / ((double)N * p);
+                }
 #pragma unroll
                 for (int i = 0; i < K; ++i) acc[i] = fma(f, lam[i], acc[i]);
             }
@@ -229,8 +236,9 @@ __global__ void __launch_bounds__(256) mc_load_kernel(TargetDev t, int64_t e_lo,
 #pragma unroll
             for (int i = 0; i < K; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], off);
         if (active && sub_lane == 0) {
-            // (sum f lam) / (N p), p = 1/|T|  (montecarlo.py:128-131, :135-141)
-            const double q = (double)N * (1.0 / __ldg(t.measure + e));
+            // (sum f lam) / (N p), p = 1/|T|  (montecarlo.py:128-131, :135-141); with a
+            // density the weights were applied per sample
+            const double q = src.density ? 1.0 : (double)N * (1.0 / __ldg(t.measure + e));
             if (contrib) {
 #pragma unroll
                 for (int i = 0; i < K; ++i) contrib[le * K + i] = acc[i] / q;
@@ -355,8 +363,11 @@ __global__ void __launch_bounds__(kMcBlock, kMcMinBlocks) mc_mesh_kernel(TargetD
         }
         __syncthreads();
     }
-    __shared__ double s_v[NW][EPW][K * D];
-    __shared__ int s_seed[NW][EPW][kSeeds];
+    // vertex rows of VS doubles read as double2 (LDS.128): VS = 2 (mod 4) puts the 16-byte
+    // reads of a warp's (up to 8) groups on distinct bank quads; seed rows padded to 17 ints
+    constexpr int VS = D == 3 ? 14 : 6;
+    __shared__ __align__(16) double s_v[NW][EPW][VS];
+    __shared__ int s_seed[NW][EPW][kSeeds + 1];
     const int wib = threadIdx.x >> 5, gib = lane / G;
 
     for (int64_t tile = warp; tile * EPW < n_el; tile += nwarps) {
@@ -377,7 +388,13 @@ __global__ void __launch_bounds__(kMcBlock, kMcMinBlocks) mc_mesh_kernel(TargetD
         __syncwarp();
         const auto vertices = [&](double (*vv)[D]) {
 #pragma unroll
-            for (int q = 0; q < K * D; ++q) vv[q / D][q % D] = s_v[wib][gib][q];
+            const double2* row = reinterpret_cast<const double2*>(s_v[wib][gib]);
+#pragma unroll
+            for (int q = 0; q < K * D / 2; ++q) {
+                const double2 u = row[q];
+                vv[(2 * q) / D][(2 * q) % D] = u.x;
+                vv[(2 * q + 1) / D][(2 * q + 1) % D] = u.y;
+            }
         };
         int next = 0;
         int jcur = 0;
@@ -752,6 +769,7 @@ static SrcDev to_src(const tt_source_t& s) {
     d.seeds = s.seeds;
     d.ecoef = s.elem_coeffs;
     d.egrad = s.elem_grad;
+    d.density = nullptr;
     return d;
 }
 
@@ -928,6 +946,69 @@ extern "C" int tt_mc_load(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const 
     if (e_hi == e_lo) return TT_OK;
     if (t->dim == 2) return dispatch_plan<2>(t, e_lo, e_hi, p, s, contrib, b, nullptr, status, as_stream(stream));
     return dispatch_plan<3>(t, e_lo, e_hi, p, s, contrib, b, nullptr, status, as_stream(stream));
+}
+
+// Importance-weighted load (montecarlo.py:165-176): the simple sample loop (mc_load_kernel)
+// for every source kind, f / (N p_j) per sample with the caller's densities.
+template <int D, int SRC, int G>
+static int launch_density(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_plan_t* p,
+                          const tt_source_t* s, const double* density, double* contrib,
+                          int32_t* status, cudaStream_t st) {
+    TargetDev td{t->nodes, t->elems, t->measure, t->gid};
+    PlanDev pd{p->n_samples, p->lam, p->seed};
+    SrcDev sd = to_src(*s);
+    sd.density = density;
+    constexpr int EPW = 32 / G;
+    const int64_t tiles = (e_hi - e_lo + EPW - 1) / EPW;
+    static const int per = blocks_per_sm(mc_load_kernel<D, TT_PLAN_SHARED, SRC, G>, 256, 0);
+    int64_t blocks = (tiles + 7) / 8;
+    const int64_t cap = (int64_t)sm_count() * per * 16;
+    blocks = blocks > cap ? cap : blocks < 1 ? 1 : blocks;
+    mc_load_kernel<D, TT_PLAN_SHARED, SRC, G><<<(unsigned)blocks, 256, 0, st>>>(td, e_lo, e_hi, pd, sd, s->expr,
+                                                                               contrib, nullptr, status);
+    return launch_check("mc_load_kernel (density)");
+}
+
+template <int D, int SRC>
+static int density_g(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_plan_t* p,
+                     const tt_source_t* s, const double* density, double* contrib, int32_t* status,
+                     cudaStream_t st) {
+    const int G = lanes_per_element(TT_SRC_VALUES, p->n_samples);
+    if (G <= 4) return launch_density<D, SRC, 4>(t, e_lo, e_hi, p, s, density, contrib, status, st);
+    if (G == 8) return launch_density<D, SRC, 8>(t, e_lo, e_hi, p, s, density, contrib, status, st);
+    if (G == 16) return launch_density<D, SRC, 16>(t, e_lo, e_hi, p, s, density, contrib, status, st);
+    return launch_density<D, SRC, 32>(t, e_lo, e_hi, p, s, density, contrib, status, st);
+}
+
+template <int D>
+static int density_src(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_plan_t* p,
+                       const tt_source_t* s, const double* density, double* contrib, int32_t* status,
+                       cudaStream_t st) {
+    switch (s->kind) {
+        case TT_SRC_EXPR: return density_g<D, TT_SRC_EXPR>(t, e_lo, e_hi, p, s, density, contrib, status, st);
+        case TT_SRC_MESH: return density_g<D, TT_SRC_MESH>(t, e_lo, e_hi, p, s, density, contrib, status, st);
+        case TT_SRC_VALUES: return density_g<D, TT_SRC_VALUES>(t, e_lo, e_hi, p, s, density, contrib, status, st);
+    }
+    set_error("tt_mc_load_density: unsupported source kind %d", s->kind);
+    return TT_ERR_INVALID_PARAMETER;
+}
+
+extern "C" int tt_mc_load_density(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_plan_t* p,
+                                  const tt_source_t* s, const double* density, double* contrib,
+                                  int32_t* status, void* stream) {
+    if (!t || !p || (t->dim != 2 && t->dim != 3) || p->dim != t->dim || p->kind != TT_PLAN_SHARED || !p->lam) {
+        set_error("tt_mc_load_density: needs a shared plan of the target's dimension");
+        return TT_ERR_INVALID_PARAMETER;
+    }
+    if (e_lo < 0 || e_hi > t->n_elems || e_lo > e_hi || p->n_samples < 1 || !density || !contrib) {
+        set_error("tt_mc_load_density: bad element range, sample count or buffers");
+        return TT_ERR_INVALID_PARAMETER;
+    }
+    int st = check_source(s, t->dim);
+    if (st) return st;
+    if (e_hi == e_lo) return TT_OK;
+    if (t->dim == 2) return density_src<2>(t, e_lo, e_hi, p, s, density, contrib, status, as_stream(stream));
+    return density_src<3>(t, e_lo, e_hi, p, s, density, contrib, status, as_stream(stream));
 }
 
 extern "C" int tt_mc_cache_ids(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_plan_t* p,

@@ -390,39 +390,53 @@ def assemble_load_mc_weighted(target, source, plan: SamplePlan, density, workers
                               device: bool = False):
     """Importance-sampled estimator sum f psi / (N p) (montecarlo.py:165-176).
 
-    ``density(elems, pts (E,N,d)) -> (E,N)`` is a host callable.  A density equal to
-    1/|T| at every sample reproduces ``assemble_load_mc`` bitwise (the same kernel is
-    used); any other density is applied to device-evaluated source values.
+    ``density(elems, pts (E,N,d)) -> (E,N)`` is the caller's host callable: it is queried
+    with host points, chunk by chunk, and its values are uploaded; the source is
+    evaluated on the device (analytic programs, mesh-backed fields) or through its own
+    host protocol (black boxes), and ``tt_mc_load_density`` accumulates f / (N p) psi.
+    A density equal to 1/|T| at every sample reproduces ``assemble_load_mc`` bitwise (the
+    uniform kernel is used).  Errors as the reference: a non-finite source value raises
+    SourceEvalFailed before a non-positive density raises InvalidDensity.
     """
     if plan.per_element:
         raise InvalidParameter("importance weighting needs a shared sample plan")
+    if plan.dim != target.DIM:
+        raise DimensionMismatch(f"{plan.dim}-D plan on a {target.DIM}-D mesh")
     dm = target.device
+    dev = dm.nodes.device
     n = plan.n_samples
+    k = target.DIM + 1
     inv_area = 1.0 / target.elem_areas
     chunk = max(1, _HOST_CHUNK_POINTS // n)
-    dens = []
+    sdesc, keep = _source_desc(source, target.DIM, target)
+    mdesc, pdesc = dm.desc(), plan.desc()
+    contrib = torch.empty((target.n_elems, k), dtype=torch.float64, device=dev)
+    status = _lib.status_word()
     uniform = True
     for c0 in range(0, target.n_elems, chunk):
         c1 = min(c0 + chunk, target.n_elems)
         pts = map_points(target, plan, c0, c1).cpu().numpy()
-        p = np.asarray(density(np.arange(c0, c1), pts), dtype=np.float64)
-        p = np.broadcast_to(p, (c1 - c0, n))
-        if np.any(p <= 0.0):
-            raise InvalidDensity("density must be strictly positive at samples")
+        p = np.ascontiguousarray(np.broadcast_to(
+            np.asarray(density(np.arange(c0, c1), pts), dtype=np.float64), (c1 - c0, n)))
         uniform = uniform and bool(np.all(p == inv_area[c0:c1, None]))
-        dens.append(p)
+        pd = torch.from_numpy(p).to(dev)
+        desc = sdesc
+        vals = None
+        if desc is None:   # host black box: its values through the reference protocol
+            f = np.asarray(source(pts.reshape(-1, target.DIM)), dtype=np.float64)
+            if f.size != (c1 - c0) * n:
+                raise DimensionMismatch(f"source returned {f.size} values for {(c1 - c0) * n} points")
+            vals = torch.from_numpy(np.ascontiguousarray(f.reshape(-1))).to(dev)
+            desc = _lib.tt_source_t()
+            desc.kind = _lib.TT_SRC_VALUES
+            desc.dim = target.DIM
+            desc.values = _lib.ptr(vals).value
+        _lib.call("tt_mc_load_density", C.byref(mdesc), c0, c1, C.byref(pdesc), C.byref(desc),
+                  _lib.ptr(pd), _lib.ptr(contrib[c0:]), _lib.ptr(status), _lib.stream_handle())
+        del vals, pd
+    _raise_status(int(status.item()))
     if uniform:
         return assemble_load_mc(target, source, plan, device=device)
-    pts = map_points(target, plan)
-    f = source(pts.reshape(-1, target.DIM)) if isinstance(source, (AnalyticField, MeshBackedField)) \
-        else torch.from_numpy(np.asarray(source(pts.cpu().numpy().reshape(-1, target.DIM)),
-                                         dtype=np.float64))
-    f = torch.as_tensor(f, device=dm.nodes.device).reshape(target.n_elems, n)
-    if not bool(torch.isfinite(f).all()):
-        raise SourceEvalFailed("source returned a non-finite value")
-    p = torch.from_numpy(np.concatenate(dens, axis=0)).to(dm.nodes.device)
-    w = f / (n * p)
-    contrib = (w @ plan.barycentric_dev).contiguous()
     b = dm.reduce_nodes(contrib)
     return b if device else b.cpu().numpy()
 
