@@ -19,6 +19,7 @@ ap.add_argument("--n", type=int, default=55)
 ap.add_argument("--samples", type=int, default=64)
 ap.add_argument("--steps", type=int, default=2)
 ap.add_argument("--mode", default="sobol")
+ap.add_argument("--c5", action="store_true", help="repeated coupling: folded R @ c + PCG")
 a = ap.parse_args()
 tgt = tt.generate_cube_mesh(a.n, 0.2, seed=20, split="kuhn")
 src = tt.generate_cube_mesh(a.n, 0.2, seed=10, split="kuhn_mirror")
@@ -26,9 +27,11 @@ fs = tt.NodalField.from_function(src, tt.get_field("smooth", dim=3).fn)
 box = tt.MeshBackedField(fs, tt.UniformGridLocator.build(src))
 mass = tgt.device.mass
 plan = tt.SamplePlan.build(a.samples, a.mode, 0, dim=3)
+op = tt.MCTransferOperator(tgt, src, plan) if a.c5 else None
 torch.cuda.synchronize()
 for _ in range(a.steps):
-    b = load_vector(tgt, box, plan, check=False)
+    fs._packed = fs._grad = None        # new coefficients every coupling step (as bench.py)
+    b = op.load(fs, check=False) if op else load_vector(tgt, box, plan, check=False)
     x, _, res = pcg_device(mass, b, tol=1e-12)
 torch.cuda.synchronize()
 print("ok", float(x.sum()))
