@@ -19,7 +19,7 @@ from .locate import EPS_LOC, OUTSIDE, UniformGridLocator
 from .montecarlo import (AnalyticField, MeshBackedField, SamplePlan, assemble_load_mc,
                          assemble_load_mc_weighted, bary_map, importance_weights)
 from .fields import NAMED_FIELDS, get_field, parse_field
-from .transfer import MCTransferOperator, transfer_mc
+from .transfer import CouplingStep, MCTransferOperator, transfer_mc
 from .metrics import (ErrorReport, IntersectionSet, dof_l2_error, find_intersections, mass_error,
                       mesh_mass_error, supermesh_l2_error, supermesh_mass_error)
 
@@ -33,7 +33,7 @@ __all__ = [
     "AnalyticField", "MeshBackedField", "SamplePlan", "assemble_load_mc",
     "assemble_load_mc_weighted", "importance_weights", "bary_map",
     "NAMED_FIELDS", "get_field", "parse_field",
-    "MCTransferOperator", "transfer_mc",
+    "MCTransferOperator", "transfer_mc", "CouplingStep",
     "ErrorReport", "dof_l2_error", "mesh_mass_error", "mass_error", "IntersectionSet",
     "find_intersections", "supermesh_l2_error", "supermesh_mass_error", "CoverageGap",
     "kernel_backend",

@@ -311,7 +311,10 @@ class DistributedPCG:
         d.send_idx, d.n_send = _lib.ptr(self.send_idx).value, len(plan.send_node_rows)
         d.send_buf, d.part = _lib.ptr(self.send_buf).value, _lib.ptr(self.part).value
         d.sums, d.state = _lib.ptr(self.sums).value, _lib.ptr(self.state).value
+        self.b = torch.zeros(max(n_on, 1), **f64)
+        d.b = _lib.ptr(self.b).value
         self.desc = d
+        self._graph = None
 
     def _call(self, name):
         _lib.call(name, C.byref(self.desc), _lib.stream_handle())
@@ -325,23 +328,41 @@ class DistributedPCG:
         self.comm.allreduce_(self.sums)
         self._call("tt_dpcg_scalars")
 
+    def _iterations(self, n: int):
+        for _ in range(n):
+            self._call("tt_dpcg_update")
+            self._exchange_and_reduce()
+
+    def _chunk(self, n: int):
+        """``n`` iterations: with NCCL one CUDA-graph replay of (update, pack, halo
+        all-to-all, spmv, all-reduce, scalars) x n, captured on first use -- every pointer
+        and all iteration scalars live in persistent device buffers, so the graph serves
+        every solve; host-staged backends run them eagerly."""
+        if self.comm.staged:
+            return self._iterations(n)
+        if self._graph is None:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._iterations(n)
+            self._graph = (g, n)
+        g, gn = self._graph
+        for _ in range(-(-n // gn)):
+            g.replay()
+
     def solve(self, b_own: torch.Tensor, tol: float = 1e-12, maxiter: int | None = None,
               chunk: int = 8):
         """Launch the solve of the owned rows; returns (x_own, best_x_own, result) after
-        the iteration's device state reports done (one host read per ``chunk`` iterations)."""
+        the iteration's device state reports done (one host read per ``chunk`` iterations;
+        iterations past done are no-ops)."""
         maxiter = 10 * self.n_global if maxiter is None else int(maxiter)
-        self.b = b_own.contiguous()
-        self.desc.b = _lib.ptr(self.b).value
+        if b_own.numel():
+            self.b[:self.n_own].copy_(b_own)
         self.desc.tol, self.desc.maxiter = float(tol), maxiter
         self._call("tt_dpcg_start")
         self._exchange_and_reduce()
         done_word = self.state.view(torch.int32)[_DONE_INT32:_DONE_INT32 + 1]
-        it = 0
         while not int(done_word.item()):
-            for _ in range(min(chunk, max(1, maxiter - it))):
-                self._call("tt_dpcg_update")
-                self._exchange_and_reduce()
-            it += chunk
+            self._chunk(chunk)
         _lib.call("tt_dpcg_finish", C.byref(self.desc), _lib.ptr(self.result), _lib.stream_handle())
         return self.vec["x"][:self.n_own], self.vec["best_x"][:self.n_own], self.result
 

@@ -135,3 +135,82 @@ class MCTransferOperator:
         b = load_vector(self.target, source, self.plan, check=False, status=status)
         x, best_x, res = pcg_device(self.mass, b, tol=self.cg_tol)
         return solved_field(self.target, x, best_x, res, status, out)
+
+
+class CouplingStep:
+    """One coupling step of a fixed (target, source mesh, plan) triple as ONE CUDA-graph
+    replay: H2D of the source coefficients -> gradient pack -> fused MC load -> ordered node
+    gather -> PCG -> D2H of the solution (extension for coupling loops; each call is the
+    reference's ``transfer_mc(target, MeshBackedField(NodalField(source, c)), plan)``,
+    transfer.py:158-163, with the same results and errors).
+
+    ``step(coeffs)`` takes the source nodal coefficients (host array or tensor) and returns
+    the target ``NodalField`` whose ``.coeffs`` is a host array.  The graph is captured on
+    the first call (after one eager warm-up step that builds the cached mesh state); a
+    device without graph support for a kernel falls back to eager launches.
+    """
+
+    def __init__(self, target, source_mesh, plan: SamplePlan, cg_tol: float = 1e-12,
+                 source_locator: UniformGridLocator | None = None, outside: str = "snap"):
+        from .montecarlo import MeshBackedField
+        if target.DIM != source_mesh.DIM or plan.dim != target.DIM:
+            raise DimensionMismatch("target, source mesh and plan dimensions differ")
+        self.target, self.source_mesh, self.plan, self.cg_tol = target, source_mesh, plan, cg_tol
+        dev = _lib.device()
+        self.c_dev = torch.zeros(source_mesh.n_nodes, dtype=torch.float64, device=dev)
+        self.c_host = torch.zeros(source_mesh.n_nodes, dtype=torch.float64).pin_memory()
+        self.x_host = torch.zeros(target.n_nodes, dtype=torch.float64).pin_memory()
+        self.flags_host = torch.zeros(8, dtype=torch.float64).pin_memory()   # result (4) + status
+        self.field = NodalField(source_mesh, self.c_dev)
+        self.source = MeshBackedField(self.field, source_locator, outside)
+        self.status = _lib.status_word()
+        self.mass = target.device.mass
+        self._graph = None
+
+    def _body(self):
+        from .montecarlo import load_vector
+        self.c_dev.copy_(self.c_host, non_blocking=True)
+        self.status.zero_()
+        self.field._grad = self.field._packed = None    # new coefficients: repack in the step
+        b = load_vector(self.target, self.source, self.plan, check=False, status=self.status)
+        x, best_x, res = pcg_device(self.mass, b, tol=self.cg_tol)
+        self.x_host.copy_(x, non_blocking=True)
+        self.flags_host[:4].copy_(res, non_blocking=True)
+        self.flags_host[4:5].view(torch.int32)[:1].copy_(self.status, non_blocking=True)
+        self._out = (x, best_x, res)
+
+    def __call__(self, coeffs) -> NodalField:
+        """The transferred field.  Like ``transfer_mc(..., out=)``, its device and host
+        coefficient buffers belong to this step object and are overwritten by the next
+        call (copy them to keep them)."""
+        c = coeffs.coeffs_dev if isinstance(coeffs, NodalField) else coeffs
+        self.c_host.copy_(torch.as_tensor(c, dtype=torch.float64).reshape(-1))
+        if self._graph is None:
+            self._body()                    # eager warm-up: builds every cached state
+            torch.cuda.current_stream().synchronize()
+            try:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    self._body()
+                self._graph = g
+            except RuntimeError:
+                self._graph = False         # (no graph support for a kernel: eager steps)
+        if self._graph:
+            self._graph.replay()
+        else:
+            self._body()
+        torch.cuda.current_stream().synchronize()
+        x, best_x, res = self._out
+        raw = self.flags_host.numpy().tobytes()
+        r = _lib.tt_pcg_result_t.from_buffer_copy(raw[:C.sizeof(_lib.tt_pcg_result_t)])
+        flags = int(self.flags_host[4:5].view(torch.int32)[0])
+        if flags:
+            _raise_status(flags)
+        if r.zero_rhs:
+            return NodalField(self.target, torch.zeros_like(x))
+        if not r.converged:
+            from .errors import NoConvergence
+            raise NoConvergence(best_x.cpu().numpy(), float(r.best_residual), int(r.iterations))
+        field = NodalField(self.target, x)
+        field._host = self.x_host.numpy()
+        return field

@@ -295,3 +295,25 @@ def test_supermesh_metrics_match_reference(tt, n):
         tt.find_intersections(shifted, src)
     with pytest.raises(tt.DimensionMismatch):
         tt.find_intersections(tt.generate_cube_mesh(2), tt.generate_cube_mesh(2))
+
+
+def test_coupling_step_graph_matches_transfer_mc(tt):
+    """CouplingStep (one CUDA-graph replay per step: H2D, pack, load, gather, PCG, D2H)
+    returns transfer_mc's solution bitwise, step after step with changing coefficients,
+    and raises the reference's errors."""
+    tgt = tt.generate_cube_mesh(8, 0.2, seed=20)
+    src = tt.generate_cube_mesh(9, 0.2, seed=10, split="kuhn_mirror")
+    loc = tt.UniformGridLocator.build(src)
+    plan = tt.SamplePlan.build(32, "sobol", 0, dim=3)
+    step = tt.CouplingStep(tgt, src, plan, cg_tol=1e-13, source_locator=loc)
+    rng = np.random.default_rng(0)
+    for k in range(3):
+        c = np.sin(src.nodes[:, 0] + k) + 2.0 + 0.1 * rng.random(src.n_nodes)
+        got = step(c).coeffs.copy()
+        ref = tt.transfer_mc(tgt, tt.MeshBackedField(tt.NodalField(src, c), loc), plan, cg_tol=1e-13).coeffs
+        assert np.array_equal(got, ref), k
+    bad = np.ones(src.n_nodes)
+    bad[3] = np.inf
+    with pytest.raises(tt.SourceEvalFailed):
+        step(bad)
+    assert np.array_equal(step(c).coeffs, ref)     # the step object is reusable after an error
