@@ -471,7 +471,18 @@ def run_ours(args):
                                                        else ncu.get("fp64_flops_per_sample")),
                                   "peak_source": "measured in this run (tt_fp64_peak_probe, DFMA)"},
                          "l1_data_pipe_pct_ncu": ncu.get("l1_data_pipe_pct") if same else None,
-                         "l1_wavefronts_per_sample_ncu": ncu.get("l1_wavefronts_per_sample") if same else None,
+                         # the roofline that binds the fused kernel: the L1/TEX LSU data pipe
+                         # (one wavefront per cycle per SM); wavefronts per sample from the
+                         # committed ncu capture, rate from this run's kernel time
+                         "binding": ({"resource": "L1/TEX LSU data pipe (global + shared wavefronts)",
+                                      "unit": "wavefronts/s",
+                                      "wavefronts_per_sample": ncu["l1_wavefronts_per_sample"],
+                                      "achieved": ncu["l1_wavefronts_per_sample"] * E_loc * args.samples / (k_ms * 1e-3),
+                                      "peak": 148 * 1.965e9,
+                                      "frac": ncu["l1_wavefronts_per_sample"] * E_loc * args.samples / (k_ms * 1e-3)
+                                              / (148 * 1.965e9),
+                                      "source": ncu_src}
+                                     if same and ncu.get("l1_wavefronts_per_sample") else None),
                          "note": ("streaming CSR SpMV over the folded load matrix R (12 B per nonzero); "
                                   "the PCG that follows dominates the step") if c5 else
                                  "fused gather kernel: < 1 compulsory HBM byte per sample; bound by the "

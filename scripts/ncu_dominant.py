@@ -32,8 +32,11 @@ out = {
     "fp64_flops_per_sample": (2 * ops["dfma"] + ops["dmul"] + ops["dadd"]) / samples,
     "fp32_flops_per_sample": (2 * ops["ffma"] + ops["fmul"] + ops["fadd"]) / samples,
     "l1_data_pipe_pct": get("l1tex__data_pipe_lsu_wavefronts.sum.pct_of_peak_sustained_elapsed"),
-    "l1_wavefronts_per_sample": (get("l1tex__data_pipe_lsu_wavefronts.sum") / samples
-                                 if "l1tex__data_pipe_lsu_wavefronts.sum" in names else None),
+    # LSU data-pipe wavefronts (global + shared), summed over the 148 SMs
+    "l1_wavefronts_per_sample": (get("SM_A.TriageCompute.l1tex__data_pipe_lsu_wavefronts.avg") * 148 / samples
+                                 if "SM_A.TriageCompute.l1tex__data_pipe_lsu_wavefronts.avg" in names else None),
+    "l1_shared_wavefronts_per_sample": (get("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum") / samples
+                                        if "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum" in names else None),
     "fp64_pipe_active_pct": get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
     "ipc": get("sm__inst_executed.avg.per_cycle_active"),
 }
