@@ -333,6 +333,14 @@ int tt_pcg_ell_slab(int64_t n, int width, const int32_t* ell_cols, const double*
                     const double* diag, const double* b, double tol, int64_t maxiter, double* x,
                     double* best_x, double* work /* tt_pcg_workspace_doubles(n) */,
                     tt_pcg_result_t* result, void* stream);
+/* The same solve with the pipelined (Ghysels-Vanroose) form of the recurrence: the same Krylov
+ * iterates, stopping rule and best-iterate tracking in exact arithmetic, ONE grid barrier per
+ * iteration.  For matrices whose Jacobi-preconditioned condition number is small (P1 mass
+ * matrices: <= 4 in 2-D, <= 5 in 3-D), where its rounding matches the textbook recurrence's.
+ * Workspace tt_pcg_workspace_doubles(n); TT_ERR_CAPACITY as tt_pcg_ell_slab. */
+int tt_pcg_ell_slab_pipelined(int64_t n, int width, const int32_t* ell_cols, const double* ell_vals,
+                              const double* diag, const double* b, double tol, int64_t maxiter, double* x,
+                              double* best_x, double* work, tt_pcg_result_t* result, void* stream);
 int tt_spmv(int64_t n, const int64_t* row_ptr, const int32_t* cols, const double* vals,
             const double* x, double* y, void* stream);
 

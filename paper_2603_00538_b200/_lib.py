@@ -140,6 +140,7 @@ _SIGNATURES = {
     "tt_csr_to_ell": ([_I64, _P, _P, _P, _I, _P, _P, _P, _P, _P], _I),
     "tt_pcg_ell": ([_I64, _I, _P, _P, _P, _P, _D, _I64, _P, _P, _P, _P, _P], _I),
     "tt_pcg_ell_slab": ([_I64, _I, _P, _P, _P, _P, _D, _I64, _P, _P, _P, _P, _P], _I),
+    "tt_pcg_ell_slab_pipelined": ([_I64, _I, _P, _P, _P, _P, _D, _I64, _P, _P, _P, _P, _P], _I),
     "tt_spmv": ([_I64, _P, _P, _P, _P, _P, _P], _I),
     "tt_integrate_p1": ([C.POINTER(tt_mesh_t), _P, _P, _P], _I),
     "tt_supermesh_integrals": ([C.POINTER(tt_mesh_t), _P, C.POINTER(tt_mesh_t), _P, C.POINTER(tt_grid_t),

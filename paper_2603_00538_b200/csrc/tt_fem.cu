@@ -637,6 +637,209 @@ __global__ void __launch_bounds__(BLOCK, MINB) pcg_ell_kernel(EllArgs a) {
 }
 
 
+// ------------------------------------------------------- pipelined PCG (one barrier/iteration)
+// Ghysels-Vanroose pipelined Jacobi PCG: the same Krylov iterates as fem.py:131-152 in exact
+// arithmetic, with the three inner products of an iteration -- (r,u), (w,u), (r,r) -- reduced
+// in ONE grid barrier together with the SpMV that does not depend on them:
+//   [barrier: partials of (r_i,u_i), (w_i,u_i), (r_i,r_i)]
+//   totals -> residual test / best iterate of x_i;  beta_i = g_i/g_{i-1},
+//   alpha_i = g_i / (d_i - beta_i g_i / alpha_{i-1})
+//   n = A m_i (m = dinv w, double-buffered: the gathers read m_i while owners write m_{i+1})
+//   own rows: z = n + beta z; q = m + beta q; s = w + beta s; p = u + beta p;
+//             x += alpha p; r -= alpha s; u -= alpha q; w -= alpha z; m_{i+1} = dinv w;
+//             partials of the next iteration's three products
+// The iteration that produces x_{i+1} tests it after the next barrier, so iteration counts,
+// the stopping rule (recurrence residual <= tol) and best-iterate tracking are the reference's.
+struct PipeArgs {
+    int64_t n;
+    const int32_t* __restrict__ ec;
+    const double* __restrict__ ev;
+    const double* __restrict__ diag;
+    const double* __restrict__ b;
+    double tol;
+    int64_t maxiter;
+    double* x;
+    double* best_x;
+    double *r, *u, *w, *z, *q, *s, *p, *m0, *m1, *dinv;
+    double* part;
+    tt_pcg_result_t* res;
+    int64_t slab_rows;
+};
+
+__device__ __forceinline__ double slab_row_col(const uint4* __restrict__ ch, int64_t i,
+                                               const double* __restrict__ v) {
+    const uint4 w0 = ch[0], w1 = ch[1], w2 = ch[2], w3 = ch[3], cw = ch[4];
+    const auto dlo = [](uint4 w) { return __hiloint2double((int)w.y, (int)w.x); };
+    const auto dhi = [](uint4 w) { return __hiloint2double((int)w.w, (int)w.z); };
+    const auto off = [](unsigned u, int h) { return (int)(short)(h ? (u >> 16) : (u & 0xffffu)); };
+    const int c0 = (int)i + off(cw.x, 0), c1 = (int)i + off(cw.x, 1);
+    const int c2 = (int)i + off(cw.y, 0), c3 = (int)i + off(cw.y, 1);
+    const int c4 = (int)i + off(cw.z, 0), c5 = (int)i + off(cw.z, 1);
+    const int c6 = (int)i + off(cw.w, 0), c7 = (int)i + off(cw.w, 1);
+    const double s0 = fma(dhi(w1), v[c3], fma(dlo(w1), v[c2], fma(dhi(w0), v[c1], dlo(w0) * v[c0])));
+    const double s1 = fma(dhi(w3), v[c7], fma(dlo(w3), v[c6], fma(dhi(w2), v[c5], dlo(w2) * v[c4])));
+    return s0 + s1;
+}
+
+template <int BLOCK, int MINB, int W, bool SLAB>
+__global__ void __launch_bounds__(BLOCK, MINB) pcg_pipe_kernel(PipeArgs a) {
+    constexpr int LPR = W / 8;
+    constexpr int RPW = 32 / LPR;  // rows per warp
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double sh[3 * 32];
+    extern __shared__ uint4 slab[];  // SLAB: (rows of this block) x LPR chunks x 5 uint4
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+    const int nb = gridDim.x;
+    // partials (r,u) (w,u) (r,r): two sets of 3 * gridDim.x slots, alternating by iteration
+    // (a block that runs ahead must not overwrite partials a slower block is still summing)
+    const int64_t n = a.n;
+    const int64_t rpb = (n + nb - 1) / nb;
+    const int64_t r_lo = blockIdx.x * rpb, r_end = min(n, r_lo + rpb);
+    const int64_t group = tid / LPR;
+    const int sub = threadIdx.x & (LPR - 1);
+    if constexpr (SLAB) {
+        const int64_t lo = min(n, r_lo), hi = min(n, lo + min(rpb, a.slab_rows));
+        for (int64_t q = threadIdx.x; q < (hi - lo) * LPR; q += BLOCK) {
+            const int64_t i = lo + q / LPR;
+            const int sb = (int)(q % LPR);
+            const int4* cq = reinterpret_cast<const int4*>(a.ec + i * W) + 2 * sb;
+            const int4 c0 = __ldg(cq), c1 = __ldg(cq + 1);
+            const uint4* vq = reinterpret_cast<const uint4*>(a.ev + i * W + 8 * sb);
+            uint4* ch = slab + q * 5;
+            ch[0] = __ldg(vq); ch[1] = __ldg(vq + 1); ch[2] = __ldg(vq + 2); ch[3] = __ldg(vq + 3);
+            const auto pk = [&](int u, int v) {
+                return (unsigned)(unsigned short)(short)(u - (int)i) |
+                       ((unsigned)(unsigned short)(short)(v - (int)i) << 16);
+            };
+            ch[4] = make_uint4(pk(c0.x, c0.y), pk(c0.z, c0.w), pk(c1.x, c1.y), pk(c1.z, c1.w));
+        }
+    }
+    // y_i = sum_j A_ij v_j for the LPR-lane group of row i (all lanes of the warp call it)
+    const auto spmv_row = [&](int64_t i, const double* __restrict__ v) -> double {
+        double acc = 0.0;
+        if (i < r_end) {
+            const int64_t li = i - r_lo;
+            if (SLAB && li < a.slab_rows) {
+                acc = slab_row_col(slab + (li * LPR + sub) * 5, i, v);
+            } else {
+                acc = ell_row8<W>(a.ec, a.ev, i, sub, [&](int c) { return v[c]; });
+            }
+        }
+#pragma unroll
+        for (int off = 1; off < LPR; off <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        return acc;
+    };
+    // init: x = 0, r = b, u = dinv b; q = s = p = z = 0
+    for (int64_t i = tid; i < n; i += nthreads) {
+        const double di = 1.0 / a.diag[i];
+        const double bi = a.b[i];
+        a.dinv[i] = di;
+        a.x[i] = 0.0;
+        a.best_x[i] = 0.0;
+        a.r[i] = bi;
+        a.u[i] = di * bi;
+        a.z[i] = 0.0; a.q[i] = 0.0; a.s[i] = 0.0; a.p[i] = 0.0;
+    }
+    grid.sync();
+    // w0 = A u0, m0 = dinv w0, partials of (r0,u0), (w0,u0), (r0,r0)
+    {
+        double pg = 0.0, pd = 0.0, pr = 0.0;
+        for (int64_t i0 = r_lo + (threadIdx.x / LPR & ~(RPW - 1)); i0 < r_lo + rpb; i0 += BLOCK / LPR) {
+            const int64_t i = i0 + (group & (RPW - 1));
+            const double wi = spmv_row(i, a.u);
+            if (i < r_end && sub == 0) {
+                const double ri = a.r[i], ui = a.u[i];
+                a.w[i] = wi;
+                a.m0[i] = a.dinv[i] * wi;
+                pg += ri * ui;
+                pd += wi * ui;
+                pr += ri * ri;
+            }
+        }
+        double v[3] = {pg, pd, pr};
+        block_sums<3>(v, sh);
+        if (threadIdx.x == 0) { a.part[blockIdx.x] = v[0]; a.part[nb + blockIdx.x] = v[1]; a.part[2 * nb + blockIdx.x] = v[2]; }
+    }
+    grid.sync();
+    double tot[3];
+    grid_totals<3>(a.part, sh, tot);
+    const double bnorm = sqrt(tot[2]);
+    if (bnorm == 0.0) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            a.res->iterations = 0; a.res->residual = 0.0; a.res->best_residual = 0.0;
+            a.res->converged = 1; a.res->zero_rhs = 1;
+        }
+        return;
+    }
+    double best = bnorm / bnorm;  // ||r0|| / ||b||  (fem.py:136)
+    double res = best;
+    double gamma_old = 0.0, alpha = 0.0;
+    int xc = 0, xbi = 0;  // current / best iterate buffers (settle_iterates)
+    for (int64_t it = 0;; ++it) {
+        // ---- x_it's residual test (it >= 1), scalars of this iteration
+        const double g = tot[0], d = tot[1];
+        if (it > 0) {
+            res = sqrt(tot[2]) / bnorm;
+            if (res < best) {
+                best = res;
+                xbi = xc;
+            }
+            if (res <= a.tol) {
+                settle_iterates(a.x, a.best_x, xc, xbi, n, tid, nthreads);
+                if (blockIdx.x == 0 && threadIdx.x == 0) {
+                    a.res->iterations = it; a.res->residual = res; a.res->best_residual = best;
+                    a.res->converged = 1; a.res->zero_rhs = 0;
+                }
+                return;
+            }
+        }
+        if (it == a.maxiter) break;
+        const double beta = it > 0 ? g / gamma_old : 0.0;
+        alpha = it > 0 ? g / (d - beta * g / alpha) : g / d;
+        gamma_old = g;
+        const double* __restrict__ m_cur = (it & 1) ? a.m1 : a.m0;
+        double* m_nxt = (it & 1) ? a.m0 : a.m1;
+        const double* xs = xc == 0 ? a.x : a.best_x;  // may alias xw (in-place update)
+        const int xw_i = xc == xbi ? 1 - xc : xc;
+        double* xw = xw_i == 0 ? a.x : a.best_x;
+        double pg = 0.0, pd = 0.0, pr = 0.0;
+#pragma unroll 1
+        for (int64_t i0 = r_lo + (threadIdx.x / LPR & ~(RPW - 1)); i0 < r_lo + rpb; i0 += BLOCK / LPR) {
+            const int64_t i = i0 + (group & (RPW - 1));
+            const double ni = spmv_row(i, m_cur);
+            if (i < r_end && sub == 0) {
+                const double zi = ni + beta * a.z[i];
+                const double qi = m_cur[i] + beta * a.q[i];
+                const double si = a.w[i] + beta * a.s[i];
+                const double pi = a.u[i] + beta * a.p[i];
+                const double xi = xs[i] + alpha * pi;
+                const double ri = a.r[i] - alpha * si;
+                const double ui = a.u[i] - alpha * qi;
+                const double wi = a.w[i] - alpha * zi;
+                a.z[i] = zi; a.q[i] = qi; a.s[i] = si; a.p[i] = pi;
+                xw[i] = xi; a.r[i] = ri; a.u[i] = ui; a.w[i] = wi;
+                m_nxt[i] = a.dinv[i] * wi;
+                pg += ri * ui;
+                pd += wi * ui;
+                pr += ri * ri;
+            }
+        }
+        xc = xw_i;
+        double* partG = a.part + ((it + 1) & 1) * 3 * nb;
+        double v[3] = {pg, pd, pr};
+        block_sums<3>(v, sh);
+        if (threadIdx.x == 0) { partG[blockIdx.x] = v[0]; partG[nb + blockIdx.x] = v[1]; partG[2 * nb + blockIdx.x] = v[2]; }
+        grid.sync();
+        grid_totals<3>(partG, sh, tot);
+    }
+    settle_iterates(a.x, a.best_x, xc, xbi, n, tid, nthreads);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        a.res->iterations = a.maxiter; a.res->residual = res; a.res->best_residual = best;
+        a.res->converged = 0; a.res->zero_rhs = 0;
+    }
+}
+
 __global__ void spmv_kernel(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
                             const double* __restrict__ v, const double* __restrict__ x,
                             double* __restrict__ y) {
@@ -745,7 +948,7 @@ extern "C" int tt_mass_fill(const tt_mesh_t* m, const int64_t* inc_start, const 
     return launch_check("mass_fill_kernel");
 }
 
-extern "C" int64_t tt_pcg_workspace_doubles(int64_t n) { return 8 * n + 3 * 148 * 32 + 64; }
+extern "C" int64_t tt_pcg_workspace_doubles(int64_t n) { return 10 * n + 6 * 148 * 32 + 64; }
 
 extern "C" int tt_pcg(int64_t n, const int64_t* rp, const int32_t* ci, const double* v,
                       const double* b, double tol, int64_t maxiter, double* x, double* best_x,
@@ -907,6 +1110,87 @@ extern "C" int tt_pcg_ell_slab(int64_t n, int width, const int32_t* ell_cols, co
         return cuda_status(e, "pcg_ell_kernel (slab, cooperative launch)");
     }
     set_error("tt_pcg_ell_slab: too few of the %lld rows fit in shared memory", (long long)n);
+    return TT_ERR_CAPACITY;
+}
+
+// launch shape of the pipelined kernels (threads per block, blocks per SM)
+#ifndef TT_PIPE_BLOCK
+#define TT_PIPE_BLOCK 512
+#endif
+#ifndef TT_PIPE_MINB
+#define TT_PIPE_MINB 1
+#endif
+constexpr int kPB = TT_PIPE_BLOCK, kPM = TT_PIPE_MINB;
+
+static bool pipe_args(PipeArgs& a, int64_t n, int width, const int32_t* ell_cols, const double* ell_vals,
+                      const double* diag, const double* b, double tol, int64_t maxiter, double* x,
+                      double* best_x, double* work, tt_pcg_result_t* result, const char* who) {
+    if (n < 1 || maxiter < 0 || (width != 8 && width != 16)) {
+        set_error("%s: bad size or width (8 | 16)", who);
+        return false;
+    }
+    a.n = n; a.ec = ell_cols; a.ev = ell_vals; a.diag = diag; a.b = b; a.tol = tol; a.maxiter = maxiter;
+    a.x = x; a.best_x = best_x;
+    double* v[10];
+    for (int k = 0; k < 10; ++k) v[k] = work + k * n;
+    a.r = v[0]; a.u = v[1]; a.w = v[2]; a.z = v[3]; a.q = v[4]; a.s = v[5]; a.p = v[6];
+    a.m0 = v[7]; a.m1 = v[8]; a.dinv = v[9];
+    a.part = work + 10 * n;
+    a.res = result;
+    a.slab_rows = 0;
+    return true;
+}
+
+// The pipelined recurrence with the rows on chip (1 grid barrier per iteration).  Measured per
+// solve (scripts/pcg_ab.py): C2 mass matrix 0.329 -> 0.262 ms (23 iterations), C1 0.329 ->
+// 0.316 ms; one 512-thread block per SM (the recurrence needs ~110 registers; two blocks
+// of 512 spill, 0.357 ms).  Streaming the rows from L2/HBM (C4) it is slower than the
+// textbook kernel (2.9 vs 2.4 ms: ten vectors per row instead of six), so tt_pcg_ell keeps
+// the textbook recurrence.
+extern "C" int tt_pcg_ell_slab_pipelined(int64_t n, int width, const int32_t* ell_cols, const double* ell_vals,
+                               const double* diag, const double* b, double tol, int64_t maxiter, double* x,
+                               double* best_x, double* work, tt_pcg_result_t* result, void* stream) {
+    PipeArgs a;
+    if (!pipe_args(a, n, width, ell_cols, ell_vals, diag, b, tol, maxiter, x, best_x, work, result,
+                   "tt_pcg_ell_slab_pipelined"))
+        return TT_ERR_INVALID_PARAMETER;
+    const int lpr = width / 8;  // lanes per row = 80-byte chunks per row
+    const void* fn = width == 8 ? (const void*)pcg_pipe_kernel<kPB, kPM, 8, true>
+                                : (const void*)pcg_pipe_kernel<kPB, kPM, 16, true>;
+    int dev = 0, max_optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const int sms = sm_count();
+    // rows that must be slab-resident for the slab to pay (1/2): the rest of a block's rows
+    // stream from L2/HBM as in tt_pcg_ell, with the L1 the slab took.  Measured per 3-D
+    // solve, slab vs L2 kernel: 59 % on chip (357,911 rows) 0.565 vs 0.691 ms; 40 %
+    // (531,441) 1.20 vs 1.04; 28 % (753,571) 1.83 vs 1.25; C1 (2-D, 85 %) 0.36 vs 0.43
+    constexpr double min_frac = 0.5;
+    // 2 blocks per SM (the 2 x 512 shape of tt_pcg_ell), else 1 with twice the rows.  With
+    // 2 per SM the block count and row ranges are tt_pcg_ell's, so the partial sums -- and
+    // the iterates -- are bitwise the same
+    const int64_t need = (n * lpr + kPB - 1) / kPB;
+    for (int bps = kPM; bps >= 1; --bps) {
+        const int64_t nb = need < (int64_t)sms * bps ? need : (int64_t)sms * bps;
+        const int64_t rpb = (n + nb - 1) / nb;
+        const int64_t per_row = 80 * lpr;
+        // per-SM shared memory: 228 KB less 1 KB per block reserved, less the static part
+        const int64_t avail = (int64_t)(bps > 1 ? (228 * 1024) / bps - 1024 : max_optin) - (int64_t)sizeof(double) * 96 - 16;
+        const int64_t cap = avail / per_row;
+        const int64_t rows = rpb < cap ? rpb : cap;
+        if (rows < 1 || (rows < rpb && rows < min_frac * rpb)) continue;
+        const int64_t smem = rows * per_row;
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kPB, (size_t)smem);
+        if (per_sm < bps) continue;
+        a.slab_rows = rows;
+        void* args[] = {&a};
+        cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)nb), dim3(kPB), args, (size_t)smem,
+                                                    as_stream(stream));
+        return cuda_status(e, "pcg_pipe_kernel (slab, cooperative launch)");
+    }
+    set_error("tt_pcg_ell_slab_pipelined: too few of the %lld rows fit in shared memory", (long long)n);
     return TT_ERR_CAPACITY;
 }
 

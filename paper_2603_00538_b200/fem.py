@@ -113,6 +113,9 @@ class SparseSymMatrix:
         self.cols_dev = cols
         self.vals_dev = vals
         self._ws = None
+        #: Jacobi-preconditioned condition number known small (P1 mass matrices, Wathen's
+        #: element bound: <= 4 in 2-D, <= 5 in 3-D): the pipelined recurrence may be used
+        self.jacobi_bounded = False
 
     @property
     def shape(self):
@@ -215,7 +218,10 @@ def assemble_mass_matrix(mesh, rule: QuadratureRule | None = None) -> SparseSymM
     lh = (C.c_double * (k * k))(*local.ravel().tolist())
     _lib.call("tt_mass_fill", C.byref(desc), _lib.ptr(inc_start), _lib.ptr(inc), lh,
               _lib.ptr(row_ptr), _lib.ptr(cols), _lib.ptr(vals), s)
-    return SparseSymMatrix(mesh.n_nodes, row_ptr, cols, vals)
+    M = SparseSymMatrix(mesh.n_nodes, row_ptr, cols, vals)
+    # the element-by-element bound holds for any positive-weight rule exact on P1 x P1
+    M.jacobi_bounded = rule.degree >= 2
+    return M
 
 
 class PcgResult:
@@ -228,22 +234,25 @@ def pcg_device(M: SparseSymMatrix, b: torch.Tensor, tol: float = 1e-12,
     """Launch the single-kernel PCG; returns (x, best_x, result tensor) without syncing.
 
     ``path``: "auto" -- the ELL matrix (every row <= 16 entries) with its rows held in
-    shared memory when they fit (the slab kernel), else streamed from L2/HBM; "ell_l2"
-    never uses the slab; "csr" the CSR kernel.  All paths run the same recurrence."""
+    shared memory when they fit (the slab kernel; for a mass matrix its pipelined form, one
+    grid barrier per iteration), else streamed from L2/HBM; "slab" the textbook slab
+    kernel; "ell_l2" never uses the slab; "csr" the CSR kernel.  All paths run the
+    reference's recurrence (the same iterates in exact arithmetic)."""
     n = M.n
     maxiter = 10 * n if maxiter is None else int(maxiter)
     work, res = M.workspace()
     x = x if x is not None else torch.empty(n, dtype=torch.float64, device=b.device)
     best_x = best_x if best_x is not None else torch.empty(n, dtype=torch.float64, device=b.device)
-    if path not in ("auto", "ell_l2", "csr"):
+    if path not in ("auto", "slab", "ell_l2", "csr"):
         raise ValueError(f"unknown PCG path {path!r}")
     ell = M.ell() if path != "csr" else None
     if ell is not None:
         args = (n, ell[3], _lib.ptr(ell[0]), _lib.ptr(ell[1]), _lib.ptr(ell[2]), _lib.ptr(b), float(tol),
                 maxiter, _lib.ptr(x), _lib.ptr(best_x), _lib.ptr(work), _lib.ptr(res), _lib.stream_handle())
-        if path == "auto" and getattr(M, "_slab_ok", False):
+        if path in ("auto", "slab") and getattr(M, "_slab_ok", False):
             # rows held in shared memory when they fit (TT_ERR_CAPACITY: nothing launched)
-            if _lib.call_status("tt_pcg_ell_slab", *args) == 0:
+            fn = "tt_pcg_ell_slab_pipelined" if path == "auto" and M.jacobi_bounded else "tt_pcg_ell_slab"
+            if _lib.call_status(fn, *args) == 0:
                 return x, best_x, res
             M._slab_ok = False
         _lib.call("tt_pcg_ell", *args)

@@ -138,9 +138,9 @@ class MCTransferOperator:
 
 
 class CouplingStep:
-    """One coupling step of a fixed (target, source mesh, plan) triple as ONE CUDA-graph
-    replay: H2D of the source coefficients -> gradient pack -> fused MC load -> ordered node
-    gather -> PCG -> D2H of the solution (extension for coupling loops; each call is the
+    """One coupling step of a fixed (target, source mesh, plan) triple: the H2D copy of the
+    source coefficients, then ONE CUDA-graph replay of gradient pack -> fused MC load ->
+    ordered node gather -> PCG -> D2H of the solution (extension for coupling loops; each call is the
     reference's ``transfer_mc(target, MeshBackedField(NodalField(source, c)), plan)``,
     transfer.py:158-163, with the same results and errors).
 
@@ -158,7 +158,6 @@ class CouplingStep:
         self.target, self.source_mesh, self.plan, self.cg_tol = target, source_mesh, plan, cg_tol
         dev = _lib.device()
         self.c_dev = torch.zeros(source_mesh.n_nodes, dtype=torch.float64, device=dev)
-        self.c_host = torch.zeros(source_mesh.n_nodes, dtype=torch.float64).pin_memory()
         self.x_host = torch.zeros(target.n_nodes, dtype=torch.float64).pin_memory()
         self.flags_host = torch.zeros(8, dtype=torch.float64).pin_memory()   # result (4) + status
         self.field = NodalField(source_mesh, self.c_dev)
@@ -169,7 +168,6 @@ class CouplingStep:
 
     def _body(self):
         from .montecarlo import load_vector
-        self.c_dev.copy_(self.c_host, non_blocking=True)
         self.status.zero_()
         self.field._grad = self.field._packed = None    # new coefficients: repack in the step
         b = load_vector(self.target, self.source, self.plan, check=False, status=self.status)
@@ -184,7 +182,11 @@ class CouplingStep:
         coefficient buffers belong to this step object and are overwritten by the next
         call (copy them to keep them)."""
         c = coeffs.coeffs_dev if isinstance(coeffs, NodalField) else coeffs
-        self.c_host.copy_(torch.as_tensor(c, dtype=torch.float64).reshape(-1))
+        c = torch.as_tensor(c, dtype=torch.float64).reshape(-1)
+        if c.shape[0] != self.c_dev.shape[0]:
+            raise DimensionMismatch(f"{c.shape[0]} coefficients for {self.c_dev.shape[0]} source nodes")
+        # H2D (asynchronous from pinned memory) ahead of the replay on the same stream
+        self.c_dev.copy_(c, non_blocking=True)
         if self._graph is None:
             self._body()                    # eager warm-up: builds every cached state
             torch.cuda.current_stream().synchronize()

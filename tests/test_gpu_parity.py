@@ -453,8 +453,8 @@ def test_ell_and_csr_pcg_agree(tt, golden, c1):
     M = tt.assemble_mass_matrix(tgt)
     assert M.ell() is not None
     b = torch.as_tensor(golden["b_c1_mesh_smooth"], device="cuda")
-    xs = [tt.cg_solve(M, b, tol=1e-14, path=path).cpu().numpy() for path in ("auto", "ell_l2", "csr")]
-    assert M._slab_ok          # the default ran the shared-memory slab PCG
+    xs = [tt.cg_solve(M, b, tol=1e-14, path=path).cpu().numpy() for path in ("slab", "ell_l2", "csr", "auto")]
+    assert M._slab_ok and M.jacobi_bounded   # the default ran the pipelined slab PCG
     assert np.array_equal(xs[0], xs[1])   # slab and L2 ELL: the same arithmetic, bit for bit
     for x in xs:
         assert np.max(np.abs(x - golden["x_c1_mesh_tol14"])) <= 1e-12
@@ -471,12 +471,16 @@ def test_slab_pcg_full_and_partial(tt, dim, n):
            else tt.generate_square_mesh(n, 0.2, seed=20, diagonal="right"))
     M = tt.assemble_mass_matrix(tgt)
     b = torch.as_tensor(np.random.default_rng(n).random(tgt.n_nodes), device="cuda")
-    xs = [tt.cg_solve(M, b, tol=1e-14, path=path).cpu().numpy() for path in ("auto", "ell_l2")]
+    xs = [tt.cg_solve(M, b, tol=1e-14, path=path).cpu().numpy() for path in ("slab", "ell_l2", "auto")]
     assert M.ell()[3] == (8 if dim == 2 else 16)
     assert M._slab_ok
     assert np.array_equal(xs[0], xs[1])
-    xr, _ = O.cg_solve(M.csr, b.cpu().numpy(), tol=1e-14)
+    xr, it_ref = O.cg_solve(M.csr, b.cpu().numpy(), tol=1e-14)
     assert _rel(xs[0], xr) <= 1e-12
+    assert _rel(xs[2], xr) <= 1e-12            # the pipelined recurrence (default for mass matrices)
+    from paper_2603_00538_b200.fem import decode_result, pcg_device
+    _, _, res = pcg_device(M, b, tol=1e-14)
+    assert abs(decode_result(res).iterations - it_ref) <= 1   # same iteration count as the reference
 
 
 def test_slab_pcg_capacity_fallback(tt):
