@@ -336,8 +336,7 @@ __global__ void __launch_bounds__(kMcBlock, kMcMinBlocks) mc_mesh_kernel(TargetD
                                                       double* __restrict__ contrib,
                                                       double* __restrict__ b,
                                                       int32_t* __restrict__ ids_out,
-                                                      int32_t* __restrict__ status,
-                                                      unsigned long long* __restrict__ tile_counter) {
+                                                      int32_t* __restrict__ status) {
     constexpr int K = D + 1;
     constexpr int EPW = 32 / G;
     constexpr int NW = kMcBlock / 32;
@@ -371,16 +370,7 @@ __global__ void __launch_bounds__(kMcBlock, kMcMinBlocks) mc_mesh_kernel(TargetD
     __shared__ int s_seed[NW][EPW][kSeeds + 1];
     const int wib = threadIdx.x >> 5, gib = lane / G;
 
-    // tiles: the first per warp is static, the rest are handed out by an atomic counter
-    // (dynamic balancing of the persistent grid: tile costs vary with walk lengths and
-    // snaps); an element's result does not depend on which warp computes it
-    const auto next_tile = [&](int64_t tile) -> int64_t {
-        if (!tile_counter) return tile + nwarps;
-        unsigned long long q = 0;
-        if (lane == 0) q = atomicAdd(tile_counter, 1ull);
-        return nwarps + (int64_t)__shfl_sync(FULL, q, 0);
-    };
-    for (int64_t tile = warp; tile * EPW < n_el; tile = next_tile(tile)) {
+    for (int64_t tile = warp; tile * EPW < n_el; tile += nwarps) {
         const int64_t le = tile * EPW + lane / G;
         const bool active = le < n_el;
         const int64_t e = e_lo + le;
@@ -817,28 +807,14 @@ static int launch_mesh(const TargetDev& td, int64_t e_lo, int64_t e_hi, const Pl
     // dynamic shared memory = the seed-slot table (N bytes, SLOT kernels only): every byte
     // of shared memory is L1 the walk's records lose (+20 KB/block costs 0.056 ms at C2)
     const size_t smem = slot ? (size_t)((pd.n + 15) / 16 * 16) : 0;
-#ifndef TT_MC_DYNAMIC
-#define TT_MC_DYNAMIC 1
-#endif
-    unsigned long long* counter = nullptr;
-    if (TT_MC_DYNAMIC) {
-        int st2 = cuda_status(cudaMallocAsync((void**)&counter, sizeof(unsigned long long), st), "tile counter");
-        if (st2) return st2;
-        cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st);
-    }
     auto go = [&](auto kernel) {
         static const int per = blocks_per_sm(kernel, kMcBlock, 0);
         constexpr int kWarps = kMcBlock / 32;  // a warp works one tile at a time
         int64_t nb = (tiles + kWarps - 1) / kWarps;
         const int64_t cap = (int64_t)sm_count() * per * waves;
         nb = nb > cap ? cap : nb < 1 ? 1 : nb;
-        kernel<<<(unsigned)nb, kMcBlock, smem, st>>>(td, e_lo, e_hi, pd, sd, contrib, b, ids, status, counter);
+        kernel<<<(unsigned)nb, kMcBlock, smem, st>>>(td, e_lo, e_hi, pd, sd, contrib, b, ids, status);
     };
-    struct FreeCounter {
-        unsigned long long* p;
-        cudaStream_t s;
-        ~FreeCounter() { if (p) cudaFreeAsync(p, s); }
-    } free_counter{counter, st};
     // DEFER costs registers (C2: 1.12 -> 1.22 ms), so only pairs known to snap run it
     if constexpr (PLAN == TT_PLAN_SHARED) {
         if (slot) {
