@@ -206,10 +206,12 @@ class _Comm:
 
     def __init__(self, group=None):
         self.group = group
-        ok = dist.is_available() and dist.is_initialized()
-        self.world = dist.get_world_size(group) if ok else 1
-        self.rank = dist.get_rank(group) if ok else 0
-        self.staged = self.world > 1 and dist.get_backend(group) != "nccl"
+        # with a process group every exchange is a real collective, world 1 included (the
+        # same code path as N GPUs); without one the step runs locally
+        self.active = dist.is_available() and dist.is_initialized()
+        self.world = dist.get_world_size(group) if self.active else 1
+        self.rank = dist.get_rank(group) if self.active else 0
+        self.staged = self.active and dist.get_backend(group) != "nccl"
 
     def _run(self, fn, *tensors):
         if not self.staged:
@@ -220,7 +222,7 @@ class _Comm:
             t.copy_(h)
 
     def alltoallv(self, out: torch.Tensor, inp: torch.Tensor, out_splits, in_splits):
-        if self.world == 1:
+        if not self.active:
             if out.numel():
                 out.copy_(inp)
             return
@@ -229,14 +231,14 @@ class _Comm:
                   out, inp)
 
     def allreduce_(self, t: torch.Tensor, op=None):
-        if self.world > 1:
+        if self.active:
             op = dist.ReduceOp.SUM if op is None else op
             self._run(lambda x: dist.all_reduce(x, op=op, group=self.group), t)
         return t
 
     def allgatherv(self, t: torch.Tensor, counts) -> torch.Tensor:
         """Concatenation over ranks of the leading ``counts[q]`` rows each rank holds."""
-        if self.world == 1:
+        if not self.active:
             return t
         m = max(counts)
         pad = torch.zeros((m,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
@@ -252,7 +254,7 @@ class _Comm:
 
     def any_flags(self, status: torch.Tensor) -> torch.Tensor:
         """Bitwise OR of an int32 status word over ranks (as MAX of its bits)."""
-        if self.world == 1:
+        if not self.active:
             return status
         bits = ((status.to(torch.int64) >> torch.arange(16, device=status.device)) & 1).to(torch.int32)
         self.allreduce_(bits, dist.ReduceOp.MAX)
@@ -412,7 +414,7 @@ class DistributedCoupling:
         locator.seeds_for(self.sub)
         flag = torch.tensor([1 if locator._seeds[self.sub][1] else 0], dtype=torch.int32,
                             device=_lib.device())
-        self.comm.allreduce_(flag, dist.ReduceOp.MAX if self.comm.world > 1 else None)
+        self.comm.allreduce_(flag, dist.ReduceOp.MAX if self.comm.active else None)
         seeds, _ = locator._seeds[self.sub]
         locator._seeds[self.sub] = (seeds, bool(int(flag.item())))
 
@@ -426,7 +428,7 @@ class DistributedCoupling:
         n_oe = p.n_own_elems
         if n_oe:
             element_contributions(self.sub, source, plan, out=self.contrib[:n_oe], status=status)
-        if self.world > 1:
+        if self.comm.active:
             k = self.k
             ns = len(p.send_rows)
             _lib.call("tt_gather_rows", ns, k, _lib.ptr(self.send_rows), _lib.ptr(self.contrib),
@@ -561,7 +563,7 @@ class DistributedMCOperator:
         y = self.buf[:self.n_sub]
         _lib.call("tt_spmv_rect", self.n_sub, _lib.ptr(rp), _lib.ptr(ci), _lib.ptr(va),
                   _lib.ptr(field.coeffs_dev), _lib.ptr(y), _lib.stream_handle())
-        if self.c.world > 1:
+        if self.c.comm.active:
             ns = int(sum(self.send_counts))
             _lib.call("tt_gather_rows", ns, 1, _lib.ptr(self.send_idx), _lib.ptr(y),
                       _lib.ptr(self.send_buf), _lib.stream_handle())

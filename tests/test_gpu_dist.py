@@ -119,3 +119,38 @@ def test_partitioned_step_world_2_gloo(tmp_path):
         _assert(r, 2)
     # the failure really was confined to one rank's elements, yet both raised
     assert sorted(r["pokes_out"] for r in res) == [False, True]
+
+
+def _nccl_worker(rank, world, port, out):
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", 0))
+    import paper_2603_00538_b200 as tt
+    from paper_2603_00538_b200.dist import DistributedCoupling
+    ref = torch.load(os.path.join(out, "ref.pt"))
+    tgt, src, fs = _problem(tt)
+    loc = tt.UniformGridLocator.build(src)
+    box = tt.MeshBackedField(fs, loc)
+    dc = DistributedCoupling(tgt, solve="distributed")
+    assert dc.comm.active and not dc.comm.staged
+    plan = tt.SamplePlan.build(32, "sobol", 3, dim=3)
+    res = {"b_bitwise": bool(torch.equal(dc.load(box, plan).cpu(), ref["b_sobol"]))}
+    errs = []
+    for _ in range(3):     # the first solve captures the CUDA graph, the next ones replay it
+        x = dc.step(box, plan, tol=1e-14).cpu()
+        errs.append(float((x - ref["x"]).abs().max() / ref["x"].abs().max()))
+    res["x_errs"] = errs
+    res["graph"] = dc._pcg._graph is not None
+    torch.save(res, os.path.join(out, "nccl.pt"))
+    dist.destroy_process_group()
+
+
+def test_partitioned_step_nccl_graph(tmp_path):
+    """The NCCL code path on this one GPU (world 1: real all-to-all and all-reduce calls,
+    with the distributed PCG's iterations captured in and replayed from a CUDA graph)."""
+    import paper_2603_00538_b200 as tt
+    torch.save(_reference(tt, *_problem(tt)), tmp_path / "ref.pt")
+    mp.spawn(_nccl_worker, args=(1, _free_port(), str(tmp_path)), nprocs=1, join=True)
+    r = torch.load(tmp_path / "nccl.pt")
+    assert r["b_bitwise"] and r["graph"]
+    assert max(r["x_errs"]) <= 1e-12, r
