@@ -348,12 +348,13 @@ int tt_spmv(int64_t n, const int64_t* row_ptr, const int32_t* cols, const double
 /* One rank's part of the distributed Jacobi PCG (fem.py:113-152 in its Chronopoulos-Gear
  * form: one all-reduce of 3 scalars per iteration).  Rows = the rank's own target nodes; the
  * local vector u is (n_ext = own + halo) long, halo entries received from their owners each
- * iteration.  Host loop per iteration:
- *   tt_dpcg_update -> tt_dpcg_pack -> exchange send_buf into u[n_own:] (NCCL) ->
- *   tt_dpcg_spmv -> all-reduce(sum) of sums[0..3) (NCCL) -> tt_dpcg_scalars
- * after one initial tt_dpcg_start -> pack -> exchange -> spmv -> all-reduce -> scalars.  The
- * iteration scalars stay on the device (state); every call is a no-op once it is done. */
-#define TT_DPCG_STATE_BYTES 128
+ * iteration.  Host sequence:
+ *   tt_dpcg_start -> halo exchange of send_buf into u[n_own:] -> tt_dpcg_spmv(parity 0) ->
+ *   all-reduce(sum) of sums[0..3);  then per iteration k (q = k & 1):
+ *   tt_dpcg_update(q) -> halo exchange -> tt_dpcg_spmv(q ^ 1) -> all-reduce of sums;
+ *   tt_dpcg_finish.  The scalars stay on the device (state); every call is a no-op once the
+ *   solve is done, so iterations can be issued in fixed chunks (e.g. one CUDA graph). */
+#define TT_DPCG_STATE_BYTES 256
 typedef struct tt_dpcg {
     int64_t n_own;            /* owned rows */
     int64_t n_ext;            /* local vector length: owned + halo */
@@ -365,9 +366,10 @@ typedef struct tt_dpcg {
     const double*  b;         /* (n_own,) */
     double* x; double* best_x; double* r; double* w; double* p; double* s; double* dinv; /* (n_own,) */
     double* u;                /* (n_ext,) */
-    const int64_t* send_idx;  /* (n_send,) own rows whose u the peers need, grouped by peer */
+    const int64_t* send_start;/* (n_own + 1,) CSR: row i's u goes to send_buf[send_pos[k]], */
+    const int64_t* send_pos;  /*   k in [send_start[i], send_start[i+1]) (one slot per peer) */
     int64_t n_send;
-    double* send_buf;         /* (n_send,) */
+    double* send_buf;         /* (n_send,) grouped by peer */
     double* part;             /* tt_dpcg_part_doubles() scratch */
     double* sums;             /* (3,) local sums (r.u, w.u, r.r): all-reduce them in place */
     double* state;            /* TT_DPCG_STATE_BYTES of device scalar state */
@@ -376,11 +378,9 @@ typedef struct tt_dpcg {
 } tt_dpcg_t;
 int64_t tt_dpcg_part_doubles(void);
 int tt_dpcg_start(const tt_dpcg_t* a, void* stream);
-int tt_dpcg_update(const tt_dpcg_t* a, void* stream);
-int tt_dpcg_pack(const tt_dpcg_t* a, void* stream);
-int tt_dpcg_spmv(const tt_dpcg_t* a, void* stream);
-int tt_dpcg_scalars(const tt_dpcg_t* a, void* stream);
-/* settles best_x / zeroes x for b = 0 and writes the result record (device) */
+int tt_dpcg_update(const tt_dpcg_t* a, int parity, void* stream);
+int tt_dpcg_spmv(const tt_dpcg_t* a, int parity, void* stream);
+/* the result record (device): iterations, residual, best residual, converged, zero_rhs */
 int tt_dpcg_finish(const tt_dpcg_t* a, tt_pcg_result_t* result, void* stream);
 /* dst[t, :] = src[idx[t], :] and dst[idx[t], :] = src[t, :] for rows of k doubles */
 int tt_gather_rows(int64_t n, int k, const int64_t* idx, const double* src, double* dst, void* stream);

@@ -87,7 +87,8 @@ class tt_dpcg_t(C.Structure):
                 ("ell_cols", C.c_void_p), ("ell_vals", C.c_void_p), ("diag", C.c_void_p), ("b", C.c_void_p),
                 ("x", C.c_void_p), ("best_x", C.c_void_p), ("r", C.c_void_p), ("w", C.c_void_p),
                 ("p", C.c_void_p), ("s", C.c_void_p), ("dinv", C.c_void_p), ("u", C.c_void_p),
-                ("send_idx", C.c_void_p), ("n_send", C.c_int64), ("send_buf", C.c_void_p),
+                ("send_start", C.c_void_p), ("send_pos", C.c_void_p), ("n_send", C.c_int64),
+                ("send_buf", C.c_void_p),
                 ("part", C.c_void_p), ("sums", C.c_void_p), ("state", C.c_void_p),
                 ("tol", C.c_double), ("maxiter", C.c_int64)]
 
@@ -147,10 +148,8 @@ _SIGNATURES = {
                                 _D, _P, _P, _P], _I),
     "tt_dpcg_part_doubles": ([], _I64),
     "tt_dpcg_start": ([_P, _P], _I),
-    "tt_dpcg_update": ([_P, _P], _I),
-    "tt_dpcg_pack": ([_P, _P], _I),
-    "tt_dpcg_spmv": ([_P, _P], _I),
-    "tt_dpcg_scalars": ([_P, _P], _I),
+    "tt_dpcg_update": ([_P, _I, _P], _I),
+    "tt_dpcg_spmv": ([_P, _I, _P], _I),
     "tt_dpcg_finish": ([_P, _P, _P], _I),
     "tt_gather_rows": ([_I64, _I, _P, _P, _P, _P], _I),
     "tt_scatter_rows": ([_I64, _I, _P, _P, _P, _P], _I),

@@ -5,18 +5,21 @@
 // rows (the target nodes it owns); its local vector u holds the owned entries followed by
 // halo entries (neighbour nodes owned by peers), received every iteration.  The recurrence
 // is the Chronopoulos-Gear form of the reference's Jacobi PCG (the same Krylov iterates in
-// exact arithmetic) because it needs ONE all-reduce per iteration -- of three scalars:
+// exact arithmetic) because it needs ONE all-reduce per iteration -- of three scalars.  An
+// iteration is two kernels and two collectives:
 //
-//   update:   p = u + beta p;  s = w + beta s;  x += alpha p;  r -= alpha s;  u = dinv r
-//   pack:     send_buf = u[send_idx]                       -> halo exchange (host: NCCL)
-//   spmv:     w = A u;  sums = (r.u, w.u, r.r) over own rows   -> all-reduce(sum) (NCCL)
-//   scalars:  res = sqrt(r.r)/||b||, best iterate, stop test;  beta = g'/g,
-//             alpha = g' / (delta - beta g'/alpha)
+//   update:  scalars from the all-reduced (r.u, w.u, r.r) -- the residual test and best
+//            iterate of x, then alpha, beta -- computed redundantly (bitwise alike) by every
+//            thread; then for the owned rows p = u + beta p, s = w + beta s, x += alpha p,
+//            r -= alpha s, u = dinv r, each new u also written to its send slots
+//                                                -> halo all-to-all of the send buffer (NCCL)
+//   spmv:    w = A u;  (r.u, w.u, r.r) over the owned rows  -> all-reduce(sum) (NCCL)
 //
-// The scalars live in device memory (tt_dpcg_state_t): no host round trip per iteration;
-// the host checks `done` once per chunk of iterations, and every kernel is a no-op once
-// done is set.  Best iterate (fem.py:141-152): the scalars kernel marks an improvement and
-// the next update copies x -> best_x before it moves x (tt_dpcg_finish settles the last).
+// The scalar state lives in device memory, ping-ponged between two slots by the update's
+// parity (its readers and its one writer never touch the same slot), so the host issues
+// iterations without reading anything; it checks `done` once per chunk of iterations (a
+// CUDA-graph replay with NCCL), and every kernel is a no-op once done is set.  Best
+// iterate (fem.py:141-152): an improved residual copies x -> best_x before x moves.
 // Local sums are block partials reduced in a fixed order by the last block, and the
 // all-reduce runs in a fixed order for a fixed world, so solves are run-to-run
 // deterministic.
@@ -27,75 +30,129 @@ namespace tt {
 struct DState {
     double alpha, beta, gamma, bnorm, res, best;
     int64_t it, maxiter;
-    int32_t done, improved, converged, zero_rhs;
+    int32_t done, converged, zero_rhs, primed;
     double tol;
-    uint32_t ticket;  // last-block counter of the spmv partial reduction
-    int32_t primed;   // the first scalars call (r = b) has run
 };
-static_assert(sizeof(DState) <= TT_DPCG_STATE_BYTES, "tt_dpcg state size");
+struct DStates {
+    DState s[2];       // ping-pong: update with parity q reads s[q], writes s[q ^ 1]
+    uint32_t ticket;   // last-block counter of the spmv partial reduction
+};
+static_assert(sizeof(DStates) <= TT_DPCG_STATE_BYTES, "tt_dpcg state size");
 
 constexpr int kDBlock = 256;
 constexpr int kDMaxBlocks = 148 * 8;
 
 __global__ void dpcg_start_kernel(tt_dpcg_t a) {
-    DState* st = reinterpret_cast<DState*>(a.state);
+    DStates* st = reinterpret_cast<DStates*>(a.state);
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t nt = (int64_t)gridDim.x * blockDim.x;
     if (tid == 0) {
-        st->alpha = st->beta = st->gamma = st->bnorm = st->res = st->best = 0.0;
-        st->it = 0; st->maxiter = a.maxiter; st->tol = a.tol;
-        st->done = st->improved = st->converged = st->zero_rhs = 0;
+        for (int q = 0; q < 2; ++q) {
+            DState& s = st->s[q];
+            s.alpha = s.beta = s.gamma = s.bnorm = s.res = s.best = 0.0;
+            s.it = 0; s.maxiter = a.maxiter; s.tol = a.tol;
+            s.done = s.converged = s.zero_rhs = s.primed = 0;
+        }
         st->ticket = 0;
-        st->primed = 0;
     }
     for (int64_t i = tid; i < a.n_own; i += nt) {
         const double di = 1.0 / a.diag[i];
         const double bi = a.b[i];
+        const double ui = di * bi;
         a.dinv[i] = di;
         a.x[i] = 0.0;
         a.best_x[i] = 0.0;
         a.r[i] = bi;
-        a.u[i] = di * bi;
+        a.u[i] = ui;
         a.p[i] = 0.0;
         a.s[i] = 0.0;
+        for (int64_t k = a.send_start[i]; k < a.send_start[i + 1]; ++k) a.send_buf[a.send_pos[k]] = ui;
     }
 }
 
-__global__ void dpcg_update_kernel(tt_dpcg_t a) {
-    const DState* st = reinterpret_cast<const DState*>(a.state);
-    if (st->done) return;
-    const double alpha = st->alpha, beta = st->beta;
-    const bool improved = st->improved != 0;
+// Iteration bookkeeping from the previous state and the all-reduced sums (fem.py:131-152);
+// every thread evaluates it identically.  Returns false when the solve is (now) done.
+__device__ __forceinline__ bool dpcg_scalars(const DState& in, const double* sums, DState& out,
+                                            bool& improved) {
+    out = in;
+    improved = false;
+    if (in.done) return false;
+    const double gam = sums[0], del = sums[1], rr = sums[2];
+    if (!in.primed) {
+        // first update (after start): r = b, u = dinv b, w = A u
+        out.primed = 1;
+        out.bnorm = sqrt(rr);
+        if (out.bnorm == 0.0) {
+            out.done = 1; out.converged = 1; out.zero_rhs = 1;
+            return false;
+        }
+        out.res = out.best = out.bnorm / out.bnorm;  // ||r0|| / ||b||  (fem.py:136)
+        out.gamma = gam;
+        out.alpha = gam / del;
+        out.beta = 0.0;
+        if (out.maxiter == 0) { out.done = 1; return false; }
+        return true;
+    }
+    out.it = in.it + 1;
+    const double res = sqrt(rr) / in.bnorm;
+    out.res = res;
+    if (res < in.best) {
+        out.best = res;
+        improved = true;  // x holds the new best
+    }
+    if (res <= in.tol) { out.done = 1; out.converged = 1; return false; }
+    if (out.it >= in.maxiter) { out.done = 1; return false; }
+    const double beta = gam / in.gamma;
+    out.alpha = gam / (del - beta * gam / in.alpha);
+    out.beta = beta;
+    out.gamma = gam;
+    return true;
+}
+
+__global__ void dpcg_update_kernel(tt_dpcg_t a, int parity) {
+    DStates* st = reinterpret_cast<DStates*>(a.state);
+    const DState in = st->s[parity];
+    DState out;
+    bool improved;
+    const bool go = dpcg_scalars(in, a.sums, out, improved);
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+    // (a finished state propagates: the next update copies it into the other slot)
+    if (tid == 0) st->s[parity ^ 1] = out;
+    if (!go) {
+        // done by this test: settle the best iterate (fem.py:141-152) -- it is x itself when
+        // this residual improved; b = 0 returns zeros
+        if (!in.done && out.zero_rhs)
+            for (int64_t i = tid; i < a.n_own; i += nt) a.x[i] = 0.0;
+        else if (!in.done && improved && !out.converged)
+            for (int64_t i = tid; i < a.n_own; i += nt) a.best_x[i] = a.x[i];
+        return;
+    }
+    const double alpha = out.alpha, beta = out.beta;
     for (int64_t i = tid; i < a.n_own; i += nt) {
         const double xi = a.x[i];
         if (improved) a.best_x[i] = xi;
         const double pi = a.u[i] + beta * a.p[i];
         const double si = a.w[i] + beta * a.s[i];
         const double ri = a.r[i] - alpha * si;
+        const double ui = a.dinv[i] * ri;
         a.p[i] = pi;
         a.s[i] = si;
         a.x[i] = xi + alpha * pi;
         a.r[i] = ri;
-        a.u[i] = a.dinv[i] * ri;
+        a.u[i] = ui;
+        for (int64_t k = a.send_start[i]; k < a.send_start[i + 1]; ++k) a.send_buf[a.send_pos[k]] = ui;
     }
-}
-
-__global__ void dpcg_pack_kernel(tt_dpcg_t a) {
-    const DState* st = reinterpret_cast<const DState*>(a.state);
-    if (st->done) return;
-    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (t < a.n_send) a.send_buf[t] = a.u[a.send_idx[t]];
 }
 
 // w = A u over the own rows (W/8 lanes per row, each lane 8 ELL entries: two int4 column
 // loads and four double2 value loads, then 8 independent gathers of u), and the block
 // partials of (r.u, w.u, r.r); the last block to finish sums the partials in block order.
+// `parity` = the slot the preceding update wrote.
 template <int W>
-__global__ void __launch_bounds__(kDBlock) dpcg_spmv_kernel(tt_dpcg_t a) {
-    DState* st = reinterpret_cast<DState*>(a.state);
-    if (st->done) return;
+__global__ void __launch_bounds__(kDBlock) dpcg_spmv_kernel(tt_dpcg_t a, int parity) {
+    DStates* st = reinterpret_cast<DStates*>(a.state);
+    if (st->s[parity].done) return;
     constexpr int LPR = W / 8;
     __shared__ double sh[3][kDBlock / 32];
     __shared__ bool last;
@@ -145,74 +202,38 @@ __global__ void __launch_bounds__(kDBlock) dpcg_spmv_kernel(tt_dpcg_t a) {
     }
     __syncthreads();
     if (!last) return;
+    // the last block: every thread sums a fixed strided subset of the block partials, then a
+    // fixed shuffle / shared tree (deterministic; a one-thread serial sum of ~1k L2 loads cost
+    // 40 us per iteration)
+    __threadfence();
+    double t[3] = {0.0, 0.0, 0.0};
+    for (unsigned q = threadIdx.x; q < gridDim.x; q += kDBlock)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) t[k] += __ldcg(a.part + k * gridDim.x + q);
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+        for (int off = 16; off > 0; off >>= 1) t[k] += __shfl_xor_sync(0xffffffffu, t[k], off);
+    __syncthreads();
+    if (lane == 0) { sh[0][w] = t[0]; sh[1][w] = t[1]; sh[2][w] = t[2]; }
+    __syncthreads();
     if (threadIdx.x < 3) {
-        __threadfence();
-        double t = 0.0;
-        for (unsigned q = 0; q < gridDim.x; ++q) t += __ldcg(a.part + threadIdx.x * gridDim.x + q);
-        a.sums[threadIdx.x] = t;
+        double u2 = 0.0;
+        for (int q = 0; q < kDBlock / 32; ++q) u2 += sh[threadIdx.x][q];
+        a.sums[threadIdx.x] = u2;
     }
     if (threadIdx.x == 0) st->ticket = 0;
 }
 
-// After the all-reduce of sums: iteration bookkeeping on one thread (fem.py:131-152).
-__global__ void dpcg_scalars_kernel(tt_dpcg_t a) {
-    DState* st = reinterpret_cast<DState*>(a.state);
-    if (st->done) return;
-    const double gam = a.sums[0], del = a.sums[1], rr = a.sums[2];
-    if (!st->primed) {
-        // first call (after start): r = b, u = dinv b, w = A u
-        st->primed = 1;
-        st->bnorm = sqrt(rr);
-        if (st->bnorm == 0.0) {
-            st->done = 1; st->converged = 1; st->zero_rhs = 1;
-            return;
-        }
-        st->res = st->best = st->bnorm / st->bnorm;  // ||r0|| / ||b||  (fem.py:136)
-        st->gamma = gam;
-        st->alpha = gam / del;
-        st->beta = 0.0;
-        st->improved = 0;
-        if (st->maxiter == 0) st->done = 1;
-        return;
-    }
-    st->it += 1;
-    const double res = sqrt(rr) / st->bnorm;
-    st->res = res;
-    st->improved = 0;
-    if (res < st->best) {
-        st->best = res;
-        st->improved = 1;  // x holds the new best: the next update (or finish) copies it
-    }
-    if (res <= st->tol) {
-        st->done = 1;
-        st->converged = 1;
-        return;
-    }
-    if (st->it >= st->maxiter) {
-        st->done = 1;
-        return;
-    }
-    const double beta = gam / st->gamma;
-    st->alpha = gam / (del - beta * gam / st->alpha);
-    st->beta = beta;
-    st->gamma = gam;
-}
-
 __global__ void dpcg_finish_kernel(tt_dpcg_t a, tt_pcg_result_t* res) {
-    const DState* st = reinterpret_cast<const DState*>(a.state);
-    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const int64_t nt = (int64_t)gridDim.x * blockDim.x;
-    if (st->zero_rhs) {
-        for (int64_t i = tid; i < a.n_own; i += nt) a.x[i] = 0.0;
-    } else if (!st->converged && st->improved) {
-        for (int64_t i = tid; i < a.n_own; i += nt) a.best_x[i] = a.x[i];
-    }
-    if (tid == 0 && res) {
-        res->iterations = st->it;
-        res->residual = st->res;
-        res->best_residual = st->best;
-        res->converged = st->converged;
-        res->zero_rhs = st->zero_rhs;
+    const DStates* st = reinterpret_cast<const DStates*>(a.state);
+    if (blockIdx.x == 0 && threadIdx.x == 0 && res) {
+        // once done both slots hold the final state; before, the later one is s[1] or s[0]
+        const DState& s = st->s[0].done ? st->s[0] : st->s[1];
+        res->iterations = s.it;
+        res->residual = s.res;
+        res->best_residual = s.best;
+        res->converged = s.converged;
+        res->zero_rhs = s.zero_rhs;
     }
 }
 
@@ -240,8 +261,9 @@ static unsigned dgrid(int64_t n) {
 }
 
 static bool dpcg_ok(const tt_dpcg_t* a) {
-    if (!a || a->n_own < 0 || a->n_ext < a->n_own || (a->width != 8 && a->width != 16) || !a->state) {
-        set_error("tt_dpcg: bad descriptor (width must be 8 or 16)");
+    if (!a || a->n_own < 0 || a->n_ext < a->n_own || (a->width != 8 && a->width != 16) || !a->state ||
+        !a->send_start) {
+        set_error("tt_dpcg: bad descriptor (width must be 8 or 16, send_start required)");
         return false;
     }
     return true;
@@ -259,37 +281,24 @@ extern "C" int tt_dpcg_start(const tt_dpcg_t* a, void* stream) {
     return launch_check("dpcg_start_kernel");
 }
 
-extern "C" int tt_dpcg_update(const tt_dpcg_t* a, void* stream) {
-    if (!dpcg_ok(a)) return TT_ERR_INVALID_PARAMETER;
-    dpcg_update_kernel<<<dgrid(a->n_own), kDBlock, 0, as_stream(stream)>>>(*a);
+extern "C" int tt_dpcg_update(const tt_dpcg_t* a, int parity, void* stream) {
+    if (!dpcg_ok(a) || (parity != 0 && parity != 1)) return TT_ERR_INVALID_PARAMETER;
+    dpcg_update_kernel<<<dgrid(a->n_own), kDBlock, 0, as_stream(stream)>>>(*a, parity);
     return launch_check("dpcg_update_kernel");
 }
 
-extern "C" int tt_dpcg_pack(const tt_dpcg_t* a, void* stream) {
-    if (!dpcg_ok(a)) return TT_ERR_INVALID_PARAMETER;
-    if (a->n_send == 0) return TT_OK;
-    dpcg_pack_kernel<<<grid_for(a->n_send, kDBlock), kDBlock, 0, as_stream(stream)>>>(*a);
-    return launch_check("dpcg_pack_kernel");
-}
-
-extern "C" int tt_dpcg_spmv(const tt_dpcg_t* a, void* stream) {
-    if (!dpcg_ok(a)) return TT_ERR_INVALID_PARAMETER;
+extern "C" int tt_dpcg_spmv(const tt_dpcg_t* a, int parity, void* stream) {
+    if (!dpcg_ok(a) || (parity != 0 && parity != 1)) return TT_ERR_INVALID_PARAMETER;
     const int lpr = a->width / 8;
     const unsigned g = dgrid(a->n_own * lpr);
-    if (a->width == 8) dpcg_spmv_kernel<8><<<g, kDBlock, 0, as_stream(stream)>>>(*a);
-    else dpcg_spmv_kernel<16><<<g, kDBlock, 0, as_stream(stream)>>>(*a);
+    if (a->width == 8) dpcg_spmv_kernel<8><<<g, kDBlock, 0, as_stream(stream)>>>(*a, parity);
+    else dpcg_spmv_kernel<16><<<g, kDBlock, 0, as_stream(stream)>>>(*a, parity);
     return launch_check("dpcg_spmv_kernel");
-}
-
-extern "C" int tt_dpcg_scalars(const tt_dpcg_t* a, void* stream) {
-    if (!dpcg_ok(a)) return TT_ERR_INVALID_PARAMETER;
-    dpcg_scalars_kernel<<<1, 1, 0, as_stream(stream)>>>(*a);
-    return launch_check("dpcg_scalars_kernel");
 }
 
 extern "C" int tt_dpcg_finish(const tt_dpcg_t* a, tt_pcg_result_t* result, void* stream) {
     if (!dpcg_ok(a)) return TT_ERR_INVALID_PARAMETER;
-    dpcg_finish_kernel<<<dgrid(a->n_own), kDBlock, 0, as_stream(stream)>>>(*a, result);
+    dpcg_finish_kernel<<<1, 32, 0, as_stream(stream)>>>(*a, result);
     return launch_check("dpcg_finish_kernel");
 }
 

@@ -268,7 +268,8 @@ def _dev_i64(a) -> torch.Tensor:
 
 
 # ------------------------------------------------------------------ distributed PCG
-_DONE_INT32 = 16   # tt_dist.cu DState: 6 doubles, 2 int64, then int32 done
+# tt_dist.cu DStates: two DState slots of 88 bytes (6 doubles, 2 int64, then int32 done, ...)
+_DONE_INT32 = (16, 16 + 22)
 
 
 class DistributedPCG:
@@ -298,11 +299,17 @@ class DistributedPCG:
         f64 = dict(dtype=torch.float64, device=dev)
         self.vec = {n: torch.zeros(max(n_on, 1), **f64) for n in ("x", "best_x", "r", "w", "p", "s", "dinv")}
         self.u = torch.zeros(max(self.n_ext, 1), **f64)
-        self.send_idx = _dev_i64(plan.send_node_rows)
-        self.send_buf = torch.zeros(max(len(plan.send_node_rows), 1), **f64)
+        # send slots of every owned row: row i's u goes to send_buf[send_pos[k]] for k in
+        # [send_start[i], send_start[i+1]) -- one slot per peer that needs it
+        rows = np.asarray(plan.send_node_rows, dtype=np.int64)
+        order = np.argsort(rows, kind="stable")
+        start = np.zeros(n_on + 1, np.int64)
+        np.cumsum(np.bincount(rows, minlength=n_on), out=start[1:])
+        self.send_start, self.send_pos = _dev_i64(start), _dev_i64(order)
+        self.send_buf = torch.zeros(max(len(rows), 1), **f64)
         self.part = torch.zeros(int(_lib.lib().tt_dpcg_part_doubles()), **f64)
         self.sums = torch.zeros(3, **f64)
-        self.state = torch.zeros(16, **f64)
+        self.state = torch.zeros(32, **f64)     # TT_DPCG_STATE_BYTES
         self.result = torch.zeros(4, **f64)     # tt_pcg_result_t
         d = _lib.tt_dpcg_t()
         d.n_own, d.n_ext, d.width = n_on, self.n_ext, W
@@ -310,36 +317,39 @@ class DistributedPCG:
         for n in ("x", "best_x", "r", "w", "p", "s", "dinv"):
             setattr(d, n, _lib.ptr(self.vec[n]).value)
         d.u = _lib.ptr(self.u).value
-        d.send_idx, d.n_send = _lib.ptr(self.send_idx).value, len(plan.send_node_rows)
+        d.send_start, d.send_pos = _lib.ptr(self.send_start).value, _lib.ptr(self.send_pos).value
+        d.n_send = len(rows)
         d.send_buf, d.part = _lib.ptr(self.send_buf).value, _lib.ptr(self.part).value
         d.sums, d.state = _lib.ptr(self.sums).value, _lib.ptr(self.state).value
         self.b = torch.zeros(max(n_on, 1), **f64)
         d.b = _lib.ptr(self.b).value
         self.desc = d
         self._graph = None
+        self._last_chunks = 1
 
-    def _call(self, name):
-        _lib.call(name, C.byref(self.desc), _lib.stream_handle())
+    def _call(self, name, *args):
+        _lib.call(name, C.byref(self.desc), *args, _lib.stream_handle())
 
-    def _exchange_and_reduce(self):
+    def _exchange_and_reduce(self, parity: int):
+        """Halo all-to-all of the send buffer, w = A u, all-reduce of the 3 partial sums."""
         p = self.plan
-        self._call("tt_dpcg_pack")
         self.comm.alltoallv(self.u[self.n_own:self.n_ext], self.send_buf[:len(p.send_node_rows)],
                             p.halo_counts, p.send_node_counts)
-        self._call("tt_dpcg_spmv")
+        self._call("tt_dpcg_spmv", parity)
         self.comm.allreduce_(self.sums)
-        self._call("tt_dpcg_scalars")
 
     def _iterations(self, n: int):
-        for _ in range(n):
-            self._call("tt_dpcg_update")
-            self._exchange_and_reduce()
+        # iteration k: update reads state slot k & 1 and writes the other (n is even, so every
+        # chunk starts at slot 0)
+        for k in range(n):
+            self._call("tt_dpcg_update", k & 1)
+            self._exchange_and_reduce((k & 1) ^ 1)
 
     def _chunk(self, n: int):
-        """``n`` iterations: with NCCL one CUDA-graph replay of (update, pack, halo
-        all-to-all, spmv, all-reduce, scalars) x n, captured on first use -- every pointer
-        and all iteration scalars live in persistent device buffers, so the graph serves
-        every solve; host-staged backends run them eagerly."""
+        """``n`` iterations: with NCCL one CUDA-graph replay of (update, halo all-to-all,
+        spmv, all-reduce) x n, captured on first use -- every pointer and all iteration
+        scalars live in persistent device buffers, so the graph serves every solve;
+        host-staged backends run them eagerly."""
         if self.comm.staged:
             return self._iterations(n)
         if self._graph is None:
@@ -353,6 +363,7 @@ class DistributedPCG:
 
     def solve(self, b_own: torch.Tensor, tol: float = 1e-12, maxiter: int | None = None,
               chunk: int = 8):
+        assert chunk % 2 == 0, "state slots alternate: chunks of an even number of iterations"
         """Launch the solve of the owned rows; returns (x_own, best_x_own, result) after
         the iteration's device state reports done (one host read per ``chunk`` iterations;
         iterations past done are no-ops)."""
@@ -361,10 +372,19 @@ class DistributedPCG:
             self.b[:self.n_own].copy_(b_own)
         self.desc.tol, self.desc.maxiter = float(tol), maxiter
         self._call("tt_dpcg_start")
-        self._exchange_and_reduce()
-        done_word = self.state.view(torch.int32)[_DONE_INT32:_DONE_INT32 + 1]
-        while not int(done_word.item()):
+        self._exchange_and_reduce(0)
+        done_idx = torch.tensor(_DONE_INT32, device=self.state.device)
+        # the first check after as many chunks as the previous solve needed (iterations past
+        # done are no-op kernels; a host round trip costs more than a few of them)
+        for _ in range(self._last_chunks - 1):
             self._chunk(chunk)
+        issued = max(self._last_chunks - 1, 0)
+        while True:
+            self._chunk(chunk)
+            issued += 1
+            if int(self.state.view(torch.int32)[done_idx].max().item()):
+                break
+        self._last_chunks = issued
         _lib.call("tt_dpcg_finish", C.byref(self.desc), _lib.ptr(self.result), _lib.stream_handle())
         return self.vec["x"][:self.n_own], self.vec["best_x"][:self.n_own], self.result
 
