@@ -46,5 +46,19 @@ for name, n in (("c2", 55), ("c4", 120)):
     out[name] = {"rows": m.n_nodes, "distributed_ms": t_d, "distributed_iters": int(it_d),
                  "distributed_us_per_iter": 1e3 * t_d / max(int(it_d), 1),
                  "single_launch_ms": t_r, "single_launch_iters": int(decode_result(res2).iterations)}
+# rank 0 of an 8-GPU C4 partition, emulated on this GPU: its kernels and graph replays on its
+# 1/8 of the rows, collectives replaced by no-ops (no convergence: a fixed 22 iterations) --
+# the per-iteration device cost a rank pays besides the NCCL latency
+m = tt.generate_cube_mesh(120, 0.2, seed=20)
+M = m.device.mass
+b = M.matvec(torch.as_tensor(np.sin(3 * m.nodes[:, 0]) + 2.0, device="cuda"))
+dc = DistributedCoupling(m, rank=0, world=8, solve="distributed")
+dc.comm.alltoallv = lambda *a, **k: None
+dc.comm.allreduce_ = lambda t, op=None: t
+b_own = b[torch.as_tensor(dc.plan.own_nodes, device="cuda")]
+t8, _ = timed(lambda: dc.solve_owned(b_own, 0.0, maxiter=22))
+out["c4_rank0_of_8_emulated"] = {"own_rows": len(dc.plan.own_nodes), "halo_rows": len(dc.plan.halo_nodes),
+                                 "interface_elems_sent": int(sum(dc.plan.send_counts)),
+                                 "ms_22_iterations_no_collectives": t8, "us_per_iter": 1e3 * t8 / 22}
 print(json.dumps(out, indent=1))
 dist.destroy_process_group()
