@@ -63,6 +63,7 @@ extern "C" {
 #define TT_FLAG_NONMANIFOLD     16  /* a facet shared by > 2 elements (mesh.py:50-53)      */
 #define TT_FLAG_WIDE_ROWS       32  /* an ELL column is > 32767 rows from its row: no slab  */
 #define TT_FLAG_SNAPPED         64  /* tt_seed_elements: an anchor point was outside (snapped) */
+#define TT_FLAG_PEER_TIMEOUT   128  /* a peer never reached a cross-GPU barrier (peer solve gave up) */
 
 /* tt_source_t.hints */
 #define TT_HINT_DEFER_SNAP       1  /* outside samples likely (the seeds saw TT_FLAG_SNAPPED):
@@ -382,6 +383,21 @@ int tt_dpcg_update(const tt_dpcg_t* a, int parity, void* stream);
 int tt_dpcg_spmv(const tt_dpcg_t* a, int parity, void* stream);
 /* the result record (device): iterations, residual, best residual, converged, zero_rhs */
 int tt_dpcg_finish(const tt_dpcg_t* a, tt_pcg_result_t* result, void* stream);
+/* Peer-memory forms (NVLink symmetric memory, no NCCL on the data path):
+ * tt_reduce_nodes_ranked -- the owner-side node reduction reading each incidence's
+ *   contribution straight from the rank that computed it: b[n] = sum over q in
+ *   [inc_start[n], inc_start[n+1]) of ptrs[inc_rank[q]][inc_entry[q]], in that order.
+ * tt_dpcg_peer_solve -- the whole distributed PCG as ONE cooperative launch per rank: u of the
+ *   owned rows lives in the rank's symmetric buffer sym[rank] (u_len doubles, then 2 x 3
+ *   partial-sum slots); halo column h is read from sym[halo_owner[h]][halo_row[h]]; two
+ *   cross-GPU barriers per iteration over the signal pads (release/acquire at system scope;
+ *   *epoch persists across solves); every rank sums the world's partials in rank order.
+ *   A barrier that waits > ~20 s sets TT_FLAG_PEER_TIMEOUT in *status and returns unconverged. */
+int tt_reduce_nodes_ranked(int64_t n_nodes, const int64_t* inc_start, const int32_t* inc_rank,
+                           const int32_t* inc_entry, const double* const* ptrs, double* b, void* stream);
+int tt_dpcg_peer_solve(const tt_dpcg_t* a, const int32_t* halo_owner, const int32_t* halo_row,
+                       double* const* sym, uint32_t* const* pads, int64_t u_len, int rank, int world,
+                       uint32_t* epoch, int32_t* status, tt_pcg_result_t* result, void* stream);
 /* dst[t, :] = src[idx[t], :] and dst[idx[t], :] = src[t, :] for rows of k doubles */
 int tt_gather_rows(int64_t n, int k, const int64_t* idx, const double* src, double* dst, void* stream);
 int tt_scatter_rows(int64_t n, int k, const int64_t* idx, const double* src, double* dst, void* stream);

@@ -25,6 +25,7 @@ TT_FLAG_NONMANIFOLD = 16
 TT_FLAG_WIDE_ROWS = 32
 TT_SEED_ANCHORS = 16
 TT_FLAG_SNAPPED = 64
+TT_FLAG_PEER_TIMEOUT = 128
 TT_HINT_DEFER_SNAP = 1
 TT_PLAN_SHARED, TT_PLAN_PHILOX = 0, 1
 TT_SRC_EXPR, TT_SRC_MESH, TT_SRC_VALUES, TT_SRC_CACHED = 0, 1, 2, 3
@@ -151,6 +152,8 @@ _SIGNATURES = {
     "tt_dpcg_update": ([_P, _I, _P], _I),
     "tt_dpcg_spmv": ([_P, _I, _P], _I),
     "tt_dpcg_finish": ([_P, _P, _P], _I),
+    "tt_reduce_nodes_ranked": ([_I64, _P, _P, _P, _P, _P, _P], _I),
+    "tt_dpcg_peer_solve": ([_P, _P, _P, _P, _P, _I64, _I, _I, _P, _P, _P, _P], _I),
     "tt_gather_rows": ([_I64, _I, _P, _P, _P, _P], _I),
     "tt_scatter_rows": ([_I64, _I, _P, _P, _P, _P], _I),
     "tt_fp64_peak_probe": ([_I64, _P, C.POINTER(_I), C.POINTER(_I), _P], _I),

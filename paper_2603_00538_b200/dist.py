@@ -389,12 +389,144 @@ class DistributedPCG:
         return self.vec["x"][:self.n_own], self.vec["best_x"][:self.n_own], self.result
 
 
+def _symm_rendezvous(t: torch.Tensor, comm: "_Comm"):
+    import torch.distributed._symmetric_memory as symm_mem
+    group = comm.group if comm.group is not None else dist.group.WORLD
+    try:
+        symm_mem.enable_symm_mem_for_group(group.group_name)
+    except Exception:
+        pass                       # newer torch: enabled on demand
+    return symm_mem.rendezvous(t, group)
+
+
+class PeerPCG:
+    """The row-partitioned PCG as ONE cooperative kernel per rank over NVLink peer memory
+    (``tt_dpcg_peer_solve``): the owned rows of u live in a symmetric-memory buffer, halo
+    columns are read from the owning peer's buffer, the world's partial sums are read from
+    every peer in rank order, and two cross-GPU flag barriers per iteration replace the
+    NCCL all-to-all and all-reduce.  No host involvement per iteration."""
+
+    _PAD_BASE = 256   # signal-pad slots used by the barrier: [base, base + world)
+
+    def __init__(self, mass, part: Partition, plan: RankPlan, comm: _Comm, n_global: int):
+        ell = mass.ell()
+        if ell is None:
+            raise ValueError("peer PCG needs the ELL mass matrix (<= 16 entries per row)")
+        if not comm.active or comm.staged:
+            raise ValueError("peer PCG needs an NCCL process group (symmetric memory over NVLink)")
+        ec, ev, dg, W = ell
+        dev = ev.device
+        self.comm, self.plan, self.n_global = comm, plan, n_global
+        n_on, n_h = len(plan.own_nodes), len(plan.halo_nodes)
+        self.n_own = n_on
+        colmap = torch.full((n_global,), -1, dtype=torch.int32, device=dev)
+        own = _dev_i64(plan.own_nodes)
+        colmap[own] = torch.arange(n_on, dtype=torch.int32, device=dev)
+        colmap[_dev_i64(plan.halo_nodes)] = torch.arange(n_on, n_on + n_h, dtype=torch.int32, device=dev)
+        self.ec = colmap[ec[own].long()].contiguous()
+        self.ev, self.diag = ev[own].contiguous(), dg[own].contiguous()
+        # halo column h: (owning rank, its local row)
+        owners = part.node_owner
+        local_row = np.empty(n_global, np.int64)
+        for q in range(part.world):
+            oq = np.flatnonzero(owners == q)
+            local_row[oq] = np.arange(len(oq))
+        self.halo_owner = torch.as_tensor(owners[plan.halo_nodes].astype(np.int32), device=dev)
+        self.halo_row = torch.as_tensor(local_row[plan.halo_nodes].astype(np.int32), device=dev)
+        self.u_len = int(np.bincount(owners, minlength=part.world).max())
+        self.sym = _sym_empty(self.u_len + 8, dev)
+        self.hdl = _symm_rendezvous(self.sym, comm)
+        if self.hdl.signal_pad_size < 4 * (self._PAD_BASE + part.world):
+            raise ValueError("symmetric-memory signal pads too small for the peer barrier")
+        self.sym_ptrs = torch.tensor(list(self.hdl.buffer_ptrs), dtype=torch.int64, device=dev)
+        self.pad_ptrs = torch.tensor([p + 4 * self._PAD_BASE for p in self.hdl.signal_pad_ptrs],
+                                     dtype=torch.int64, device=dev)
+        f64 = dict(dtype=torch.float64, device=dev)
+        self.vec = {n: torch.zeros(max(n_on, 1), **f64) for n in ("x", "best_x", "r", "w", "p", "s", "dinv", "b")}
+        self.part = torch.zeros(int(_lib.lib().tt_dpcg_part_doubles()), **f64)
+        self.epoch = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.result = torch.zeros(4, **f64)
+        d = _lib.tt_dpcg_t()
+        d.n_own, d.n_ext, d.width = n_on, n_on + n_h, W
+        d.ell_cols, d.ell_vals, d.diag = (_lib.ptr(t).value for t in (self.ec, self.ev, self.diag))
+        for n in ("x", "best_x", "r", "w", "p", "s", "dinv", "b"):
+            setattr(d, n, _lib.ptr(self.vec[n]).value)
+        d.u = _lib.ptr(self.sym).value
+        d.part = _lib.ptr(self.part).value
+        self.desc = d
+
+    def solve(self, b_own: torch.Tensor, tol: float = 1e-12, maxiter: int | None = None):
+        from .errors import TransferError
+        maxiter = 10 * self.n_global if maxiter is None else int(maxiter)
+        if b_own.numel():
+            self.vec["b"][:self.n_own].copy_(b_own)
+        self.desc.tol, self.desc.maxiter = float(tol), maxiter
+        self.status.zero_()
+        _lib.call("tt_dpcg_peer_solve", C.byref(self.desc), _lib.ptr(self.halo_owner), _lib.ptr(self.halo_row),
+                  _lib.ptr(self.sym_ptrs), _lib.ptr(self.pad_ptrs), self.u_len, self.comm.rank, self.comm.world,
+                  _lib.ptr(self.epoch), _lib.ptr(self.status), _lib.ptr(self.result), _lib.stream_handle())
+        if int(self.status.item()) & _lib.TT_FLAG_PEER_TIMEOUT:
+            raise TransferError("peer PCG: a peer never reached a cross-GPU barrier")
+        return self.vec["x"][:self.n_own], self.vec["best_x"][:self.n_own], self.result
+
+
+def _sym_empty(n: int, dev) -> torch.Tensor:
+    import torch.distributed._symmetric_memory as symm_mem
+    t = symm_mem.empty(n, dtype=torch.float64, device=dev)
+    t.zero_()
+    return t
+
+
+class PeerLoadExchange:
+    """The load exchange over NVLink peer memory: each rank writes its element contributions
+    into a symmetric-memory buffer and every owner sums its nodes' incidences reading them
+    straight from the ranks that computed them (``tt_reduce_nodes_ranked``, the single-GPU
+    np.add.at order: b bitwise GPU-count invariant) -- one kernel between two device-side
+    barriers instead of a gather, an NCCL all-to-all and a reduction."""
+
+    def __init__(self, coupling: "DistributedCoupling"):
+        c = coupling
+        part, p, k = c.part, c.plan, c.k
+        dev = c.contrib.device
+        counts = np.bincount(part.elem_rank, minlength=part.world)
+        self.buf = _sym_empty(int(counts.max()) * k + 8, dev)
+        self.hdl = _symm_rendezvous(self.buf, c.comm)
+        self.ptrs = torch.tensor(list(self.hdl.buffer_ptrs), dtype=torch.int64, device=dev)
+        local = np.empty(part.target.n_elems, np.int64)
+        for q in range(part.world):
+            eq = np.flatnonzero(part.elem_rank == q)
+            local[eq] = np.arange(len(eq))
+        flat = part.target.elements.ravel()
+        q_idx = np.flatnonzero(part.node_owner[flat] == p.rank)
+        order = np.argsort(flat[q_idx], kind="stable")
+        q_idx = q_idx[order]                       # owned nodes' incidences, ascending (e, a) per node
+        e, a = q_idx // k, q_idx % k
+        self.inc_rank = torch.as_tensor(part.elem_rank[e].astype(np.int32), device=dev)
+        self.inc_entry = torch.as_tensor((local[e] * k + a).astype(np.int32), device=dev)
+        self.inc_start = c.inc_start
+        self.c = c
+
+    def load_owned(self, source, plan, status) -> torch.Tensor:
+        from .montecarlo import element_contributions
+        c, p, k = self.c, self.c.plan, self.c.k
+        self.hdl.barrier(channel=0)           # peers are done reading the previous step
+        n = p.n_own_elems
+        if n:
+            element_contributions(c.sub, source, plan, out=self.buf[:n * k].view(n, k), status=status)
+        self.hdl.barrier(channel=1)           # every rank's contributions are visible
+        b = torch.empty(max(len(p.own_nodes), 1), dtype=torch.float64, device=self.buf.device)
+        _lib.call("tt_reduce_nodes_ranked", len(p.own_nodes), _lib.ptr(self.inc_start), _lib.ptr(self.inc_rank),
+                  _lib.ptr(self.inc_entry), _lib.ptr(self.ptrs), _lib.ptr(b), _lib.stream_handle())
+        return b[:len(p.own_nodes)]
+
+
 # ------------------------------------------------------------------ the coupling step
 class DistributedCoupling:
     """Partitioned MC transfer step over the ranks of ``group`` (one GPU each)."""
 
     def __init__(self, target, rank: int | None = None, world: int | None = None, group=None,
-                 partition: str = "morton", solve: str = "auto"):
+                 partition: str = "morton", solve: str = "auto", exchange: str = "nccl"):
         self.comm = _Comm(group)
         self.rank = self.comm.rank if rank is None else int(rank)
         self.world = self.comm.world if world is None else int(world)
@@ -419,10 +551,13 @@ class DistributedCoupling:
         self.gather_order = _dev_i64(np.concatenate(all_own))
         if solve == "auto":
             solve = "distributed" if (self.world > 1 and target.n_nodes >= 1_000_000) else "replicated"
-        if solve not in ("distributed", "replicated"):
+        if solve not in ("distributed", "peer", "replicated"):
             raise ValueError(f"unknown solve mode {solve!r}")
+        if exchange not in ("nccl", "peer"):
+            raise ValueError(f"unknown exchange {exchange!r}")
         self.solve_mode = solve
         self._pcg = None
+        self._peer_load = PeerLoadExchange(self) if exchange == "peer" else None
 
     # ---- load
     def _defer_hint(self, locator):
@@ -445,6 +580,8 @@ class DistributedCoupling:
         status = status if status is not None else _lib.status_word()
         if isinstance(source, MeshBackedField) and source.locator.walk:
             self._defer_hint(source.locator)
+        if self._peer_load is not None:
+            return self._peer_load.load_owned(source, plan, status)
         n_oe = p.n_own_elems
         if n_oe:
             element_contributions(self.sub, source, plan, out=self.contrib[:n_oe], status=status)
@@ -484,9 +621,11 @@ class DistributedCoupling:
     # ---- solve
     def solve_owned(self, b_own: torch.Tensor, tol: float = 1e-12, maxiter: int | None = None):
         """(x, best_x, result): owned parts (distributed) or full vectors (replicated)."""
-        if self.solve_mode == "distributed":
+        if self.solve_mode in ("distributed", "peer"):
             if self._pcg is None:
-                self._pcg = DistributedPCG(self.target.device.mass, self.plan, self.comm, self.target.n_nodes)
+                self._pcg = (PeerPCG(self.target.device.mass, self.part, self.plan, self.comm, self.target.n_nodes)
+                             if self.solve_mode == "peer" else
+                             DistributedPCG(self.target.device.mass, self.plan, self.comm, self.target.n_nodes))
             return self._pcg.solve(b_own, tol, maxiter)
         from .fem import pcg_device
         return pcg_device(self.target.device.mass, self.gather_full(b_own), tol=tol, maxiter=maxiter)
@@ -502,7 +641,7 @@ class DistributedCoupling:
         r, flags = decode_result(res, status)     # one synchronisation: solve + load status
         if flags:
             self._raise(status)
-        distributed = self.solve_mode == "distributed"
+        distributed = self.solve_mode != "replicated"
         if r.zero_rhs:
             x = torch.zeros_like(x)
         if not r.converged:
@@ -600,7 +739,7 @@ class DistributedMCOperator:
         from .errors import NoConvergence
         x, best_x, res = self.c.solve_owned(self.load_owned(field), self.cg_tol)
         r = decode_result(res)
-        distributed = self.c.solve_mode == "distributed"
+        distributed = self.c.solve_mode != "replicated"
         if r.zero_rhs:
             x = torch.zeros_like(x)
         if not r.converged:

@@ -33,4 +33,8 @@ if T 300 python scripts/profile_step.py --steps 3 --c5 > /dev/null 2>&1; then
   T 900 $N -k regex:spmv_rect -o $O/spmv_rect python scripts/profile_step.py --steps 3 --c5 > /dev/null 2>&1 || echo "ncu spmv failed"
 fi
 T 900 $N -k regex:supermesh_kernel -o $O/supermesh python scripts/profile_supermesh.py > /dev/null 2>&1 || echo "ncu supermesh failed"
+# text summaries on the box (gpurun copies back at most 64 MiB): keep only the fused kernel's report
+for r in $O/*.ncu-rep; do python scripts/ncu_summary.py $r > ${r%.ncu-rep}.txt 2>&1; done
+python scripts/ncu_dominant.py $O/mc_mesh.ncu-rep 63888000 "mc_mesh_kernel<3,SHARED,G=4,SLOT> (C2, N=64)" > $O/ncu_dominant_kernel.json 2>&1
+for r in $O/*.ncu-rep; do case $r in */mc_mesh.ncu-rep) ;; *) rm -f $r ;; esac; done
 ls -la $O

@@ -154,3 +154,37 @@ def test_partitioned_step_nccl_graph(tmp_path):
     r = torch.load(tmp_path / "nccl.pt")
     assert r["b_bitwise"] and r["graph"]
     assert max(r["x_errs"]) <= 1e-12, r
+
+
+def _peer_worker(rank, world, port, out):
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", 0))
+    import paper_2603_00538_b200 as tt
+    from paper_2603_00538_b200.dist import DistributedCoupling
+    ref = torch.load(os.path.join(out, "ref.pt"))
+    tgt, src, fs = _problem(tt)
+    loc = tt.UniformGridLocator.build(src)
+    box = tt.MeshBackedField(fs, loc)
+    dc = DistributedCoupling(tgt, solve="peer", exchange="peer")
+    plan = tt.SamplePlan.build(32, "sobol", 3, dim=3)
+    res = {"b_bitwise": bool(torch.equal(dc.load(box, plan).cpu(), ref["b_sobol"]))}
+    errs = []
+    for _ in range(3):     # the barrier epochs persist across solves
+        x = dc.step(box, plan, tol=1e-14).cpu()
+        errs.append(float((x - ref["x"]).abs().max() / ref["x"].abs().max()))
+    res["x_errs"] = errs
+    torch.save(res, os.path.join(out, "peer.pt"))
+    dist.destroy_process_group()
+
+
+def test_partitioned_step_peer_memory(tmp_path):
+    """The NVLink peer-memory forms on this one GPU (world 1, symmetric memory): the
+    contribution exchange read by the owners' reduction kernel, and the distributed PCG as one
+    cooperative kernel with cross-GPU flag barriers (here with itself)."""
+    import paper_2603_00538_b200 as tt
+    torch.save(_reference(tt, *_problem(tt)), tmp_path / "ref.pt")
+    mp.spawn(_peer_worker, args=(1, _free_port(), str(tmp_path)), nprocs=1, join=True)
+    r = torch.load(tmp_path / "peer.pt")
+    assert r["b_bitwise"]
+    assert max(r["x_errs"]) <= 1e-12, r
