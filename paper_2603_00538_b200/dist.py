@@ -478,6 +478,21 @@ def _sym_empty(n: int, dev) -> torch.Tensor:
     return t
 
 
+def peer_incidence(part: Partition, plan: RankPlan):
+    """The owned nodes' incidences (ascending global (element, vertex) within each node, the
+    CSR of ``plan.inc_start``) as (computing rank, entry in that rank's contribution buffer)."""
+    k = part.k
+    local = np.empty(part.target.n_elems, np.int64)
+    for q in range(part.world):
+        eq = np.flatnonzero(part.elem_rank == q)
+        local[eq] = np.arange(len(eq))
+    flat = part.target.elements.ravel()
+    q_idx = np.flatnonzero(part.node_owner[flat] == plan.rank)
+    q_idx = q_idx[np.argsort(flat[q_idx], kind="stable")]
+    e, a = q_idx // k, q_idx % k
+    return part.elem_rank[e].astype(np.int32), (local[e] * k + a).astype(np.int32)
+
+
 class PeerLoadExchange:
     """The load exchange over NVLink peer memory: each rank writes its element contributions
     into a symmetric-memory buffer and every owner sums its nodes' incidences reading them
@@ -493,17 +508,9 @@ class PeerLoadExchange:
         self.buf = _sym_empty(int(counts.max()) * k + 8, dev)
         self.hdl = _symm_rendezvous(self.buf, c.comm)
         self.ptrs = torch.tensor(list(self.hdl.buffer_ptrs), dtype=torch.int64, device=dev)
-        local = np.empty(part.target.n_elems, np.int64)
-        for q in range(part.world):
-            eq = np.flatnonzero(part.elem_rank == q)
-            local[eq] = np.arange(len(eq))
-        flat = part.target.elements.ravel()
-        q_idx = np.flatnonzero(part.node_owner[flat] == p.rank)
-        order = np.argsort(flat[q_idx], kind="stable")
-        q_idx = q_idx[order]                       # owned nodes' incidences, ascending (e, a) per node
-        e, a = q_idx // k, q_idx % k
-        self.inc_rank = torch.as_tensor(part.elem_rank[e].astype(np.int32), device=dev)
-        self.inc_entry = torch.as_tensor((local[e] * k + a).astype(np.int32), device=dev)
+        inc_rank, inc_entry = peer_incidence(part, p)
+        self.inc_rank = torch.as_tensor(inc_rank, device=dev)
+        self.inc_entry = torch.as_tensor(inc_entry, device=dev)
         self.inc_start = c.inc_start
         self.c = c
 
