@@ -60,9 +60,13 @@ def parse_args():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="N>1 collectives (gloo: host-staged, for boxes with fewer GPUs than ranks)")
-    ap.add_argument("--solve", default="auto", choices=["auto", "distributed", "replicated"],
-                    help="N>1 PCG: row-partitioned (halo exchange + 1 all-reduce/iteration) or "
+    ap.add_argument("--solve", default="auto", choices=["auto", "distributed", "peer", "replicated"],
+                    help="N>1 PCG: row-partitioned with NCCL (halo all-to-all + 1 all-reduce/iteration), "
+                         "row-partitioned over NVLink peer memory (one cooperative kernel per rank), or "
                          "replicated on every rank; auto = distributed from 1M target nodes")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer"],
+                    help="N>1 load exchange: NCCL all-to-all of interface contributions, or the owners "
+                         "reading them from peer memory")
     return ap.parse_args()
 
 
@@ -98,7 +102,8 @@ def workload_config(args, world, coupling=None):
     tname, sname = mesh_names(args)
     part = "single GPU"
     if world > 1:
-        part = (f"Morton-ordered target-element parts x{world}, owner-summed interface loads (all-to-all), "
+        part = (f"Morton-ordered target-element parts x{world}, owner-summed interface loads "
+                f"({'peer memory' if args.exchange == 'peer' else 'NCCL all-to-all'}), "
                 f"{coupling.solve_mode if coupling else args.solve} PCG")
     return {"workload": WORKLOADS[args.config],
             "target": tname, "source": sname,
@@ -263,7 +268,7 @@ def run_ours(args):
     c5 = args.config == "c5"
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
     status = _lib.status_word()
-    coupling = DistributedCoupling(tgt, solve=args.solve) if world > 1 else None
+    coupling = DistributedCoupling(tgt, solve=args.solve, exchange=args.exchange) if world > 1 else None
     ops = {}
 
     def operator(plan):
