@@ -327,8 +327,11 @@ __device__ __forceinline__ int seed_slot_nearest(const double* lam) {
 //         anchor (N bytes of dynamic shared memory), built once per block.
 //   DEFER (pairs whose seeds saw outside anchors): an outside sample's nearest-element
 //         search is parked and run warp-cooperatively at the end of the tile.
+#ifndef TT_MC_MINB
+#define TT_MC_MINB 5
+#endif
 constexpr int kMcBlock = 128;
-constexpr int kMcMinBlocks = 5;
+constexpr int kMcMinBlocks = TT_MC_MINB;
 
 template <int D, int PLAN, int G, bool SLOT, bool DEFER>
 __global__ void __launch_bounds__(kMcBlock, kMcMinBlocks) mc_mesh_kernel(TargetDev t, int64_t e_lo, int64_t e_hi,

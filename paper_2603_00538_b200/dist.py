@@ -502,6 +502,8 @@ class PeerLoadExchange:
 
     def __init__(self, coupling: "DistributedCoupling"):
         c = coupling
+        if not c.comm.active or c.comm.staged:
+            raise ValueError("the peer load exchange needs an NCCL process group (symmetric memory over NVLink)")
         part, p, k = c.part, c.plan, c.k
         dev = c.contrib.device
         counts = np.bincount(part.elem_rank, minlength=part.world)

@@ -195,7 +195,7 @@ class CouplingStep:
                 with torch.cuda.graph(g):
                     self._body()
                 self._graph = g
-            except RuntimeError:
+            except Exception:
                 self._graph = False         # (no graph support for a kernel: eager steps)
         if self._graph:
             self._graph.replay()
