@@ -20,9 +20,14 @@ ap.add_argument("--samples", type=int, default=64)
 ap.add_argument("--steps", type=int, default=2)
 ap.add_argument("--mode", default="sobol")
 ap.add_argument("--c5", action="store_true", help="repeated coupling: folded R @ c + PCG")
+ap.add_argument("--torus", action="store_true", help="the C3 torus pair instead of cubes")
 a = ap.parse_args()
-tgt = tt.generate_cube_mesh(a.n, 0.2, seed=20, split="kuhn")
-src = tt.generate_cube_mesh(a.n, 0.2, seed=10, split="kuhn_mirror")
+if a.torus:
+    tgt = tt.generate_torus_mesh(40, 80, 260, perturbation=0.2, seed=20)
+    src = tt.generate_torus_mesh(36, 88, 240, perturbation=0.2, seed=10, split="kuhn_mirror")
+else:
+    tgt = tt.generate_cube_mesh(a.n, 0.2, seed=20, split="kuhn")
+    src = tt.generate_cube_mesh(a.n, 0.2, seed=10, split="kuhn_mirror")
 fs = tt.NodalField.from_function(src, tt.get_field("smooth", dim=3).fn)
 box = tt.MeshBackedField(fs, tt.UniformGridLocator.build(src))
 mass = tgt.device.mass
