@@ -666,3 +666,28 @@ def test_importance_weighted_nonuniform_matches_reference(tt, golden, c1):
         tt.assemble_load_mc_weighted(tgt, tt.AnalyticField(lambda x, y: x + y), plan, bad_dens)
     with pytest.raises(tt.SourceEvalFailed):
         tt.assemble_load_mc_weighted(tgt, tt.AnalyticField(lambda x, y: np.log(x - 2.0)), plan, bad_dens)
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_pipelined_pcg_no_convergence_and_iterates(tt, dim):
+    """The pipelined slab PCG (the default for mass matrices) keeps the reference's
+    outcomes (fem.py:131-152): the same converged x, iteration counts within one of the
+    reference recurrence, NoConvergence after maxiter carrying the best iterate and its
+    residual (matched against the oracle's recurrence to 1e-9), b = 0 -> zeros."""
+    import torch
+    mesh = (tt.generate_square_mesh(30, 0.2, seed=5) if dim == 2 else tt.generate_cube_mesh(9, 0.2, seed=5))
+    M = tt.assemble_mass_matrix(mesh)
+    assert M.jacobi_bounded
+    b = np.random.default_rng(dim).random(mesh.n_nodes)
+    for maxiter in (1, 2, 5, 9):
+        with pytest.raises(tt.NoConvergence) as got:
+            tt.cg_solve(M, b, tol=1e-16, maxiter=maxiter)
+        with pytest.raises(O.NoConvergence) as ref:
+            O.cg_solve(M.csr, b, tol=1e-16, maxiter=maxiter)
+        assert got.value.iterations == maxiter
+        assert got.value.residual == pytest.approx(ref.value.residual, rel=1e-9)
+        assert _rel(got.value.best_x, ref.value.best_x) <= 1e-9
+    x = tt.cg_solve(M, b, tol=1e-14)
+    xr, _ = O.cg_solve(M.csr, b, tol=1e-14)
+    assert _rel(x, xr) <= 1e-12
+    assert np.array_equal(tt.cg_solve(M, np.zeros(mesh.n_nodes)), np.zeros(mesh.n_nodes))
