@@ -390,7 +390,6 @@ __global__ void __launch_bounds__(kMcBlock, kMcMinBlocks) mc_mesh_kernel(TargetD
         }
         __syncwarp();
         const auto vertices = [&](double (*vv)[D]) {
-#pragma unroll
             const double2* row = reinterpret_cast<const double2*>(s_v[wib][gib]);
 #pragma unroll
             for (int q = 0; q < K * D / 2; ++q) {
