@@ -4,6 +4,8 @@ C/OpenMP (oracle/c: the reference's first-ascending-candidate cell scan +
 nearest-centroid snap, _compiled.pyx:147-174, locate.py:97-127), the grid CSR bit-exact
 (locate.py:42-70), and the load vector b normwise <= 1e-12 (montecarlo.py:110-147).
 
+  C1  square n=707 pair (999,698 triangles), N = 64 Sobol   64.0 M samples (2-D: the
+      reference's own meshes; its compiled scan is what the C port restates)
   C2  cube n=55 pair (998,250 tets), N = 64 Sobol            63.9 M samples
   C3  LTX-like torus pair (4,992,000 / 4,561,920 tets), N=16  79.9 M samples, with the
       snap path (non-matching faceted boundaries) in both kernel variants
@@ -26,6 +28,9 @@ pytestmark = pytest.mark.gpu
 
 
 def _meshes(tt, name):
+    if name == "c1":
+        return (tt.generate_square_mesh(707, 0.2, seed=20, diagonal="right"),
+                tt.generate_square_mesh(707, 0.2, seed=10, diagonal="left"), 64)
     if name == "c2":
         return (tt.generate_cube_mesh(55, 0.2, seed=20, split="kuhn"),
                 tt.generate_cube_mesh(55, 0.2, seed=10, split="kuhn_mirror"), 64)
@@ -36,18 +41,21 @@ def _meshes(tt, name):
             tt.generate_cube_mesh(120, 0.2, seed=10, split="kuhn_mirror"), 16)
 
 
-@pytest.mark.parametrize("name", ["c2", "c3", "c4"])
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4"])
 def test_full_size_ids_and_load_vs_oracle(name):
     import torch
     import paper_2603_00538_b200 as tt
     from paper_2603_00538_b200.montecarlo import sample_source_elements
 
     tgt, src, N = _meshes(tt, name)
-    coeffs = np.sin(src.nodes[:, 0]) * np.cos(src.nodes[:, 1]) * np.cos(src.nodes[:, 2]) + 2.0
+    d = tgt.DIM
+    coeffs = np.sin(src.nodes[:, 0]) * np.cos(src.nodes[:, 1]) + 2.0
+    if d == 3:
+        coeffs = np.sin(src.nodes[:, 0]) * np.cos(src.nodes[:, 1]) * np.cos(src.nodes[:, 2]) + 2.0
     fs = tt.NodalField(src, coeffs)
     loc = tt.UniformGridLocator.build(src)
-    plan = tt.SamplePlan.build(N, "sobol", 0, dim=3)
-    lam = O.bary_map(O.sobol(N, 3))
+    plan = tt.SamplePlan.build(N, "sobol", 0, dim=d)
+    lam = O.bary_map(O.sobol(N, d))
     assert np.array_equal(plan.barycentric, lam)
 
     # ---- oracle: the reference algorithm on every sample (C/OpenMP, all host cores)
