@@ -116,10 +116,6 @@ typedef struct tt_mesh {
     const double*  measure;   /* (n_elems,) |area| / |volume| (may be NULL where unused) */
     const int32_t* gid;       /* optional (n_elems,) global element ids of a partition mesh:
                                  the Philox stream counter of element e is gid[e] (NULL = e) */
-    const int32_t* inc_slot;  /* optional (n_elems * k,) node-major output: tt_mc_load writes the
-                                 contribution of (e, a) to contrib[inc_slot[e*k + a]] (the position
-                                 of e*k+a in the node incidence, tt_incidence_slots); NULL =
-                                 element-major contrib[(e - e_lo)*k + a] */
 } tt_mesh_t;
 
 /* Packed per-element locate record, stride TT_REC_STRIDE(dim) doubles (64 B in 2-D,
@@ -301,12 +297,6 @@ int tt_incidence_fill(const tt_mesh_t* mesh, const int64_t* inc_start,
 int tt_reduce_nodes(int64_t n_nodes, int k, const int64_t* inc_start, const int32_t* inc,
                     int64_t e_lo, int64_t e_hi, const double* contrib, double* b,
                     void* stream);
-
-/* slot[inc[q]] = q: the node-major position of every incidence (for tt_mesh_t.inc_slot) */
-int tt_incidence_slots(int64_t n_entries, const int32_t* inc, int32_t* slot, void* stream);
-/* b[n] = sum of vals[inc_start[n] .. inc_start[n+1]) in order (node-major contributions) */
-int tt_reduce_nodes_nm(int64_t n_nodes, const int64_t* inc_start, const double* vals, double* b,
-                       void* stream);
 
 /* ---- P1 mass matrix (CSR, exactly symmetric) ---- */
 int tt_mass_pattern(const tt_mesh_t* mesh, const int64_t* inc_start, const int32_t* inc,

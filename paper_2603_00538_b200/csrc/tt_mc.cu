@@ -153,23 +153,7 @@ struct TargetDev {
     const int32_t* __restrict__ elems;
     const double* __restrict__ measure;
     const int32_t* __restrict__ gid;  // optional global element ids (Philox counters)
-    const int32_t* __restrict__ slot; // optional node-major output slots (E, k): see store_contrib
 };
-
-// Element contribution a of element e (local le): element-major contrib[le*K + a], or -- with
-// node-major slots (tt_mesh_t.inc_slot) -- at the position of the incidence (e, a) in the
-// node -> incidence CSR, so the node gather reads every node's terms contiguously
-template <int K>
-__device__ __forceinline__ void store_contrib(const int32_t* __restrict__ slot, double* contrib, int64_t e,
-                                              int64_t le, const double* v) {
-    if (slot) {
-#pragma unroll
-        for (int i = 0; i < K; ++i) contrib[__ldg(slot + e * K + i)] = v[i];
-    } else {
-#pragma unroll
-        for (int i = 0; i < K; ++i) contrib[le * K + i] = v[i];
-    }
-}
 
 // Philox stream counter of element e: its global id (a rank's partition mesh numbers its
 // elements locally; tt_mesh_t.gid maps them back), so streams are partition independent
@@ -256,10 +240,8 @@ __global__ void __launch_bounds__(256) mc_load_kernel(TargetDev t, int64_t e_lo,
             // density the weights were applied per sample
             const double q = src.density ? 1.0 : (double)N * (1.0 / __ldg(t.measure + e));
             if (contrib) {
-                double v[K];
 #pragma unroll
-                for (int i = 0; i < K; ++i) v[i] = acc[i] / q;
-                store_contrib<K>(t.slot, contrib, e, le, v);
+                for (int i = 0; i < K; ++i) contrib[le * K + i] = acc[i] / q;
             } else {
 #pragma unroll
                 for (int i = 0; i < K; ++i) atomicAdd(b + __ldg(t.elems + e * K + i), acc[i] / q);
@@ -601,10 +583,8 @@ __global__ void __launch_bounds__(kMcBlock, kMcMinBlocks) mc_mesh_kernel(TargetD
         if (active && sub_lane == 0) {
             const double q = (double)N * (1.0 / __ldg(t.measure + e));
             if (contrib) {
-                double v[K];
 #pragma unroll
-                for (int i = 0; i < K; ++i) v[i] = acc[i] / q;
-                store_contrib<K>(t.slot, contrib, e, le, v);
+                for (int i = 0; i < K; ++i) contrib[le * K + i] = acc[i] / q;
             } else if (b) {
 #pragma unroll
                 for (int i = 0; i < K; ++i) atomicAdd(b + __ldg(t.elems + e * K + i), acc[i] / q);
@@ -750,28 +730,6 @@ __global__ void reduce_nodes_kernel(int64_t n_nodes, int k, const int64_t* __res
     b[n] = s;
 }
 
-// b[n] = the node's terms in incidence order (ascending (e, a): np.add.at's order), read
-// contiguously from the node-major contribution array the fused kernel wrote
-__global__ void reduce_nodes_nm_kernel(int64_t n_nodes, const int64_t* __restrict__ inc_start,
-                                       const double* __restrict__ vals, double* __restrict__ b) {
-    const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (n >= n_nodes) return;
-    const int64_t q0 = __ldg(inc_start + n), q1 = __ldg(inc_start + n + 1);
-    double s = 0.0;
-    int64_t q = q0;
-    for (; q + 4 <= q1; q += 4) {
-        const double v0 = __ldg(vals + q), v1 = __ldg(vals + q + 1), v2 = __ldg(vals + q + 2), v3 = __ldg(vals + q + 3);
-        s = add(add(add(add(s, v0), v1), v2), v3);
-    }
-    for (; q < q1; ++q) s = add(s, __ldg(vals + q));
-    b[n] = s;
-}
-
-__global__ void incidence_slot_kernel(int64_t nent, const int32_t* __restrict__ inc, int32_t* __restrict__ slot) {
-    const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (q < nent) slot[inc[q]] = (int32_t)q;
-}
-
 __global__ void incidence_count_kernel(int64_t nent, const int32_t* __restrict__ elems,
                                        unsigned long long* __restrict__ counts) {
     int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -876,7 +834,7 @@ template <int D, int PLAN, int SRC, int G>
 static int launch_mc(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_plan_t* p,
                      const tt_source_t* s, double* contrib, double* b, int32_t* ids,
                      int32_t* status, cudaStream_t st) {
-    TargetDev td{t->nodes, t->elems, t->measure, t->gid, t->inc_slot};
+    TargetDev td{t->nodes, t->elems, t->measure, t->gid};
     PlanDev pd{p->n_samples, p->lam, p->seed};
     SrcDev sd = to_src(*s);
     if constexpr (SRC == TT_SRC_MESH) {
@@ -998,7 +956,7 @@ template <int D, int SRC, int G>
 static int launch_density(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_plan_t* p,
                           const tt_source_t* s, const double* density, double* contrib,
                           int32_t* status, cudaStream_t st) {
-    TargetDev td{t->nodes, t->elems, t->measure, t->gid, t->inc_slot};
+    TargetDev td{t->nodes, t->elems, t->measure, t->gid};
     PlanDev pd{p->n_samples, p->lam, p->seed};
     SrcDev sd = to_src(*s);
     sd.density = density;
@@ -1083,7 +1041,7 @@ extern "C" int tt_map_points(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, con
     }
     int64_t total = (e_hi - e_lo) * p->n_samples;
     if (total == 0) return TT_OK;
-    TargetDev td{t->nodes, t->elems, t->measure, t->gid, t->inc_slot};
+    TargetDev td{t->nodes, t->elems, t->measure, t->gid};
     PlanDev pd{p->n_samples, p->lam, p->seed};
     auto s = as_stream(stream);
     if (t->dim == 2)
@@ -1172,23 +1130,6 @@ extern "C" int tt_reduce_nodes(int64_t n_nodes, int k, const int64_t* inc_start,
     reduce_nodes_kernel<<<grid_for(n_nodes, 256), 256, 0, as_stream(stream)>>>(
         n_nodes, k, inc_start, inc, e_lo, e_hi, contrib, b);
     return launch_check("reduce_nodes_kernel");
-}
-
-extern "C" int tt_incidence_slots(int64_t n_entries, const int32_t* inc, int32_t* slot, void* stream) {
-    if (n_entries < 0 || (n_entries && (!inc || !slot))) {
-        set_error("tt_incidence_slots: bad arguments");
-        return TT_ERR_INVALID_PARAMETER;
-    }
-    if (n_entries == 0) return TT_OK;
-    incidence_slot_kernel<<<grid_for(n_entries, 256), 256, 0, as_stream(stream)>>>(n_entries, inc, slot);
-    return launch_check("incidence_slot_kernel");
-}
-
-extern "C" int tt_reduce_nodes_nm(int64_t n_nodes, const int64_t* inc_start, const double* vals, double* b,
-                                  void* stream) {
-    if (n_nodes == 0) return TT_OK;
-    reduce_nodes_nm_kernel<<<grid_for(n_nodes, 256), 256, 0, as_stream(stream)>>>(n_nodes, inc_start, vals, b);
-    return launch_check("reduce_nodes_nm_kernel");
 }
 
 extern "C" int tt_pack_coeffs(const tt_mesh_t* m, const double* coeffs, double* out, void* stream) {

@@ -42,19 +42,9 @@ class DeviceMesh:
                   _lib.ptr(self.rec), _lib.ptr(self.centroids), _lib.stream_handle())
         self.measure = self.signed_measure.abs()
 
-    def desc(self, with_measure: bool = True, node_major: bool = False) -> _lib.tt_mesh_t:
+    def desc(self, with_measure: bool = True) -> _lib.tt_mesh_t:
         return _lib.mesh_desc(self.dim, self.n_nodes, self.n_elems, self.nodes, self.elems,
-                              self.measure if with_measure else None, self.gid,
-                              self.inc_slot if node_major else None)
-
-    @cached_property
-    def inc_slot(self) -> torch.Tensor:
-        """(E*k,) i32: the position of incidence e*k+a in the node incidence CSR -- the fused
-        kernel's node-major output slots (the node gather then reads contiguously)."""
-        _, inc = self.incidence
-        slot = torch.empty_like(inc)
-        _lib.call("tt_incidence_slots", inc.numel(), _lib.ptr(inc), _lib.ptr(slot), _lib.stream_handle())
-        return slot
+                              self.measure if with_measure else None, self.gid)
 
     @cached_property
     def incidence(self):

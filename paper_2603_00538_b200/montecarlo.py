@@ -310,23 +310,19 @@ def sample_source_elements(target, locator: UniformGridLocator, plan: SamplePlan
 
 def element_contributions(target, source, plan: SamplePlan, e_lo: int = 0,
                           e_hi: int | None = None, out: torch.Tensor | None = None,
-                          status: torch.Tensor | None = None, node_major: bool = False) -> torch.Tensor:
+                          status: torch.Tensor | None = None) -> torch.Tensor:
     """contrib (e_hi-e_lo, k): sum_j f(x_j) psi_a(x_j) / (N p), p = 1/|T|
-    (montecarlo.py:110-132).  Data-dependent errors are OR-ed into ``status``.
-    ``node_major`` (whole mesh only): the (E*k,) array of the contributions at their
-    positions in the node incidence CSR (the layout ``tt_reduce_nodes_nm`` reads)."""
+    (montecarlo.py:110-132).  Data-dependent errors are OR-ed into ``status``."""
     if plan.dim != target.DIM:
         raise DimensionMismatch(f"{plan.dim}-D plan on a {target.DIM}-D mesh")
     e_hi = target.n_elems if e_hi is None else e_hi
-    if node_major and (e_lo, e_hi) != (0, target.n_elems):
-        raise InvalidParameter("node-major contributions cover the whole mesh")
     dm = target.device
     k = target.DIM + 1
     contrib = out if out is not None else torch.empty((e_hi - e_lo, k), dtype=torch.float64,
                                                       device=dm.nodes.device)
     status = status if status is not None else _lib.status_word()
     sdesc, keep = _source_desc(source, target.DIM, target)
-    mdesc, pdesc = dm.desc(node_major=node_major), plan.desc()
+    mdesc, pdesc = dm.desc(), plan.desc()
     s = _lib.stream_handle()
     if sdesc is not None:
         _lib.call("tt_mc_load", C.byref(mdesc), e_lo, e_hi, C.byref(pdesc), C.byref(sdesc),
@@ -347,7 +343,7 @@ def element_contributions(target, source, plan: SamplePlan, e_lo: int = 0,
         vd.dim = target.DIM
         vd.values = _lib.ptr(vals).value
         _lib.call("tt_mc_load", C.byref(mdesc), c0, c1, C.byref(pdesc), C.byref(vd),
-                  _lib.ptr(contrib if node_major else contrib[c0 - e_lo:]), None, _lib.ptr(status), s)
+                  _lib.ptr(contrib[c0 - e_lo:]), None, _lib.ptr(status), s)
         del vals
     return contrib
 
@@ -365,15 +361,7 @@ def load_vector(target, source, plan: SamplePlan, e_lo: int = 0, e_hi: int | Non
     status = status if status is not None else _lib.status_word()
     # (the deterministic path builds the source descriptor once, inside element_contributions)
     sdesc, keep = (None, ()) if deterministic else _source_desc(source, target.DIM, target)
-    if sdesc is None and (e_lo, e_hi) == (0, target.n_elems):
-        # the fused kernel writes node-major; the gather then reads each node's terms
-        # contiguously, in the same (np.add.at) order
-        vals = element_contributions(target, source, plan, status=status, node_major=True)
-        inc_start, _ = dm.incidence
-        b = torch.empty(target.n_nodes, dtype=torch.float64, device=dm.nodes.device)
-        _lib.call("tt_reduce_nodes_nm", target.n_nodes, _lib.ptr(inc_start), _lib.ptr(vals), _lib.ptr(b),
-                  _lib.stream_handle())
-    elif sdesc is None:
+    if sdesc is None:
         contrib = element_contributions(target, source, plan, e_lo, e_hi, status=status)
         b = dm.reduce_nodes(contrib, e_lo, e_hi)
     else:
