@@ -416,7 +416,7 @@ def assemble_load_mc_weighted(target, source, plan: SamplePlan, density, workers
     for c0 in range(0, target.n_elems, chunk):
         c1 = min(c0 + chunk, target.n_elems)
         pts = map_points(target, plan, c0, c1).cpu().numpy()
-        p = np.ascontiguousarray(np.broadcast_to(
+        p = np.array(np.broadcast_to(
             np.asarray(density(np.arange(c0, c1), pts), dtype=np.float64), (c1 - c0, n)))
         uniform = uniform and bool(np.all(p == inv_area[c0:c1, None]))
         pd = torch.from_numpy(p).to(dev)
