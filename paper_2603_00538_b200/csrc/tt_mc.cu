@@ -700,19 +700,23 @@ __global__ void pack_grad_kernel(int64_t E, const int32_t* __restrict__ elems,
 
 // b[n] = sum over the node's incidences (e*k + a ascending) of contrib[e - e_lo, a],
 // starting from 0.0 -- exactly np.add.at's accumulation order (montecarlo.py:146).
+#ifndef TT_REDUCE_BATCH
+#define TT_REDUCE_BATCH 8
+#endif
 __global__ void reduce_nodes_kernel(int64_t n_nodes, int k, const int64_t* __restrict__ inc_start,
                                     const int32_t* __restrict__ inc, int64_t e_lo, int64_t e_hi,
                                     const double* __restrict__ contrib, double* __restrict__ b) {
+    constexpr int B = TT_REDUCE_BATCH;
     int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (n >= n_nodes) return;
     double s = 0.0;
     const int64_t q1 = inc_start[n + 1];
-    // 8 incidences per trip: all index loads, then all (independent) contribution gathers,
-    // then the adds in ascending order -- the np.add.at order, with 8 gathers in flight
-    for (int64_t q = inc_start[n]; q < q1; q += 8) {
-        int64_t src[8];
+    // B incidences per trip: all index loads, then all (independent) contribution gathers,
+    // then the adds in ascending order -- the np.add.at order, with B gathers in flight
+    for (int64_t q = inc_start[n]; q < q1; q += B) {
+        int64_t src[B];
 #pragma unroll
-        for (int t = 0; t < 8; ++t) {
+        for (int t = 0; t < B; ++t) {
             src[t] = -1;
             if (q + t < q1) {
                 const int64_t ea = __ldg(inc + q + t);
@@ -720,11 +724,11 @@ __global__ void reduce_nodes_kernel(int64_t n_nodes, int k, const int64_t* __res
                 if (e >= e_lo && e < e_hi) src[t] = (e - e_lo) * k + (ea - e * k);
             }
         }
-        double v[8];
+        double v[B];
 #pragma unroll
-        for (int t = 0; t < 8; ++t) v[t] = src[t] >= 0 ? __ldg(contrib + src[t]) : 0.0;
+        for (int t = 0; t < B; ++t) v[t] = src[t] >= 0 ? __ldg(contrib + src[t]) : 0.0;
 #pragma unroll
-        for (int t = 0; t < 8; ++t)
+        for (int t = 0; t < B; ++t)
             if (src[t] >= 0) s = add(s, v[t]);
     }
     b[n] = s;
