@@ -350,13 +350,19 @@ class DistributedPCG:
         spmv, all-reduce) x n, captured on first use -- every pointer and all iteration
         scalars live in persistent device buffers, so the graph serves every solve;
         host-staged backends run them eagerly."""
-        if self.comm.staged:
+        if self.comm.staged or self._graph is False:
             return self._iterations(n)
         if self._graph is None:
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                self._iterations(n)
-            self._graph = (g, n)
+            try:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    self._iterations(n)
+                self._graph = (g, n)
+            except Exception:
+                # (a collective that cannot be captured: eager iterations from now on; the
+                # device state is untouched, nothing ran during the failed capture)
+                self._graph = False
+                return self._iterations(n)
         g, gn = self._graph
         for _ in range(-(-n // gn)):
             g.replay()
@@ -542,6 +548,8 @@ class DistributedCoupling:
         if (self.rank, self.world) != (self.comm.rank, self.comm.world) and self.comm.world > 1:
             raise ValueError("rank/world disagree with the process group")
         self.target = target
+        if self.world > target.n_elems:
+            raise ValueError(f"{self.world} ranks for {target.n_elems} target elements")
         self.part = Partition(target, self.world, partition)
         p = self.plan = self.part.rank_plan(self.rank)
         self.sub = target.submesh(p.own_elems)
