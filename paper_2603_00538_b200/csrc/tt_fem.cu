@@ -777,6 +777,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) pcg_pipe_kernel(PipeArgs a) {
     double gamma_old = 0.0, alpha = 0.0;
     int xc = 0, xbi = 0;  // current / best iterate buffers (settle_iterates)
     for (int64_t it = 0;; ++it) {
+        PCG_MARK(it, 0);
         // ---- x_it's residual test (it >= 1), scalars of this iteration
         const double g = tot[0], d = tot[1];
         if (it > 0) {
@@ -804,6 +805,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) pcg_pipe_kernel(PipeArgs a) {
         const int xw_i = xc == xbi ? 1 - xc : xc;
         double* xw = xw_i == 0 ? a.x : a.best_x;
         double pg = 0.0, pd = 0.0, pr = 0.0;
+        PCG_MARK(it, 1);
 #pragma unroll 1
         for (int64_t i0 = r_lo + (threadIdx.x / LPR & ~(RPW - 1)); i0 < r_lo + rpb; i0 += BLOCK / LPR) {
             const int64_t i = i0 + (group & (RPW - 1));
@@ -826,12 +828,16 @@ __global__ void __launch_bounds__(BLOCK, MINB) pcg_pipe_kernel(PipeArgs a) {
             }
         }
         xc = xw_i;
+        PCG_MARK(it, 2);
         double* partG = a.part + ((it + 1) & 1) * 3 * nb;
         double v[3] = {pg, pd, pr};
         block_sums<3>(v, sh);
         if (threadIdx.x == 0) { partG[blockIdx.x] = v[0]; partG[nb + blockIdx.x] = v[1]; partG[2 * nb + blockIdx.x] = v[2]; }
+        PCG_MARK(it, 3);
         grid.sync();
+        PCG_MARK(it, 4);
         grid_totals<3>(partG, sh, tot);
+        PCG_MARK(it, 5);
     }
     settle_iterates(a.x, a.best_x, xc, xbi, n, tid, nthreads);
     if (blockIdx.x == 0 && threadIdx.x == 0) {

@@ -1,4 +1,4 @@
-"""Per-iteration phase split of the ELL PCG from the instrumented build
+"""Per-iteration phase split of the textbook slab PCG (path="slab") from the instrumented build
 (TT_LIB_PATH=<lib built with -DTT_PCG_TRACE>): globaltimer marks of block 0."""
 import ctypes as C
 import sys
@@ -20,7 +20,7 @@ fs = tt.NodalField.from_function(src, tt.get_field("smooth", dim=3).fn)
 b = load_vector(tgt, tt.MeshBackedField(fs), tt.SamplePlan.build(64, "sobol", 0, dim=3))
 mass = tgt.device.mass
 for _ in range(3):
-    pcg_device(mass, b, tol=1e-12)
+    pcg_device(mass, b, tol=1e-12, path="slab")
 torch.cuda.synchronize()
 buf = (C.c_ulonglong * (64 * 6))()
 _lib.lib().tt_debug_pcg_trace(buf)
