@@ -98,13 +98,16 @@ def mesh_names(args):
     return f"cube n={n} kuhn jitter0.2 seed20", f"cube n={n} kuhn_mirror jitter0.2 seed10"
 
 
-def workload_config(args, world, coupling=None):
+def workload_config(args, world, n_nodes):
+    """The config object of the JSON line; both arms print the same one (``n_nodes`` = the
+    target's node count, which decides the N>1 PCG form under --solve auto)."""
+    from paper_2603_00538_b200.dist import resolve_solve
     tname, sname = mesh_names(args)
     part = "single GPU"
     if world > 1:
         part = (f"Morton-ordered target-element parts x{world}, owner-summed interface loads "
-                f"({'peer memory' if args.exchange == 'peer' else 'NCCL all-to-all'}), "
-                f"{coupling.solve_mode if coupling else args.solve} PCG")
+                f"({'peer memory' if args.exchange == 'peer' else args.backend.upper() + ' all-to-all'}), "
+                f"{resolve_solve(args.solve, world, n_nodes)} PCG")
     return {"workload": WORKLOADS[args.config],
             "target": tname, "source": sname,
             "field": ("sin(x)cos(y)+2" if args.config == "c1" else "sin(x)cos(y)cos(z)+2")
@@ -475,7 +478,7 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": hib, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (generated meshes, analytic field interpolated on the source)",
-            "config": workload_config(args, world, coupling),
+            "config": workload_config(args, world, tgt.n_nodes),
             "load_ms_per_step": load_ms, "pcg_iterations": int(r.iterations),
             # SURVEY 8(d)'s sample throughput S / t_load (load phase, slowest rank); `value`
             # is the stricter S / t_step with the PCG included (c5: ms per step)
@@ -633,7 +636,7 @@ def run_reference(args):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_config(args, world), "cpu_baseline": cpu,
+            "config": workload_config(args, world, len(tn)), "cpu_baseline": cpu,
             "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -675,7 +678,7 @@ def run_reference_real(args, world):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": workload_config(args, world), "cpu_baseline": cpu,
+            "data": "synthetic", "config": workload_config(args, world, tgt.n_nodes), "cpu_baseline": cpu,
             "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 

@@ -537,6 +537,15 @@ class PeerLoadExchange:
 
 
 # ------------------------------------------------------------------ the coupling step
+def resolve_solve(solve: str, world: int, n_nodes: int) -> str:
+    """The PCG form ``solve="auto"`` picks: row-partitioned (distributed) from 1M target nodes
+    on more than one rank, where the per-rank solve shrinks with the world; below that the
+    replicated solve, whose single-GPU kernel beats a partitioned iteration's collectives."""
+    if solve != "auto":
+        return solve
+    return "distributed" if (world > 1 and n_nodes >= 1_000_000) else "replicated"
+
+
 class DistributedCoupling:
     """Partitioned MC transfer step over the ranks of ``group`` (one GPU each)."""
 
@@ -566,8 +575,7 @@ class DistributedCoupling:
         all_own = [np.flatnonzero(owners == q) for q in range(self.world)]
         self.own_counts = [len(v) for v in all_own]
         self.gather_order = _dev_i64(np.concatenate(all_own))
-        if solve == "auto":
-            solve = "distributed" if (self.world > 1 and target.n_nodes >= 1_000_000) else "replicated"
+        solve = resolve_solve(solve, self.world, target.n_nodes)
         if solve not in ("distributed", "peer", "replicated"):
             raise ValueError(f"unknown solve mode {solve!r}")
         if exchange not in ("nccl", "peer"):

@@ -202,3 +202,14 @@ def test_peer_incidence_reproduces_add_at_order(world):
             for q in range(p.inc_start[i], p.inc_start[i + 1]):
                 s = s + bufs[rk[q]][ent[q]]
             assert s == ref[n]
+
+
+def test_resolve_solve_rule():
+    """solve="auto": the row-partitioned PCG from 1M target nodes on more than one rank, the
+    replicated one otherwise; explicit modes pass through (bench.py prints the resolved form in
+    both arms' config)."""
+    from paper_2603_00538_b200.dist import resolve_solve
+    assert resolve_solve("auto", 1, 10_000_000) == "replicated"
+    assert resolve_solve("auto", 8, 999_999) == "replicated"
+    assert resolve_solve("auto", 2, 1_000_000) == "distributed"
+    assert resolve_solve("peer", 1, 10) == "peer"
