@@ -109,7 +109,7 @@ int main(int argc, char** argv) {
     /* node incidence (target: load reduction + mass; source: walk neighbours) */
     int64_t *t_inc_s, *s_inc_s, *cur2;
     int32_t *t_inc, *s_inc;
-    CU(cudaMalloc((void**)&t_inc_s, 8 * (tnn + 1))); CU(cudaMalloc((void**)&t_inc, 12 * tne));
+    CU(cudaMalloc((void**)&t_inc_s, 8 * (tnn + 1))); CU(cudaMalloc((void**)&t_inc, 12 * tne + 16));
     CU(cudaMalloc((void**)&s_inc_s, 8 * (snn + 1))); CU(cudaMalloc((void**)&s_inc, 12 * sne));
     CU(cudaMalloc((void**)&cur2, 8 * (tnn > snn ? tnn : snn)));
     CK(tt_incidence_count(&T, t_inc_s, st)); CK(tt_incidence_fill(&T, t_inc_s, t_inc, cur2, st));

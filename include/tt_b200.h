@@ -255,6 +255,12 @@ int tt_mc_load(const tt_mesh_t* target, int64_t e_lo, int64_t e_hi, const tt_pla
                double* contrib /* (e_hi-e_lo, k) or NULL */,
                double* b /* (n_nodes) atomically accumulated when contrib == NULL */,
                int32_t* status, void* stream);
+/* tt_mc_load with the contribution buffer transposed when contrib_ld > 0:
+ * contrib[a*contrib_ld + (e - e_lo)] (contrib_ld >= e_hi - e_lo; the node gather's layout,
+ * tt_reduce_nodes_ld); contrib_ld = 0 is tt_mc_load's (e_hi - e_lo, k) row-major buffer. */
+int tt_mc_load_ld(const tt_mesh_t* target, int64_t e_lo, int64_t e_hi, const tt_plan_t* plan,
+                  const tt_source_t* src, double* contrib, int64_t contrib_ld, double* b,
+                  int32_t* status, void* stream);
 
 /* importance-weighted load (montecarlo.py:165-176): contrib[e, a] = sum_j f_j / (N p_ej) lambda_ja
  * with the caller's densities p (e_hi-e_lo, N) for a shared plan; p <= 0 sets
@@ -294,9 +300,19 @@ int tt_incidence_count(const tt_mesh_t* mesh, int64_t* inc_start /* (n_nodes+1) 
 int tt_incidence_fill(const tt_mesh_t* mesh, const int64_t* inc_start,
                       int32_t* inc /* (E*k) entries e*k+a, ascending per node */,
                       int64_t* cursor_scratch /* (n_nodes) */, void* stream);
+/* b[n] = sum of contrib[(e - e_lo)*k + a] over node n's incidences e*k + a with
+ * e_lo <= e < e_hi, in ascending order from 0.0 (np.add.at's order); k = 1, 3 or 4.  inc is
+ * read in aligned 16-byte chunks: it must be 16-byte aligned and readable to a multiple of 4
+ * entries. */
 int tt_reduce_nodes(int64_t n_nodes, int k, const int64_t* inc_start, const int32_t* inc,
                     int64_t e_lo, int64_t e_hi, const double* contrib, double* b,
                     void* stream);
+/* The same sum over a transposed contribution buffer (contrib_ld > 0, k = 3 or 4):
+ * contrib[a*contrib_ld + (e - e_lo)], the layout tt_mc_load_ld writes for it; contrib_ld = 0
+ * is tt_reduce_nodes. */
+int tt_reduce_nodes_ld(int64_t n_nodes, int k, const int64_t* inc_start, const int32_t* inc,
+                       int64_t e_lo, int64_t e_hi, const double* contrib, int64_t contrib_ld,
+                       double* b, void* stream);
 
 /* ---- P1 mass matrix (CSR, exactly symmetric) ---- */
 int tt_mass_pattern(const tt_mesh_t* mesh, const int64_t* inc_start, const int32_t* inc,

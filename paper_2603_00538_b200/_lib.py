@@ -122,6 +122,8 @@ _SIGNATURES = {
     "tt_eval_points": ([C.POINTER(tt_source_t), _P, _I64, _P, _P, _P], _I),
     "tt_mc_load": ([C.POINTER(tt_mesh_t), _I64, _I64, C.POINTER(tt_plan_t),
                     C.POINTER(tt_source_t), _P, _P, _P, _P], _I),
+    "tt_mc_load_ld": ([C.POINTER(tt_mesh_t), _I64, _I64, C.POINTER(tt_plan_t),
+                       C.POINTER(tt_source_t), _P, _I64, _P, _P, _P], _I),
     "tt_mc_load_density": ([C.POINTER(tt_mesh_t), _I64, _I64, C.POINTER(tt_plan_t),
                             C.POINTER(tt_source_t), _P, _P, _P, _P], _I),
     "tt_mc_cache_ids": ([C.POINTER(tt_mesh_t), _I64, _I64, C.POINTER(tt_plan_t),
@@ -135,6 +137,7 @@ _SIGNATURES = {
     "tt_incidence_count": ([C.POINTER(tt_mesh_t), _P, _P], _I),
     "tt_incidence_fill": ([C.POINTER(tt_mesh_t), _P, _P, _P, _P], _I),
     "tt_reduce_nodes": ([_I64, _I, _P, _P, _I64, _I64, _P, _P, _P], _I),
+    "tt_reduce_nodes_ld": ([_I64, _I, _P, _P, _I64, _I64, _P, _I64, _P, _P], _I),
     "tt_mass_pattern": ([C.POINTER(tt_mesh_t), _P, _P, _P, _P, _P], _I),
     "tt_mass_fill": ([C.POINTER(tt_mesh_t), _P, _P, C.POINTER(_D), _P, _P, _P, _P], _I),
     "tt_pcg_workspace_doubles": ([_I64], _I64),
@@ -229,6 +232,17 @@ def call_status(name: str, *args) -> int:
     if code != TT_ERR_CAPACITY:
         check(code, name)
     return code
+
+
+def contrib_ld(t) -> int:
+    """Layout of an (n, k) element-contribution tensor for the C ABI: 0 when row-major
+    (contiguous), ld when it is the transpose of a (k, ld) buffer (strides (1, ld), ld >= n)."""
+    n, k = t.shape
+    if t.is_contiguous():
+        return 0
+    if t.stride(0) == 1 and t.stride(1) >= n:
+        return int(t.stride(1))
+    raise ValueError(f"contribution tensor with strides {t.stride()}: need row-major or transposed")
 
 
 def ptr(t) -> C.c_void_p:

@@ -182,7 +182,7 @@ template <int D, int PLAN, int SRC, int G>
 __global__ void __launch_bounds__(256) mc_load_kernel(TargetDev t, int64_t e_lo, int64_t e_hi,
                                                       PlanDev plan, SrcDev src,
                                                       const __grid_constant__ tt_expr_t expr,
-                                                      double* __restrict__ contrib,
+                                                      double* __restrict__ contrib, int64_t cld,
                                                       double* __restrict__ b,
                                                       int32_t* __restrict__ status) {
     constexpr int K = D + 1;
@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(256) mc_load_kernel(TargetDev t, int64_t e_lo,
             const double q = src.density ? 1.0 : (double)N * (1.0 / __ldg(t.measure + e));
             if (contrib) {
 #pragma unroll
-                for (int i = 0; i < K; ++i) contrib[le * K + i] = acc[i] / q;
+                for (int i = 0; i < K; ++i) contrib[cld ? i * cld + le : le * K + i] = acc[i] / q;
             } else {
 #pragma unroll
                 for (int i = 0; i < K; ++i) atomicAdd(b + __ldg(t.elems + e * K + i), acc[i] / q);
@@ -336,7 +336,7 @@ constexpr int kMcMinBlocks = TT_MC_MINB;
 template <int D, int PLAN, int G, bool SLOT, bool DEFER>
 __global__ void __launch_bounds__(kMcBlock, kMcMinBlocks) mc_mesh_kernel(TargetDev t, int64_t e_lo, int64_t e_hi,
                                                       PlanDev plan, SrcDev src,
-                                                      double* __restrict__ contrib,
+                                                      double* __restrict__ contrib, int64_t cld,
                                                       double* __restrict__ b,
                                                       int32_t* __restrict__ ids_out,
                                                       int32_t* __restrict__ status) {
@@ -584,7 +584,7 @@ __global__ void __launch_bounds__(kMcBlock, kMcMinBlocks) mc_mesh_kernel(TargetD
             const double q = (double)N * (1.0 / __ldg(t.measure + e));
             if (contrib) {
 #pragma unroll
-                for (int i = 0; i < K; ++i) contrib[le * K + i] = acc[i] / q;
+                for (int i = 0; i < K; ++i) contrib[cld ? i * cld + le : le * K + i] = acc[i] / q;
             } else if (b) {
 #pragma unroll
                 for (int i = 0; i < K; ++i) atomicAdd(b + __ldg(t.elems + e * K + i), acc[i] / q);
@@ -700,35 +700,45 @@ __global__ void pack_grad_kernel(int64_t E, const int32_t* __restrict__ elems,
 
 // b[n] = sum over the node's incidences (e*k + a ascending) of contrib[e - e_lo, a],
 // starting from 0.0 -- exactly np.add.at's accumulation order (montecarlo.py:146).
-#ifndef TT_REDUCE_BATCH
-#define TT_REDUCE_BATCH 8
-#endif
-__global__ void reduce_nodes_kernel(int64_t n_nodes, int k, const int64_t* __restrict__ inc_start,
+// Entry q = e*k + a is in the element range iff e_lo*k <= q < e_hi*k.  Row-major contrib
+// (LD = false) is then read at q - e_lo*k; the transposed layout (LD: contrib[a*ld + e - e_lo],
+// what the fused kernel writes for the node gather) at a*ld + e - e_lo -- there the gathers of
+// a warp's consecutive nodes, which take the same vertex slot of elements a few ids apart on
+// structured meshes, share lines (0.41 lines per gather at C2 instead of 1.0).  Index loads are
+// 16-byte aligned int4 chunks covering the node's incidence range (two chunks = 8 positions per
+// trip, out-of-range ones masked): 2 LDG.128 instead of 8 LDG.32 per trip; then the trip's (up
+// to 8) independent contribution gathers, then the adds in ascending order.
+template <int K, bool LD>
+__global__ void reduce_nodes_kernel(int64_t n_nodes, const int64_t* __restrict__ inc_start,
                                     const int32_t* __restrict__ inc, int64_t e_lo, int64_t e_hi,
-                                    const double* __restrict__ contrib, double* __restrict__ b) {
-    constexpr int B = TT_REDUCE_BATCH;
+                                    int64_t ld, const double* __restrict__ contrib, double* __restrict__ b) {
     int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (n >= n_nodes) return;
+    const int64_t lo_k = e_lo * K, hi_k = e_hi * K;
     double s = 0.0;
-    const int64_t q1 = inc_start[n + 1];
-    // B incidences per trip: all index loads, then all (independent) contribution gathers,
-    // then the adds in ascending order -- the np.add.at order, with B gathers in flight
-    for (int64_t q = inc_start[n]; q < q1; q += B) {
-        int64_t src[B];
+    const int64_t q0 = __ldg(inc_start + n), q1 = __ldg(inc_start + n + 1);
+    for (int64_t c = q0 & ~int64_t(3); c < q1; c += 8) {
+        const int4 u = __ldg(reinterpret_cast<const int4*>(inc + c));
+        const int4 w = c + 4 < q1 ? __ldg(reinterpret_cast<const int4*>(inc + c + 4)) : make_int4(0, 0, 0, 0);
+        const int ea[8] = {u.x, u.y, u.z, u.w, w.x, w.y, w.z, w.w};
+        int64_t src[8];
 #pragma unroll
-        for (int t = 0; t < B; ++t) {
+        for (int t = 0; t < 8; ++t) {
             src[t] = -1;
-            if (q + t < q1) {
-                const int64_t ea = __ldg(inc + q + t);
-                const int64_t e = ea / k;
-                if (e >= e_lo && e < e_hi) src[t] = (e - e_lo) * k + (ea - e * k);
+            if (c + t >= q0 && c + t < q1 && ea[t] >= lo_k && ea[t] < hi_k) {
+                if constexpr (LD) {
+                    const int e = ea[t] / K;            // constant divisor
+                    src[t] = (int64_t)(ea[t] - e * K) * ld + (e - e_lo);
+                } else {
+                    src[t] = ea[t] - lo_k;
+                }
             }
         }
-        double v[B];
+        double v[8];
 #pragma unroll
-        for (int t = 0; t < B; ++t) v[t] = src[t] >= 0 ? __ldg(contrib + src[t]) : 0.0;
+        for (int t = 0; t < 8; ++t) v[t] = src[t] >= 0 ? __ldg(contrib + src[t]) : 0.0;
 #pragma unroll
-        for (int t = 0; t < B; ++t)
+        for (int t = 0; t < 8; ++t)
             if (src[t] >= 0) s = add(s, v[t]);
     }
     b[n] = s;
@@ -802,7 +812,7 @@ static int lanes_per_element(int src_kind, int64_t N) {
 // same kernel instance, so cached ids are exactly the ids every load walks to).
 template <int D, int PLAN, int G>
 static int launch_mesh(const TargetDev& td, int64_t e_lo, int64_t e_hi, const PlanDev& pd,
-                       const SrcDev& sd, bool defer, double* contrib, double* b, int32_t* ids,
+                       const SrcDev& sd, bool defer, double* contrib, int64_t cld, double* b, int32_t* ids,
                        int32_t* status, cudaStream_t st) {
     constexpr int EPW = 32 / G;
     const int64_t tiles = (e_hi - e_lo + EPW - 1) / EPW;
@@ -819,7 +829,7 @@ static int launch_mesh(const TargetDev& td, int64_t e_lo, int64_t e_hi, const Pl
         int64_t nb = (tiles + kWarps - 1) / kWarps;
         const int64_t cap = (int64_t)sm_count() * per * waves;
         nb = nb > cap ? cap : nb < 1 ? 1 : nb;
-        kernel<<<(unsigned)nb, kMcBlock, smem, st>>>(td, e_lo, e_hi, pd, sd, contrib, b, ids, status);
+        kernel<<<(unsigned)nb, kMcBlock, smem, st>>>(td, e_lo, e_hi, pd, sd, contrib, cld, b, ids, status);
     };
     // DEFER costs registers (C2: 1.12 -> 1.22 ms), so only pairs known to snap run it
     if constexpr (PLAN == TT_PLAN_SHARED) {
@@ -836,14 +846,14 @@ static int launch_mesh(const TargetDev& td, int64_t e_lo, int64_t e_hi, const Pl
 
 template <int D, int PLAN, int SRC, int G>
 static int launch_mc(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_plan_t* p,
-                     const tt_source_t* s, double* contrib, double* b, int32_t* ids,
+                     const tt_source_t* s, double* contrib, int64_t cld, double* b, int32_t* ids,
                      int32_t* status, cudaStream_t st) {
     TargetDev td{t->nodes, t->elems, t->measure, t->gid};
     PlanDev pd{p->n_samples, p->lam, p->seed};
     SrcDev sd = to_src(*s);
     if constexpr (SRC == TT_SRC_MESH) {
         return launch_mesh<D, PLAN, G>(td, e_lo, e_hi, pd, sd, (s->hints & TT_HINT_DEFER_SNAP) != 0,
-                                       contrib, b, ids, status, st);
+                                       contrib, cld, b, ids, status, st);
     } else {
         constexpr int EPW = 32 / G;
         const int64_t tiles = (e_hi - e_lo + EPW - 1) / EPW;
@@ -852,33 +862,33 @@ static int launch_mc(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_pl
         const int64_t cap = (int64_t)sm_count() * per * 16;
         blocks = blocks > cap ? cap : blocks < 1 ? 1 : blocks;
         mc_load_kernel<D, PLAN, SRC, G><<<(unsigned)blocks, 256, 0, st>>>(td, e_lo, e_hi, pd, sd,
-                                                                          s->expr, contrib, b, status);
+                                                                          s->expr, contrib, cld, b, status);
         return launch_check("mc_load_kernel");
     }
 }
 
 template <int D, int PLAN, int SRC>
 static int dispatch_g(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_plan_t* p,
-                      const tt_source_t* s, double* contrib, double* b, int32_t* ids,
+                      const tt_source_t* s, double* contrib, int64_t cld, double* b, int32_t* ids,
                       int32_t* status, cudaStream_t st) {
     const int G = lanes_per_element(SRC, p->n_samples);
     if constexpr (SRC == TT_SRC_MESH)
-        if (G == 2) return launch_mc<D, PLAN, SRC, 2>(t, e_lo, e_hi, p, s, contrib, b, ids, status, st);
-    if (G == 4) return launch_mc<D, PLAN, SRC, 4>(t, e_lo, e_hi, p, s, contrib, b, ids, status, st);
-    if (G == 8) return launch_mc<D, PLAN, SRC, 8>(t, e_lo, e_hi, p, s, contrib, b, ids, status, st);
-    if (G == 16) return launch_mc<D, PLAN, SRC, 16>(t, e_lo, e_hi, p, s, contrib, b, ids, status, st);
-    return launch_mc<D, PLAN, SRC, 32>(t, e_lo, e_hi, p, s, contrib, b, ids, status, st);
+        if (G == 2) return launch_mc<D, PLAN, SRC, 2>(t, e_lo, e_hi, p, s, contrib, cld, b, ids, status, st);
+    if (G == 4) return launch_mc<D, PLAN, SRC, 4>(t, e_lo, e_hi, p, s, contrib, cld, b, ids, status, st);
+    if (G == 8) return launch_mc<D, PLAN, SRC, 8>(t, e_lo, e_hi, p, s, contrib, cld, b, ids, status, st);
+    if (G == 16) return launch_mc<D, PLAN, SRC, 16>(t, e_lo, e_hi, p, s, contrib, cld, b, ids, status, st);
+    return launch_mc<D, PLAN, SRC, 32>(t, e_lo, e_hi, p, s, contrib, cld, b, ids, status, st);
 }
 
 template <int D, int PLAN>
 static int dispatch_src(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_plan_t* p,
-                        const tt_source_t* s, double* contrib, double* b, int32_t* ids,
+                        const tt_source_t* s, double* contrib, int64_t cld, double* b, int32_t* ids,
                         int32_t* status, cudaStream_t st) {
     switch (s->kind) {
-        case TT_SRC_EXPR: return dispatch_g<D, PLAN, TT_SRC_EXPR>(t, e_lo, e_hi, p, s, contrib, b, ids, status, st);
-        case TT_SRC_MESH: return dispatch_g<D, PLAN, TT_SRC_MESH>(t, e_lo, e_hi, p, s, contrib, b, ids, status, st);
-        case TT_SRC_VALUES: return dispatch_g<D, PLAN, TT_SRC_VALUES>(t, e_lo, e_hi, p, s, contrib, b, ids, status, st);
-        case TT_SRC_CACHED: return dispatch_g<D, PLAN, TT_SRC_CACHED>(t, e_lo, e_hi, p, s, contrib, b, ids, status, st);
+        case TT_SRC_EXPR: return dispatch_g<D, PLAN, TT_SRC_EXPR>(t, e_lo, e_hi, p, s, contrib, cld, b, ids, status, st);
+        case TT_SRC_MESH: return dispatch_g<D, PLAN, TT_SRC_MESH>(t, e_lo, e_hi, p, s, contrib, cld, b, ids, status, st);
+        case TT_SRC_VALUES: return dispatch_g<D, PLAN, TT_SRC_VALUES>(t, e_lo, e_hi, p, s, contrib, cld, b, ids, status, st);
+        case TT_SRC_CACHED: return dispatch_g<D, PLAN, TT_SRC_CACHED>(t, e_lo, e_hi, p, s, contrib, cld, b, ids, status, st);
     }
     set_error("tt_mc_load: unknown source kind %d", s->kind);
     return TT_ERR_INVALID_PARAMETER;
@@ -886,10 +896,10 @@ static int dispatch_src(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt
 
 template <int D>
 static int dispatch_plan(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_plan_t* p,
-                         const tt_source_t* s, double* contrib, double* b, int32_t* ids,
+                         const tt_source_t* s, double* contrib, int64_t cld, double* b, int32_t* ids,
                          int32_t* status, cudaStream_t st) {
-    if (p->kind == TT_PLAN_SHARED) return dispatch_src<D, TT_PLAN_SHARED>(t, e_lo, e_hi, p, s, contrib, b, ids, status, st);
-    if (p->kind == TT_PLAN_PHILOX) return dispatch_src<D, TT_PLAN_PHILOX>(t, e_lo, e_hi, p, s, contrib, b, ids, status, st);
+    if (p->kind == TT_PLAN_SHARED) return dispatch_src<D, TT_PLAN_SHARED>(t, e_lo, e_hi, p, s, contrib, cld, b, ids, status, st);
+    if (p->kind == TT_PLAN_PHILOX) return dispatch_src<D, TT_PLAN_PHILOX>(t, e_lo, e_hi, p, s, contrib, cld, b, ids, status, st);
     set_error("tt_mc_load: unknown plan kind %d", p->kind);
     return TT_ERR_INVALID_PARAMETER;
 }
@@ -928,9 +938,9 @@ static int check_source(const tt_source_t* s, int dim) {
 
 using namespace tt;
 
-extern "C" int tt_mc_load(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_plan_t* p,
-                          const tt_source_t* s, double* contrib, double* b, int32_t* status,
-                          void* stream) {
+extern "C" int tt_mc_load_ld(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_plan_t* p,
+                             const tt_source_t* s, double* contrib, int64_t contrib_ld, double* b,
+                             int32_t* status, void* stream) {
     if (!t || !p || (t->dim != 2 && t->dim != 3) || p->dim != t->dim) {
         set_error("tt_mc_load: target/plan dimension mismatch");
         return TT_ERR_DIMENSION_MISMATCH;
@@ -943,6 +953,10 @@ extern "C" int tt_mc_load(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const 
         set_error("tt_mc_load: shared plan without lambda table");
         return TT_ERR_INVALID_PARAMETER;
     }
+    if (contrib_ld != 0 && contrib_ld < e_hi - e_lo) {
+        set_error("tt_mc_load_ld: contrib_ld smaller than the element range");
+        return TT_ERR_INVALID_PARAMETER;
+    }
     if (!contrib && !b) {
         set_error("tt_mc_load: need contrib or b output");
         return TT_ERR_INVALID_PARAMETER;
@@ -950,8 +964,14 @@ extern "C" int tt_mc_load(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const 
     int st = check_source(s, t->dim);
     if (st) return st;
     if (e_hi == e_lo) return TT_OK;
-    if (t->dim == 2) return dispatch_plan<2>(t, e_lo, e_hi, p, s, contrib, b, nullptr, status, as_stream(stream));
-    return dispatch_plan<3>(t, e_lo, e_hi, p, s, contrib, b, nullptr, status, as_stream(stream));
+    if (t->dim == 2) return dispatch_plan<2>(t, e_lo, e_hi, p, s, contrib, contrib_ld, b, nullptr, status, as_stream(stream));
+    return dispatch_plan<3>(t, e_lo, e_hi, p, s, contrib, contrib_ld, b, nullptr, status, as_stream(stream));
+}
+
+extern "C" int tt_mc_load(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_plan_t* p,
+                          const tt_source_t* s, double* contrib, double* b, int32_t* status,
+                          void* stream) {
+    return tt_mc_load_ld(t, e_lo, e_hi, p, s, contrib, 0, b, status, stream);
 }
 
 // Importance-weighted load (montecarlo.py:165-176): the simple sample loop (mc_load_kernel)
@@ -971,7 +991,7 @@ static int launch_density(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const 
     const int64_t cap = (int64_t)sm_count() * per * 16;
     blocks = blocks > cap ? cap : blocks < 1 ? 1 : blocks;
     mc_load_kernel<D, TT_PLAN_SHARED, SRC, G><<<(unsigned)blocks, 256, 0, st>>>(td, e_lo, e_hi, pd, sd, s->expr,
-                                                                               contrib, nullptr, status);
+                                                                               contrib, 0, nullptr, status);
     return launch_check("mc_load_kernel (density)");
 }
 
@@ -1033,8 +1053,8 @@ extern "C" int tt_mc_cache_ids(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, c
     s.dim = t->dim;
     s.grid = *g;
     s.seeds = seeds;
-    if (t->dim == 2) return dispatch_plan<2>(t, e_lo, e_hi, p, &s, nullptr, nullptr, ids, nullptr, as_stream(stream));
-    return dispatch_plan<3>(t, e_lo, e_hi, p, &s, nullptr, nullptr, ids, nullptr, as_stream(stream));
+    if (t->dim == 2) return dispatch_plan<2>(t, e_lo, e_hi, p, &s, nullptr, 0, nullptr, ids, nullptr, as_stream(stream));
+    return dispatch_plan<3>(t, e_lo, e_hi, p, &s, nullptr, 0, nullptr, ids, nullptr, as_stream(stream));
 }
 
 extern "C" int tt_map_points(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_plan_t* p,
@@ -1127,13 +1147,39 @@ extern "C" int tt_incidence_fill(const tt_mesh_t* m, const int64_t* inc_start, i
     return launch_check("incidence fill/sort");
 }
 
+extern "C" int tt_reduce_nodes_ld(int64_t n_nodes, int k, const int64_t* inc_start, const int32_t* inc,
+                                  int64_t e_lo, int64_t e_hi, const double* contrib, int64_t contrib_ld,
+                                  double* b, void* stream) {
+    if (n_nodes == 0) return TT_OK;
+    if ((k != 1 && k != 3 && k != 4) || e_lo < 0 || contrib_ld < 0 || (k == 1 && contrib_ld)) {
+        set_error("tt_reduce_nodes: k must be 1 (row-major only), 3 or 4; e_lo and contrib_ld >= 0");
+        return TT_ERR_INVALID_PARAMETER;
+    }
+    // the int4 index loads read whole 16-byte chunks around a node's range (up to 3 entries
+    // past the last one): inc must be 16-byte aligned and readable to a multiple of 4 entries
+    if ((reinterpret_cast<uintptr_t>(inc) & 15) != 0) {
+        set_error("tt_reduce_nodes: inc must be 16-byte aligned");
+        return TT_ERR_INVALID_PARAMETER;
+    }
+    const int64_t hi = e_hi > (int64_t)INT32_MAX ? (int64_t)INT32_MAX : e_hi;   // entries are int32
+    auto s = as_stream(stream);
+    const unsigned grid = grid_for(n_nodes, 256);
+    if (k == 1) {
+        reduce_nodes_kernel<1, false><<<grid, 256, 0, s>>>(n_nodes, inc_start, inc, e_lo, hi, 0, contrib, b);
+    } else if (k == 3) {
+        if (contrib_ld) reduce_nodes_kernel<3, true><<<grid, 256, 0, s>>>(n_nodes, inc_start, inc, e_lo, hi, contrib_ld, contrib, b);
+        else reduce_nodes_kernel<3, false><<<grid, 256, 0, s>>>(n_nodes, inc_start, inc, e_lo, hi, 0, contrib, b);
+    } else {
+        if (contrib_ld) reduce_nodes_kernel<4, true><<<grid, 256, 0, s>>>(n_nodes, inc_start, inc, e_lo, hi, contrib_ld, contrib, b);
+        else reduce_nodes_kernel<4, false><<<grid, 256, 0, s>>>(n_nodes, inc_start, inc, e_lo, hi, 0, contrib, b);
+    }
+    return launch_check("reduce_nodes_kernel");
+}
+
 extern "C" int tt_reduce_nodes(int64_t n_nodes, int k, const int64_t* inc_start, const int32_t* inc,
                                int64_t e_lo, int64_t e_hi, const double* contrib, double* b,
                                void* stream) {
-    if (n_nodes == 0) return TT_OK;
-    reduce_nodes_kernel<<<grid_for(n_nodes, 256), 256, 0, as_stream(stream)>>>(
-        n_nodes, k, inc_start, inc, e_lo, e_hi, contrib, b);
-    return launch_check("reduce_nodes_kernel");
+    return tt_reduce_nodes_ld(n_nodes, k, inc_start, inc, e_lo, e_hi, contrib, 0, b, stream);
 }
 
 extern "C" int tt_pack_coeffs(const tt_mesh_t* m, const double* coeffs, double* out, void* stream) {

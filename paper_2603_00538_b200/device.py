@@ -21,6 +21,16 @@ import torch
 from . import _lib
 
 
+def padded_i32(host=None, n: int | None = None) -> torch.Tensor:
+    """(n,) int32 device tensor whose storage is padded to a multiple of 4 entries (the
+    node gather reads incidence lists in aligned int4 chunks); from ``host`` if given."""
+    n = len(host) if host is not None else n
+    buf = torch.zeros(max((n + 3) // 4 * 4, 4), dtype=torch.int32, device=_lib.device())
+    if host is not None and n:
+        buf[:n].copy_(torch.as_tensor(host))
+    return buf[:n]
+
+
 class DeviceMesh:
     def __init__(self, mesh):
         self.mesh = mesh
@@ -51,7 +61,7 @@ class DeviceMesh:
         """(inc_start (n+1,) i64, inc (E*k,) i32): node -> element-vertex entries."""
         dev = self.nodes.device
         inc_start = torch.empty(self.n_nodes + 1, dtype=torch.int64, device=dev)
-        inc = torch.empty(self.n_elems * self.k, dtype=torch.int32, device=dev)
+        inc = padded_i32(None, self.n_elems * self.k)
         cursor = torch.empty(max(self.n_nodes, 1), dtype=torch.int64, device=dev)
         desc = self.desc()
         s = _lib.stream_handle()
@@ -62,13 +72,15 @@ class DeviceMesh:
 
     def reduce_nodes(self, contrib: torch.Tensor, e_lo: int = 0, e_hi: int | None = None,
                      out: torch.Tensor | None = None) -> torch.Tensor:
-        """b[n] = sum of contrib over the node's incidences in ascending (e, a) order."""
+        """b[n] = sum of contrib over the node's incidences in ascending (e, a) order
+        (montecarlo.py:144-147); contrib row-major or transposed (element_contributions)."""
         e_hi = self.n_elems if e_hi is None else e_hi
         inc_start, inc = self.incidence
         b = out if out is not None else torch.empty(self.n_nodes, dtype=torch.float64,
                                                     device=self.nodes.device)
-        _lib.call("tt_reduce_nodes", self.n_nodes, self.k, _lib.ptr(inc_start), _lib.ptr(inc),
-                  e_lo, e_hi, _lib.ptr(contrib), _lib.ptr(b), _lib.stream_handle())
+        _lib.call("tt_reduce_nodes_ld", self.n_nodes, self.k, _lib.ptr(inc_start), _lib.ptr(inc),
+                  e_lo, e_hi, _lib.ptr(contrib), _lib.contrib_ld(contrib), _lib.ptr(b),
+                  _lib.stream_handle())
         return b
 
     @cached_property

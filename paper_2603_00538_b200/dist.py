@@ -267,6 +267,13 @@ def _dev_i64(a) -> torch.Tensor:
     return torch.as_tensor(np.ascontiguousarray(a, dtype=np.int64), device=_lib.device())
 
 
+def _dev_inc(a) -> torch.Tensor:
+    """An incidence list for tt_reduce_nodes on the device: 16-byte aligned, its storage
+    padded to a multiple of 4 entries (the kernel reads whole int4 chunks)."""
+    from .device import padded_i32
+    return padded_i32(np.ascontiguousarray(a, dtype=np.int32))
+
+
 # ------------------------------------------------------------------ distributed PCG
 # tt_dist.cu DStates: two DState slots of 88 bytes (6 doubles, 2 int64, then int32 done, ...)
 _DONE_INT32 = (16, 16 + 22)
@@ -569,7 +576,7 @@ class DistributedCoupling:
         self.send_rows = _dev_i64(p.send_rows)
         self.send_buf = torch.zeros((max(len(p.send_rows), 1), k), dtype=torch.float64, device=dev)
         self.inc_start = _dev_i64(p.inc_start)
-        self.inc = torch.as_tensor(p.inc, device=dev)
+        self.inc = _dev_inc(p.inc)
         self.own_nodes = _dev_i64(p.own_nodes)
         owners = self.part.node_owner
         all_own = [np.flatnonzero(owners == q) for q in range(self.world)]
@@ -732,7 +739,7 @@ class DistributedMCOperator:
         rank_all = np.concatenate([np.full(len(v), i, np.int64) for i, v in enumerate(lists_node)])
         loc = np.searchsorted(p.own_nodes, node_all)
         order = np.lexsort((rank_all, loc))
-        self.inc = torch.as_tensor(src_all[order].astype(np.int32), device=_lib.device())
+        self.inc = _dev_inc(src_all[order])
         start = np.zeros(n_on + 1, np.int64)
         np.cumsum(np.bincount(loc, minlength=n_on), out=start[1:])
         self.inc_start = _dev_i64(start)

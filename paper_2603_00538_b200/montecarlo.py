@@ -312,21 +312,24 @@ def element_contributions(target, source, plan: SamplePlan, e_lo: int = 0,
                           e_hi: int | None = None, out: torch.Tensor | None = None,
                           status: torch.Tensor | None = None) -> torch.Tensor:
     """contrib (e_hi-e_lo, k): sum_j f(x_j) psi_a(x_j) / (N p), p = 1/|T|
-    (montecarlo.py:110-132).  Data-dependent errors are OR-ed into ``status``."""
+    (montecarlo.py:110-132).  Data-dependent errors are OR-ed into ``status``.  The returned
+    tensor is the transpose of a (k, e_hi-e_lo) buffer (the node gather reads a vertex slot of
+    neighbouring elements from one line); ``out`` may be row-major or such a transpose."""
     if plan.dim != target.DIM:
         raise DimensionMismatch(f"{plan.dim}-D plan on a {target.DIM}-D mesh")
     e_hi = target.n_elems if e_hi is None else e_hi
     dm = target.device
     k = target.DIM + 1
-    contrib = out if out is not None else torch.empty((e_hi - e_lo, k), dtype=torch.float64,
-                                                      device=dm.nodes.device)
+    contrib = out if out is not None else torch.empty((k, e_hi - e_lo), dtype=torch.float64,
+                                                      device=dm.nodes.device).t()
+    ld = _lib.contrib_ld(contrib)
     status = status if status is not None else _lib.status_word()
     sdesc, keep = _source_desc(source, target.DIM, target)
     mdesc, pdesc = dm.desc(), plan.desc()
     s = _lib.stream_handle()
     if sdesc is not None:
-        _lib.call("tt_mc_load", C.byref(mdesc), e_lo, e_hi, C.byref(pdesc), C.byref(sdesc),
-                  _lib.ptr(contrib), None, _lib.ptr(status), s)
+        _lib.call("tt_mc_load_ld", C.byref(mdesc), e_lo, e_hi, C.byref(pdesc), C.byref(sdesc),
+                  _lib.ptr(contrib), ld, None, _lib.ptr(status), s)
         return contrib
     # host black box: materialise points per chunk, query, accumulate the values
     chunk = max(1, _HOST_CHUNK_POINTS // plan.n_samples)
@@ -342,8 +345,8 @@ def element_contributions(target, source, plan: SamplePlan, e_lo: int = 0,
         vd.kind = _lib.TT_SRC_VALUES
         vd.dim = target.DIM
         vd.values = _lib.ptr(vals).value
-        _lib.call("tt_mc_load", C.byref(mdesc), c0, c1, C.byref(pdesc), C.byref(vd),
-                  _lib.ptr(contrib[c0 - e_lo:]), None, _lib.ptr(status), s)
+        _lib.call("tt_mc_load_ld", C.byref(mdesc), c0, c1, C.byref(pdesc), C.byref(vd),
+                  _lib.ptr(contrib[c0 - e_lo:]), ld, None, _lib.ptr(status), s)
         del vals
     return contrib
 

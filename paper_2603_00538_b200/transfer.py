@@ -111,11 +111,12 @@ class MCTransferOperator:
         s.coeffs = _lib.ptr(source_field.coeffs_dev).value
         s.cached_ids = _lib.ptr(self.src_elem_dev).value
         s.elem_coeffs = _lib.ptr(source_field.elem_coeffs()).value
-        contrib = torch.empty((self.target.n_elems, k), dtype=torch.float64, device=dm.nodes.device)
+        E = self.target.n_elems
+        contrib = torch.empty((k, E), dtype=torch.float64, device=dm.nodes.device).t()
         status = status if status is not None else _lib.status_word()
         mdesc, pdesc = dm.desc(), self.plan.desc()
-        _lib.call("tt_mc_load", C.byref(mdesc), 0, self.target.n_elems, C.byref(pdesc), C.byref(s),
-                  _lib.ptr(contrib), None, _lib.ptr(status), _lib.stream_handle())
+        _lib.call("tt_mc_load_ld", C.byref(mdesc), 0, E, C.byref(pdesc), C.byref(s),
+                  _lib.ptr(contrib), E, None, _lib.ptr(status), _lib.stream_handle())
         b = dm.reduce_nodes(contrib)
         if check:
             _raise_status(int(status.item()))
