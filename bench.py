@@ -487,7 +487,9 @@ def run_ours(args):
                                             "load (source pack + fused MC kernel + node gather), max over ranks")},
             "e2e": e2e,
             "roofline": {"bound": "hbm",
-                         "kernel": "spmv_rect (folded R @ c)" if c5 else "mc_mesh_kernel<3,SHARED,G,SLOT>",
+                         "kernel": ("spmv_rect (folded R @ c)" if c5 else
+                                    f"mc_mesh_kernel<{tgt.DIM},{'PHILOX' if args.mode == 'philox' else 'SHARED'},G,"
+                                    f"{'SLOT' if args.mode != 'philox' else 'NOSLOT'}>"),
                          "achieved": achieved, "peak": peak_hbm, "unit": "GB/s",
                          "frac": achieved / peak_hbm, "peak_source": peak_src,
                          "traffic": traffic, "kernel_ms": k_ms, "algorithmic_bytes": alg_bytes,

@@ -105,6 +105,38 @@ def test_deterministic_reduction_matches_add_at_order(tt):
     assert np.array_equal(b, ref)
 
 
+@pytest.mark.parametrize("dim", [2, 3])
+def test_node_gather_layouts_and_ranges(tt, dim):
+    """tt_reduce_nodes (row-major contributions) and tt_reduce_nodes_ld (the transposed buffer
+    the fused kernel writes): bit-identical to np.add.at over the whole mesh and over element
+    ranges (the partition meshes' form), on a shuffled element order (irregular incidence
+    lists, ranges not aligned to the int4 index chunks); element_contributions returns the
+    transposed layout and fills a row-major ``out`` the same."""
+    import torch
+    from paper_2603_00538_b200.montecarlo import element_contributions
+    m = tt.generate_square_mesh(13, 0.2, seed=2) if dim == 2 else tt.generate_cube_mesh(5, 0.2, seed=2)
+    perm = np.random.default_rng(dim).permutation(m.n_elems)
+    m = (tt.TriMesh if dim == 2 else tt.TetMesh).from_arrays(m.nodes, m.elements[perm])
+    dm = m.device
+    rng = np.random.default_rng(7)
+    c = rng.standard_normal((m.n_elems, dim + 1)) * 10.0 ** rng.integers(-6, 6, (m.n_elems, 1))
+    row = torch.as_tensor(c, device="cuda")
+    tr = row.t().contiguous().t()
+    assert not tr.is_contiguous()
+    for lo, hi in ((0, m.n_elems), (3, m.n_elems), (0, m.n_elems - 5), (7, 7 + m.n_elems // 3)):
+        ref = np.zeros(m.n_nodes)
+        np.add.at(ref, m.elements[lo:hi], c[lo:hi])
+        for t in (row, tr):
+            assert np.array_equal(dm.reduce_nodes(t[lo:hi], lo, hi).cpu().numpy(), ref), (lo, hi, t.stride())
+    plan = tt.SamplePlan.build(16, "sobol", 0, dim=dim)
+    f = tt.AnalyticField(tt.get_field("smooth", dim=dim).fn)
+    a = element_contributions(m, f, plan)
+    assert a.stride() == (1, m.n_elems)
+    out = torch.empty((m.n_elems, dim + 1), dtype=torch.float64, device="cuda")
+    element_contributions(m, f, plan, out=out)
+    assert torch.equal(a, out)
+
+
 @pytest.mark.parametrize("n", [1, 2, 5, 33, 600])
 def test_pcg_small_systems_all_paths(tt, n):
     """Tiny SPD systems through the slab, L2-ELL and CSR PCGs (block ranges with no rows,
