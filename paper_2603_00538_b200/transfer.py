@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import ctypes as C
 
+import numpy as np
 import torch
 
 from . import _lib
@@ -161,6 +162,11 @@ class CouplingStep:
         self.c_dev = torch.zeros(source_mesh.n_nodes, dtype=torch.float64, device=dev)
         self.x_host = torch.zeros(target.n_nodes, dtype=torch.float64).pin_memory()
         self.flags_host = torch.zeros(8, dtype=torch.float64).pin_memory()   # result (4) + status
+        # host views of the pinned result words, read after the step's one synchronisation
+        flags_np = self.flags_host.numpy()
+        self._res_view = _lib.tt_pcg_result_t.from_buffer(flags_np)
+        self._status_view = flags_np[4:5].view(np.int32)
+        self._x_np = self.x_host.numpy()
         self.field = NodalField(source_mesh, self.c_dev)
         self.source = MeshBackedField(self.field, source_locator, outside)
         self.status = _lib.status_word()
@@ -204,9 +210,8 @@ class CouplingStep:
             self._body()
         torch.cuda.current_stream().synchronize()
         x, best_x, res = self._out
-        raw = self.flags_host.numpy().tobytes()
-        r = _lib.tt_pcg_result_t.from_buffer_copy(raw[:C.sizeof(_lib.tt_pcg_result_t)])
-        flags = int(self.flags_host[4:5].view(torch.int32)[0])
+        r = self._res_view
+        flags = int(self._status_view[0])
         if flags:
             _raise_status(flags)
         if r.zero_rhs:
@@ -214,6 +219,6 @@ class CouplingStep:
         if not r.converged:
             from .errors import NoConvergence
             raise NoConvergence(best_x.cpu().numpy(), float(r.best_residual), int(r.iterations))
-        field = NodalField(self.target, x)
-        field._host = self.x_host.numpy()
+        field = NodalField.__new__(NodalField)     # (x is already a device f64 vector)
+        field.mesh, field.coeffs_dev, field._host = self.target, x, self._x_np
         return field
