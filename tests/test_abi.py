@@ -76,3 +76,20 @@ def test_no_device_raises_loudly():
         pytest.skip("a GPU is present")
     with pytest.raises(DeviceUnavailable):
         _lib.lib()
+
+
+def test_contrib_ld_layouts():
+    """The C ABI's contribution layout argument: 0 for a row-major (n, k) tensor (including
+    empty and one-row tensors), ld for the transpose of a (k, ld) buffer and its row slices;
+    anything else is refused."""
+    import pytest
+    import torch
+    from paper_2603_00538_b200._lib import contrib_ld
+    for n in (0, 1, 2, 7):
+        assert contrib_ld(torch.empty((n, 4), dtype=torch.float64)) == 0
+        t = torch.empty((4, n), dtype=torch.float64).t()
+        assert contrib_ld(t) in ((0,) if n <= 1 else (n,))
+    t = torch.empty((3, 10), dtype=torch.float64).t()
+    assert contrib_ld(t[4:]) == 10 and contrib_ld(t[4:]) >= t[4:].shape[0]
+    with pytest.raises(ValueError):
+        contrib_ld(torch.empty((10, 8), dtype=torch.float64)[:, ::2])
