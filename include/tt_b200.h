@@ -178,8 +178,9 @@ typedef struct tt_source {
                                  elements per target element (tt_seed_elements), or NULL */
     const double*  elem_coeffs;/* TT_SRC_MESH/CACHED optional (E_s, 4) per-element vertex
                                  coefficients (tt_pack_coeffs); replaces src_elems+coeffs */
-    const double*  elem_grad;  /* TT_SRC_MESH optional (E_s, 4): gradient g (dim) and the value at
-                                 the origin vertex (tt_pack_grad): f = c_last + g.(x - o) */
+    const double*  elem_grad;  /* TT_SRC_MESH (E_s, 4): gradient g (dim) and the value at the
+                                 origin vertex (tt_pack_grad): f = c_last + g.(x - o); required
+                                 when seeds and grid.wrec are set (TT_ERR_INVALID_PARAMETER) */
 } tt_source_t;
 
 typedef struct tt_pcg_result {

@@ -961,6 +961,11 @@ extern "C" int tt_mc_load_ld(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, con
         set_error("tt_mc_load: need contrib or b output");
         return TT_ERR_INVALID_PARAMETER;
     }
+    if (s && s->kind == TT_SRC_MESH && s->grid.walk && s->grid.wrec && s->seeds && !s->elem_grad) {
+        // the compact walk's certified hits evaluate f from the gradient records
+        set_error("tt_mc_load: a walk source (seeds + grid.wrec) needs elem_grad (tt_pack_grad)");
+        return TT_ERR_INVALID_PARAMETER;
+    }
     int st = check_source(s, t->dim);
     if (st) return st;
     if (e_hi == e_lo) return TT_OK;

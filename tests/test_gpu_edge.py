@@ -181,3 +181,24 @@ def test_gradient_records_match_numpy(tt, dim):
     np.testing.assert_array_equal(rec[:, dim], c[:, dim])
     if dim == 2:
         assert np.all(rec[:, 3] == 0.0)
+
+
+def test_walk_source_without_gradient_records_is_refused(tt):
+    """A C-ABI mesh source set up for the compact walk (seeds + walk records) but without
+    the gradient records its certified hits evaluate f from is refused with
+    TT_ERR_INVALID_PARAMETER instead of loading f = 0."""
+    import ctypes as C
+    import torch
+    from paper_2603_00538_b200 import _lib
+    tgt = tt.generate_cube_mesh(3, 0.2, seed=20)
+    src = tt.generate_cube_mesh(4, 0.2, seed=10, split="kuhn_mirror")
+    fs = tt.NodalField.from_function(src, tt.get_field("smooth", dim=3).fn)
+    box = tt.MeshBackedField(fs, tt.UniformGridLocator.build(src))
+    s = box.desc(3, tgt)
+    assert s.seeds and s.grid.wrec and s.elem_grad
+    s.elem_grad = None
+    plan = tt.SamplePlan.build(16, "sobol", 0, dim=3)
+    contrib = torch.empty((tgt.n_elems, 4), dtype=torch.float64, device="cuda")
+    rc = _lib.lib().tt_mc_load(C.byref(tgt.device.desc()), 0, tgt.n_elems, C.byref(plan.desc()), C.byref(s),
+                               _lib.ptr(contrib), None, _lib.ptr(_lib.status_word()), _lib.stream_handle())
+    assert rc == _lib.TT_ERR_INVALID_PARAMETER
