@@ -683,9 +683,14 @@ __device__ __forceinline__ double slab_row_col(const uint4* __restrict__ ch, int
     return s0 + s1;
 }
 
+// One lane per row: the lane sums its row's 8-column chunks in order (the recurrence's
+// own-row updates then keep every lane busy; 2 lanes per row, where one lane idles through
+// the updates: C2 solve 0.222 vs 0.213 ms)
 template <int BLOCK, int MINB, int W, bool SLAB>
 __global__ void __launch_bounds__(BLOCK, MINB) pcg_pipe_kernel(PipeArgs a) {
-    constexpr int LPR = W / 8;
+    constexpr int CPR = W / 8;     // 8-column chunks per row
+    constexpr int LPR = 1;         // lanes per row
+    constexpr int CPL = CPR / LPR; // chunks per lane
     constexpr int RPW = 32 / LPR;  // rows per warp
     cg::grid_group grid = cg::this_grid();
     __shared__ double sh[3 * 32];
@@ -702,9 +707,9 @@ __global__ void __launch_bounds__(BLOCK, MINB) pcg_pipe_kernel(PipeArgs a) {
     const int sub = threadIdx.x & (LPR - 1);
     if constexpr (SLAB) {
         const int64_t lo = min(n, r_lo), hi = min(n, lo + min(rpb, a.slab_rows));
-        for (int64_t q = threadIdx.x; q < (hi - lo) * LPR; q += BLOCK) {
-            const int64_t i = lo + q / LPR;
-            const int sb = (int)(q % LPR);
+        for (int64_t q = threadIdx.x; q < (hi - lo) * CPR; q += BLOCK) {
+            const int64_t i = lo + q / CPR;
+            const int sb = (int)(q % CPR);
             const int4* cq = reinterpret_cast<const int4*>(a.ec + i * W) + 2 * sb;
             const int4 c0 = __ldg(cq), c1 = __ldg(cq + 1);
             const uint4* vq = reinterpret_cast<const uint4*>(a.ev + i * W + 8 * sb);
@@ -723,9 +728,13 @@ __global__ void __launch_bounds__(BLOCK, MINB) pcg_pipe_kernel(PipeArgs a) {
         if (i < r_end) {
             const int64_t li = i - r_lo;
             if (SLAB && li < a.slab_rows) {
-                acc = slab_row_col(slab + (li * LPR + sub) * 5, i, v);
+                acc = slab_row_col(slab + (li * CPR + sub * CPL) * 5, i, v);
+#pragma unroll
+                for (int c = 1; c < CPL; ++c) acc += slab_row_col(slab + (li * CPR + sub * CPL + c) * 5, i, v);
             } else {
-                acc = ell_row8<W>(a.ec, a.ev, i, sub, [&](int c) { return v[c]; });
+                acc = ell_row8<W>(a.ec, a.ev, i, sub * CPL, [&](int c) { return v[c]; });
+#pragma unroll
+                for (int c = 1; c < CPL; ++c) acc += ell_row8<W>(a.ec, a.ev, i, sub * CPL + c, [&](int cc) { return v[cc]; });
             }
         }
 #pragma unroll
