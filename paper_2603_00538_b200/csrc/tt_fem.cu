@@ -1178,7 +1178,7 @@ extern "C" int tt_pcg_ell_slab_pipelined(int64_t n, int width, const int32_t* el
     if (!pipe_args(a, n, width, ell_cols, ell_vals, diag, b, tol, maxiter, x, best_x, work, result,
                    "tt_pcg_ell_slab_pipelined"))
         return TT_ERR_INVALID_PARAMETER;
-    const int lpr = width / 8;  // lanes per row = 80-byte chunks per row
+    const int cpr = width / 8;  // 80-byte slab chunks per row
     const void* fn = width == 8 ? (const void*)pcg_pipe_kernel<kPB, kPM, 8, true>
                                 : (const void*)pcg_pipe_kernel<kPB, kPM, 16, true>;
     int dev = 0, max_optin = 0;
@@ -1193,11 +1193,12 @@ extern "C" int tt_pcg_ell_slab_pipelined(int64_t n, int width, const int32_t* el
     // 2 blocks per SM (the 2 x 512 shape of tt_pcg_ell), else 1 with twice the rows.  With
     // 2 per SM the block count and row ranges are tt_pcg_ell's, so the partial sums -- and
     // the iterates -- are bitwise the same
-    const int64_t need = (n * lpr + kPB - 1) / kPB;
+    // blocks of at least kPB / 2 rows (one lane per row), at most one wave
+    const int64_t need = (2 * n + kPB - 1) / kPB;
     for (int bps = kPM; bps >= 1; --bps) {
         const int64_t nb = need < (int64_t)sms * bps ? need : (int64_t)sms * bps;
         const int64_t rpb = (n + nb - 1) / nb;
-        const int64_t per_row = 80 * lpr;
+        const int64_t per_row = 80 * cpr;
         // per-SM shared memory: 228 KB less 1 KB per block reserved, less the static part
         const int64_t avail = (int64_t)(bps > 1 ? (228 * 1024) / bps - 1024 : max_optin) - (int64_t)sizeof(double) * 96 - 16;
         const int64_t cap = avail / per_row;
