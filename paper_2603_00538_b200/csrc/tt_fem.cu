@@ -1190,10 +1190,8 @@ extern "C" int tt_pcg_ell_slab_pipelined(int64_t n, int width, const int32_t* el
     // solve, slab vs L2 kernel: 59 % on chip (357,911 rows) 0.565 vs 0.691 ms; 40 %
     // (531,441) 1.20 vs 1.04; 28 % (753,571) 1.83 vs 1.25; C1 (2-D, 85 %) 0.36 vs 0.43
     constexpr double min_frac = 0.5;
-    // 2 blocks per SM (the 2 x 512 shape of tt_pcg_ell), else 1 with twice the rows.  With
-    // 2 per SM the block count and row ranges are tt_pcg_ell's, so the partial sums -- and
-    // the iterates -- are bitwise the same
-    // blocks of at least kPB / 2 rows (one lane per row), at most one wave
+    // kPM blocks per SM (one 512-thread block: the recurrence needs ~128 registers), blocks of
+    // at least kPB / 2 rows (one lane per row), at most one wave
     const int64_t need = (2 * n + kPB - 1) / kPB;
     for (int bps = kPM; bps >= 1; --bps) {
         const int64_t nb = need < (int64_t)sms * bps ? need : (int64_t)sms * bps;
