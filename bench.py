@@ -390,8 +390,10 @@ def run_ours(args):
     x_host = torch.empty(tgt.n_nodes, dtype=torch.float64).pin_memory()
     c_dev = torch.empty(src.n_nodes, dtype=torch.float64, device="cuda")
 
-    graph_step = tt.CouplingStep(tgt, src, plan, cg_tol=1e-12, source_locator=loc) \
-        if coupling is None and not c5 else None
+    graph_step = None
+    if coupling is None:
+        graph_step = tt.CouplingStep(tgt, src, plan, cg_tol=1e-12, source_locator=loc,
+                                     operator=operator(plan) if c5 else None)
 
     def e2e_api(use_graph):
         def run():
@@ -467,8 +469,10 @@ def run_ours(args):
             e2e = {"value": S / (e2e_ms * 1e-3), "unit": "samples/s"}
         e2e.update({"ms_per_step": e2e_ms, "h2d_bytes_per_step": src.n_nodes * 8,
                     "d2h_bytes_per_step": tgt.n_nodes * 8,
-                    "api": ("CouplingStep(c_pinned).coeffs (H2D + one CUDA-graph replay of pack, load, "
-                            "gather, PCG, D2H)" if e2e_graph_ms is not None and e2e_graph_ms <= e2e_plain_ms else
+                    "api": (("CouplingStep(c_pinned, operator=MCTransferOperator).coeffs (H2D + one CUDA-graph "
+                             "replay of R @ c, PCG, D2H)" if c5 else
+                             "CouplingStep(c_pinned).coeffs (H2D + one CUDA-graph replay of pack, load, "
+                             "gather, PCG, D2H)") if e2e_graph_ms is not None and e2e_graph_ms <= e2e_plain_ms else
                             "NodalField(pinned H2D) -> transfer_mc(MeshBackedField, out=pinned x).coeffs | "
                             "MCTransferOperator.apply(field, out=pinned x).coeffs (c5) | "
                             "DistributedCoupling.step / DistributedMCOperator.apply + x D2H (N>1)"),

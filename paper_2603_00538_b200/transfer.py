@@ -144,7 +144,9 @@ class CouplingStep:
     source coefficients, then ONE CUDA-graph replay of gradient pack -> fused MC load ->
     ordered node gather -> PCG -> D2H of the solution (extension for coupling loops; each call is the
     reference's ``transfer_mc(target, MeshBackedField(NodalField(source, c)), plan)``,
-    transfer.py:158-163, with the same results and errors).
+    transfer.py:158-163, with the same results and errors).  Given ``operator=`` (an
+    ``MCTransferOperator`` of the same triple), each call is ``operator.apply`` instead: the
+    folded R @ c -> PCG -> D2H in one replay.
 
     ``step(coeffs)`` takes the source nodal coefficients (host array or tensor) and returns
     the target ``NodalField`` whose ``.coeffs`` is a host array.  The graph is captured on
@@ -153,11 +155,18 @@ class CouplingStep:
     """
 
     def __init__(self, target, source_mesh, plan: SamplePlan, cg_tol: float = 1e-12,
-                 source_locator: UniformGridLocator | None = None, outside: str = "snap"):
+                 source_locator: UniformGridLocator | None = None, outside: str = "snap",
+                 operator: "MCTransferOperator | None" = None):
         from .montecarlo import MeshBackedField
         if target.DIM != source_mesh.DIM or plan.dim != target.DIM:
             raise DimensionMismatch("target, source mesh and plan dimensions differ")
+        if operator is not None and (operator.target is not target or operator.source_mesh is not source_mesh
+                                     or operator.plan.n_samples != plan.n_samples):
+            raise DimensionMismatch("the operator was built for another (target, source mesh, plan)")
         self.target, self.source_mesh, self.plan, self.cg_tol = target, source_mesh, plan, cg_tol
+        # with an MCTransferOperator the step is its apply (cached localisation: R @ c + PCG,
+        # transfer.py:112-115) instead of a full load
+        self.operator = operator
         dev = _lib.device()
         self.c_dev = torch.zeros(source_mesh.n_nodes, dtype=torch.float64, device=dev)
         self.x_host = torch.zeros(target.n_nodes, dtype=torch.float64).pin_memory()
@@ -177,7 +186,10 @@ class CouplingStep:
         from .montecarlo import load_vector
         self.status.zero_()
         self.field._grad = self.field._packed = None    # new coefficients: repack in the step
-        b = load_vector(self.target, self.source, self.plan, check=False, status=self.status)
+        if self.operator is not None:
+            b = self.operator.load(self.field, check=False, status=self.status)
+        else:
+            b = load_vector(self.target, self.source, self.plan, check=False, status=self.status)
         x, best_x, res = pcg_device(self.mass, b, tol=self.cg_tol)
         self.x_host.copy_(x, non_blocking=True)
         self.flags_host[:4].copy_(res, non_blocking=True)

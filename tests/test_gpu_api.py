@@ -317,3 +317,21 @@ def test_coupling_step_graph_matches_transfer_mc(tt):
     with pytest.raises(tt.SourceEvalFailed):
         step(bad)
     assert np.array_equal(step(c).coeffs, ref)     # the step object is reusable after an error
+
+
+def test_coupling_step_with_operator_matches_apply(tt):
+    """CouplingStep(operator=MCTransferOperator): each call is the operator's apply (folded
+    R @ c + PCG) as one graph replay, bitwise equal to apply, step after step."""
+    tgt = tt.generate_cube_mesh(8, 0.2, seed=20)
+    src = tt.generate_cube_mesh(9, 0.2, seed=10, split="kuhn_mirror")
+    loc = tt.UniformGridLocator.build(src)
+    plan = tt.SamplePlan.build(20, "sobol", 0, dim=3)
+    op = tt.MCTransferOperator(tgt, src, plan, cg_tol=1e-13, source_locator=loc)
+    step = tt.CouplingStep(tgt, src, plan, cg_tol=1e-13, source_locator=loc, operator=op)
+    for k in range(3):
+        c = np.cos(src.nodes[:, 1] + k) + 2.0
+        got = step(c).coeffs.copy()
+        ref = op.apply(tt.NodalField(src, c)).coeffs
+        assert np.array_equal(got, ref), k
+    with pytest.raises(tt.DimensionMismatch):
+        tt.CouplingStep(tgt, src, tt.SamplePlan.build(21, "sobol", 0, dim=3), operator=op)
