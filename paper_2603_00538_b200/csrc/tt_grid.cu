@@ -196,12 +196,27 @@ __global__ void grid_fill_kernel(GridDev g, int64_t E, const double* __restrict_
             }
 }
 
-// ascending sort of each CSR segment (segments are short: ~6 (2-D) to ~25 (3-D) ids)
+// ascending sort of each CSR segment (segments are short: ~6 (2-D) to ~25 (3-D) ids).  A
+// segment of up to 64 ids is sorted in a thread-local buffer (L1-resident) instead of with
+// dependent global-memory round trips; longer ones in place.
 __global__ void segment_sort_kernel(int64_t nseg, const int64_t* __restrict__ start,
                                     int32_t* __restrict__ vals) {
     int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (s >= nseg) return;
-    int64_t a = start[s], b = start[s + 1];
+    const int64_t a = start[s], b = start[s + 1];
+    if (b - a <= 64) {
+        int32_t buf[64];
+        const int n = (int)(b - a);
+        for (int i = 0; i < n; ++i) buf[i] = vals[a + i];
+        for (int i = 1; i < n; ++i) {
+            const int32_t v = buf[i];
+            int j = i - 1;
+            while (j >= 0 && buf[j] > v) { buf[j + 1] = buf[j]; --j; }
+            buf[j + 1] = v;
+        }
+        for (int i = 0; i < n; ++i) vals[a + i] = buf[i];
+        return;
+    }
     for (int64_t i = a + 1; i < b; ++i) {
         int32_t v = vals[i];
         int64_t j = i - 1;
@@ -411,30 +426,42 @@ __global__ void walk_prep_kernel(int64_t E, const double* __restrict__ nodes,
 }
 
 // Walk seeds per target element: the source elements containing its kSeeds anchor points
-// (x = sum_a A[s][a] v_a; reference scan, snapped when outside).  Layout (E, kSeeds).
+// (x = sum_a A[s][a] v_a; reference scan, snapped when outside).  Layout (E, kSeeds).  One
+// thread per target element: the first anchor by the reference scan, the next ones -- a few
+// elements away -- by the certified walk from the previous anchor's element when the grid
+// has walk records (locate_walk returns exactly the scan's element and lambda, falling back to
+// the scan itself when uncertain), so 15 of the 16 scans become one or two record tests.
 template <int D>
 __global__ void seed_kernel(GridDev g, const double* __restrict__ nodes,
                             const int32_t* __restrict__ elems, int64_t e_lo, int64_t n_el,
                             int32_t* __restrict__ seeds, int32_t* __restrict__ status) {
     constexpr int K = D + 1;
-    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (t >= n_el * kSeeds) return;
-    const int64_t i = t / kSeeds;
-    const int which = (int)(t % kSeeds);
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n_el) return;
     const int64_t e = e_lo + i;
-    double x[D];
-    for (int c = 0; c < D; ++c) {
-        double s = mul(anchor<D>(which, 0), nodes[(int64_t)elems[e * K] * D + c]);
-        for (int a = 1; a < K; ++a) s = add(s, mul(anchor<D>(which, a), nodes[(int64_t)elems[e * K + a] * D + c]));
-        x[c] = s;
+    double v[K][D];
+    for (int a = 0; a < K; ++a)
+        for (int c = 0; c < D; ++c) v[a][c] = nodes[(int64_t)elems[e * K + a] * D + c];
+    int prev = -1;
+    bool snapped = false;
+#pragma unroll 1
+    for (int which = 0; which < kSeeds; ++which) {
+        double x[D];
+        for (int c = 0; c < D; ++c) {
+            double s = mul(anchor<D>(which, 0), v[0][c]);
+            for (int a = 1; a < K; ++a) s = add(s, mul(anchor<D>(which, a), v[a][c]));
+            x[c] = s;
+        }
+        double l[D + 1];
+        int es = (g.walk && prev >= 0) ? locate_walk<D>(g, x, 1e-12, prev, l) : locate_point<D>(g, x, 1e-12, l);
+        if (es < 0) {
+            es = nearest_element<D>(g, x);
+            snapped = true;
+        }
+        seeds[i * kSeeds + which] = es;
+        prev = es;
     }
-    double l[D + 1];
-    int es = locate_point<D>(g, x, 1e-12, l);
-    if (es < 0) {
-        es = nearest_element<D>(g, x);
-        if (status) atomicOr(status, TT_FLAG_SNAPPED);
-    }
-    seeds[t] = es;
+    if (snapped && status) atomicOr(status, TT_FLAG_SNAPPED);
 }
 
 static int64_t ncells_of(const tt_grid_t* g) {
@@ -652,8 +679,8 @@ extern "C" int tt_seed_elements(const tt_grid_t* g, const tt_mesh_t* t, int64_t 
     GridDev gd = to_dev(*g);
     auto s = as_stream(stream);
     if (g->dim == 2)
-        seed_kernel<2><<<grid_for((e_hi - e_lo) * kSeeds, 128), 128, 0, s>>>(gd, t->nodes, t->elems, e_lo, e_hi - e_lo, seeds, status);
+        seed_kernel<2><<<grid_for(e_hi - e_lo, 128), 128, 0, s>>>(gd, t->nodes, t->elems, e_lo, e_hi - e_lo, seeds, status);
     else
-        seed_kernel<3><<<grid_for((e_hi - e_lo) * kSeeds, 128), 128, 0, s>>>(gd, t->nodes, t->elems, e_lo, e_hi - e_lo, seeds, status);
+        seed_kernel<3><<<grid_for(e_hi - e_lo, 128), 128, 0, s>>>(gd, t->nodes, t->elems, e_lo, e_hi - e_lo, seeds, status);
     return launch_check("seed_kernel");
 }

@@ -765,6 +765,19 @@ __global__ void segment_sort_kernel2(int64_t nseg, const int64_t* __restrict__ s
     int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (s >= nseg) return;
     int64_t a = start[s], b = start[s + 1];
+    if (b - a <= 64) {  // (node incidences: ~23 in 3-D) sorted in a thread-local buffer
+        int32_t buf[64];
+        const int n = (int)(b - a);
+        for (int i = 0; i < n; ++i) buf[i] = vals[a + i];
+        for (int i = 1; i < n; ++i) {
+            const int32_t v = buf[i];
+            int j = i - 1;
+            while (j >= 0 && buf[j] > v) { buf[j + 1] = buf[j]; --j; }
+            buf[j + 1] = v;
+        }
+        for (int i = 0; i < n; ++i) vals[a + i] = buf[i];
+        return;
+    }
     for (int64_t i = a + 1; i < b; ++i) {
         int32_t v = vals[i];
         int64_t j = i - 1;

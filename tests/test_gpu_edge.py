@@ -202,3 +202,26 @@ def test_walk_source_without_gradient_records_is_refused(tt):
     rc = _lib.lib().tt_mc_load(C.byref(tgt.device.desc()), 0, tgt.n_elems, C.byref(plan.desc()), C.byref(s),
                                _lib.ptr(contrib), None, _lib.ptr(_lib.status_word()), _lib.stream_handle())
     assert rc == _lib.TT_ERR_INVALID_PARAMETER
+
+
+@pytest.mark.parametrize("pair", ["square", "cube", "torus"])
+def test_walk_seeds_equal_scan_seeds(tt, pair):
+    """tt_seed_elements walks from the previous anchor's element when the grid has walk
+    records: the seed table and the outside flag equal the reference-scan table (walk=False
+    locator) exactly, on matching, non-matching and curved (snapping) pairs."""
+    import torch
+    if pair == "square":
+        tgt, src = tt.generate_square_mesh(30, 0.2, seed=20), tt.generate_square_mesh(33, 0.2, seed=10)
+    elif pair == "cube":
+        tgt = tt.generate_cube_mesh(9, 0.2, seed=20)
+        src = tt.generate_cube_mesh(10, 0.2, seed=10, split="kuhn_mirror")
+    else:
+        tgt = tt.generate_torus_mesh(6, 12, 30, perturbation=0.2, seed=20)
+        src = tt.generate_torus_mesh(5, 14, 26, perturbation=0.2, seed=10, split="kuhn_mirror")
+    walk = tt.UniformGridLocator.build(src)
+    scan = tt.UniformGridLocator.build(src, walk=False)
+    assert walk.walk and not scan.walk
+    assert torch.equal(walk.seeds_for(tgt), scan.seeds_for(tgt))
+    assert walk.snap_prone(tgt) == scan.snap_prone(tgt)
+    if pair == "torus":
+        assert walk.snap_prone(tgt)
