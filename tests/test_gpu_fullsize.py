@@ -118,3 +118,57 @@ def test_full_size_folded_operator_vs_oracle():
     del op
     gc.collect()
     torch.cuda.empty_cache()
+
+
+def test_full_size_c1_against_the_reference_itself():
+    """C1 at full size (999,698-triangle pair, N = 64: 64.0 M samples) against the REFERENCE
+    itself (oracle/_ref: tritransfer with its compiled backend, built here from
+    /root/reference by oracle/build_ref.sh and shipped with the repo snapshot): every sample's
+    source element equals the reference's locate_many on the reference's own sample points
+    (montecarlo.py:123-124, _compiled.pyx:127-175), and b equals the reference's
+    assemble_load_mc to 1e-12."""
+    import os
+    import sys
+    from pathlib import Path
+    ref_dir = Path(__file__).resolve().parents[1] / "oracle" / "_ref"
+    if not (ref_dir / "tritransfer").is_dir():
+        pytest.skip("oracle/_ref (the reference build) is not present")
+    sys.path.insert(0, str(ref_dir))
+    import tritransfer as ref
+    from tritransfer.fem import NodalField as RNodalField
+    from tritransfer.montecarlo import MeshBackedField as RMeshBackedField, SamplePlan as RSamplePlan
+    from tritransfer.montecarlo import assemble_load_mc as r_assemble
+    import torch
+    import paper_2603_00538_b200 as tt
+    from paper_2603_00538_b200.montecarlo import sample_source_elements
+
+    rt = ref.generate_square_mesh(707, 0.2, seed=20, diagonal="right")
+    rs = ref.generate_square_mesh(707, 0.2, seed=10, diagonal="left")
+    tgt, src, N = _meshes(tt, "c1")
+    assert np.array_equal(rt.nodes, tgt.nodes) and np.array_equal(rt.elements, tgt.elements)
+    assert np.array_equal(rs.nodes, src.nodes) and np.array_equal(rs.elements, src.elements)
+    coeffs = np.sin(src.nodes[:, 0]) * np.cos(src.nodes[:, 1]) + 2.0
+    rplan = RSamplePlan.build(N, "sobol", 0)
+    plan = tt.SamplePlan.build(N, "sobol", 0)
+    assert np.array_equal(rplan.barycentric, plan.barycentric)
+    rbox = RMeshBackedField(RNodalField(rs, coeffs))
+    loc = tt.UniformGridLocator.build(src)
+    ids = sample_source_elements(tgt, loc, plan).cpu().numpy()
+    # the reference's own point map and locate, chunk by chunk
+    lam = rplan.barycentric
+    coords = rt.nodes[rt.elements]                               # (E, 3, 2)
+    chunk = 50_000
+    for e0 in range(0, rt.n_elems, chunk):
+        pts = np.einsum("nj,ejd->end", lam, coords[e0:e0 + chunk])
+        elem, _ = rbox.locator.locate_many(pts.reshape(-1, 2))
+        assert np.all(elem >= 0)                                  # C1 is a matching square pair
+        got = ids[e0:e0 + chunk].ravel()
+        bad = np.flatnonzero(got != elem)
+        assert len(bad) == 0, f"elements [{e0}, {e0 + chunk}): {len(bad)} ids differ"
+    del ids
+    b_ref = r_assemble(rt, rbox, rplan, workers=os.cpu_count() or 1)
+    b = tt.assemble_load_mc(tgt, tt.MeshBackedField(tt.NodalField(src, coeffs), loc), plan)
+    assert np.max(np.abs(b - b_ref)) / np.max(np.abs(b_ref)) <= 1e-12
+    del loc
+    gc.collect()
+    torch.cuda.empty_cache()
