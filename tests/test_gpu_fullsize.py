@@ -125,8 +125,8 @@ def test_full_size_c1_against_the_reference_itself():
     itself (oracle/_ref: tritransfer with its compiled backend, built here from
     /root/reference by oracle/build_ref.sh and shipped with the repo snapshot): every sample's
     source element equals the reference's locate_many on the reference's own sample points
-    (montecarlo.py:123-124, _compiled.pyx:127-175), and b equals the reference's
-    assemble_load_mc to 1e-12."""
+    (montecarlo.py:123-124, _compiled.pyx:127-175), b equals the reference's assemble_load_mc
+    and x its transfer_mc (cg_tol 1e-14 on both sides) to 1e-12."""
     import os
     import sys
     from pathlib import Path
@@ -167,8 +167,14 @@ def test_full_size_c1_against_the_reference_itself():
         assert len(bad) == 0, f"elements [{e0}, {e0 + chunk}): {len(bad)} ids differ"
     del ids
     b_ref = r_assemble(rt, rbox, rplan, workers=os.cpu_count() or 1)
-    b = tt.assemble_load_mc(tgt, tt.MeshBackedField(tt.NodalField(src, coeffs), loc), plan)
+    box = tt.MeshBackedField(tt.NodalField(src, coeffs), loc)
+    b = tt.assemble_load_mc(tgt, box, plan)
     assert np.max(np.abs(b - b_ref)) / np.max(np.abs(b_ref)) <= 1e-12
-    del loc
+    # and the transferred field (transfer.py:158-163) at cg_tol 1e-14 on both sides
+    from tritransfer.transfer import transfer_mc as r_transfer
+    x_ref = r_transfer(rt, rbox, rplan, cg_tol=1e-14, workers=os.cpu_count() or 1).coeffs
+    x = tt.transfer_mc(tgt, box, plan, cg_tol=1e-14).coeffs
+    assert np.max(np.abs(x - x_ref)) / np.max(np.abs(x_ref)) <= 1e-12
+    del loc, box
     gc.collect()
     torch.cuda.empty_cache()
