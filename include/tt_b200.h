@@ -155,6 +155,11 @@ typedef struct tt_plan {
     int64_t  n_samples;       /* N samples per element */
     const double* lam;        /* SHARED: (N, dim+1) barycentric table */
     uint64_t seed;            /* PHILOX: key */
+    const int32_t* order;     /* SHARED, optional (NULL: plan order): the order in which the fused
+                                 mesh kernel takes an element's samples, with lam_walk = lam in
+                                 that order (tt_plan_walk_order); ids are reported in plan order,
+                                 loads differ only in the summation order */
+    const double* lam_walk;
 } tt_plan_t;
 
 typedef struct tt_expr {
@@ -251,6 +256,11 @@ int tt_map_points(const tt_mesh_t* target, int64_t e_lo, int64_t e_hi, const tt_
                   double* points /* (e_hi-e_lo, N, dim) */, void* stream);
 int tt_eval_points(const tt_source_t* src, const double* points, int64_t count,
                    double* values, int32_t* status, void* stream);
+/* order[N] = the shared plan's sample indices grouped by nearest walk anchor (stable) and
+ * lam_walk (N, dim+1) = lam in that order, so a lane group of the fused kernel starts its walks
+ * from the same seed element (1 <= N <= 4096) */
+int tt_plan_walk_order(int dim, int64_t n_samples, const double* lam, int32_t* order, double* lam_walk,
+                       void* stream);
 int tt_mc_load(const tt_mesh_t* target, int64_t e_lo, int64_t e_hi, const tt_plan_t* plan,
                const tt_source_t* src,
                double* contrib /* (e_hi-e_lo, k) or NULL */,

@@ -61,7 +61,8 @@ class tt_grid_t(C.Structure):
 
 class tt_plan_t(C.Structure):
     _fields_ = [("kind", C.c_int32), ("dim", C.c_int32), ("n_samples", C.c_int64),
-                ("lam", C.c_void_p), ("seed", C.c_uint64)]
+                ("lam", C.c_void_p), ("seed", C.c_uint64), ("order", C.c_void_p),
+                ("lam_walk", C.c_void_p)]
 
 
 class tt_expr_t(C.Structure):
@@ -120,6 +121,7 @@ _SIGNATURES = {
     "tt_snap": ([C.POINTER(tt_grid_t), _P, _I64, _P, _P, _P], _I),
     "tt_map_points": ([C.POINTER(tt_mesh_t), _I64, _I64, C.POINTER(tt_plan_t), _P, _P], _I),
     "tt_eval_points": ([C.POINTER(tt_source_t), _P, _I64, _P, _P, _P], _I),
+    "tt_plan_walk_order": ([_I, _I64, _P, _P, _P, _P], _I),
     "tt_mc_load": ([C.POINTER(tt_mesh_t), _I64, _I64, C.POINTER(tt_plan_t),
                     C.POINTER(tt_source_t), _P, _P, _P, _P], _I),
     "tt_mc_load_ld": ([C.POINTER(tt_mesh_t), _I64, _I64, C.POINTER(tt_plan_t),

@@ -165,6 +165,9 @@ struct PlanDev {
     int64_t n;
     const double* __restrict__ lam;
     uint64_t seed;
+    const int32_t* __restrict__ order;  // fused SLOT kernel: lam is the plan's table in this
+                                        // order (lam_walk); ids are written back at order[j]
+    const double* __restrict__ lam_walk;
 };
 
 template <int D>
@@ -357,6 +360,9 @@ __global__ void __launch_bounds__(kMcBlock, kMcMinBlocks) mc_mesh_kernel(TargetD
     const bool walk = g.walk && src.seeds && g.wrec;
     int flags = 0;
     constexpr bool USE_SLOT = SLOT && PLAN == TT_PLAN_SHARED;
+    // SLOT: each sample's nearest walk anchor.  With plan.order the launch passes the plan's
+    // table in that order (tt_plan_walk_order: grouped by nearest anchor, so a group's lanes
+    // start their walks from the same seed element); sample j here is plan sample order[j]
     extern __shared__ int8_t s_slot[];  // N bytes (launch: dynamic shared memory)
     if constexpr (USE_SLOT) {
         for (int64_t j = threadIdx.x; j < N; j += kMcBlock) {
@@ -537,7 +543,7 @@ __global__ void __launch_bounds__(kMcBlock, kMcMinBlocks) mc_mesh_kernel(TargetD
             if (done) {
                 TT_STAT(2, 1);
                 if (!fw_hit) TT_STAT(4, 1);
-                if (ids_out) ids_out[le * N + jcur] = hit;
+                if (ids_out) ids_out[le * N + (plan.order ? plan.order[jcur] : jcur)] = hit;
                 double f = 0.0;
                 if (fw_hit) f = fw_f;
                 else if (hit >= 0 && (contrib || b)) f = p1_eval<D>(src, hit, l);
@@ -833,6 +839,10 @@ static int launch_mesh(const TargetDev& td, int64_t e_lo, int64_t e_hi, const Pl
     // better than 16 waves at C2, N = 64); 32-lane groups (N >= 512) keep 16 waves (+1 %)
     const int waves = G >= 32 ? 16 : 1;
     const bool slot = PLAN == TT_PLAN_SHARED && pd.n <= kSlotCap;
+    // the walk order (tt_plan_walk_order) applies to the slot-table kernels only
+    PlanDev pw = pd;
+    if (!slot || !pd.order || !pd.lam_walk) pw.order = nullptr;
+    else pw.lam = pd.lam_walk;
     // dynamic shared memory = the seed-slot table (N bytes, SLOT kernels only): every byte
     // of shared memory is L1 the walk's records lose (+20 KB/block costs 0.056 ms at C2)
     const size_t smem = slot ? (size_t)((pd.n + 15) / 16 * 16) : 0;
@@ -842,7 +852,7 @@ static int launch_mesh(const TargetDev& td, int64_t e_lo, int64_t e_hi, const Pl
         int64_t nb = (tiles + kWarps - 1) / kWarps;
         const int64_t cap = (int64_t)sm_count() * per * waves;
         nb = nb > cap ? cap : nb < 1 ? 1 : nb;
-        kernel<<<(unsigned)nb, kMcBlock, smem, st>>>(td, e_lo, e_hi, pd, sd, contrib, cld, b, ids, status);
+        kernel<<<(unsigned)nb, kMcBlock, smem, st>>>(td, e_lo, e_hi, pw, sd, contrib, cld, b, ids, status);
     };
     // DEFER costs registers (C2: 1.12 -> 1.22 ms), so only pairs known to snap run it
     if constexpr (PLAN == TT_PLAN_SHARED) {
@@ -862,7 +872,7 @@ static int launch_mc(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_pl
                      const tt_source_t* s, double* contrib, int64_t cld, double* b, int32_t* ids,
                      int32_t* status, cudaStream_t st) {
     TargetDev td{t->nodes, t->elems, t->measure, t->gid};
-    PlanDev pd{p->n_samples, p->lam, p->seed};
+    PlanDev pd{p->n_samples, p->lam, p->seed, p->order, p->lam_walk};
     SrcDev sd = to_src(*s);
     if constexpr (SRC == TT_SRC_MESH) {
         return launch_mesh<D, PLAN, G>(td, e_lo, e_hi, pd, sd, (s->hints & TT_HINT_DEFER_SNAP) != 0,
@@ -986,6 +996,41 @@ extern "C" int tt_mc_load_ld(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, con
     return dispatch_plan<3>(t, e_lo, e_hi, p, s, contrib, contrib_ld, b, nullptr, status, as_stream(stream));
 }
 
+// One block: each sample's nearest walk anchor (the fused kernel's rule), then a stable
+// counting sort of the sample indices by anchor.
+template <int D>
+__global__ void walk_order_kernel(int64_t n, const double* __restrict__ lam, int32_t* __restrict__ order,
+                                  double* __restrict__ lam_walk) {
+    constexpr int K = D + 1;
+    __shared__ int8_t s_key[kSlotCap];
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+        double l[K];
+#pragma unroll
+        for (int a = 0; a < K; ++a) l[a] = lam[j * K + a];
+        s_key[j] = (int8_t)seed_slot_nearest<D>(l);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int start[kSeeds + 1] = {0};
+        for (int64_t j = 0; j < n; ++j) ++start[s_key[j] + 1];
+        for (int k = 0; k < kSeeds; ++k) start[k + 1] += start[k];
+        for (int64_t j = 0; j < n; ++j) order[start[s_key[j]]++] = (int32_t)j;
+    }
+    __syncthreads();
+    for (int64_t q = threadIdx.x; q < n * K; q += blockDim.x) lam_walk[q] = lam[(int64_t)order[q / K] * K + q % K];
+}
+
+extern "C" int tt_plan_walk_order(int dim, int64_t n_samples, const double* lam, int32_t* order,
+                                  double* lam_walk, void* stream) {
+    if ((dim != 2 && dim != 3) || n_samples < 1 || n_samples > kSlotCap || !lam || !order || !lam_walk) {
+        set_error("tt_plan_walk_order: dim 2/3, 1 <= n_samples <= %d, lam, order and lam_walk required", kSlotCap);
+        return TT_ERR_INVALID_PARAMETER;
+    }
+    if (dim == 2) walk_order_kernel<2><<<1, 256, 0, as_stream(stream)>>>(n_samples, lam, order, lam_walk);
+    else walk_order_kernel<3><<<1, 256, 0, as_stream(stream)>>>(n_samples, lam, order, lam_walk);
+    return launch_check("walk_order_kernel");
+}
+
 extern "C" int tt_mc_load(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const tt_plan_t* p,
                           const tt_source_t* s, double* contrib, double* b, int32_t* status,
                           void* stream) {
@@ -999,7 +1044,7 @@ static int launch_density(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, const 
                           const tt_source_t* s, const double* density, double* contrib,
                           int32_t* status, cudaStream_t st) {
     TargetDev td{t->nodes, t->elems, t->measure, t->gid};
-    PlanDev pd{p->n_samples, p->lam, p->seed};
+    PlanDev pd{p->n_samples, p->lam, p->seed, p->order, p->lam_walk};
     SrcDev sd = to_src(*s);
     sd.density = density;
     constexpr int EPW = 32 / G;
@@ -1084,7 +1129,7 @@ extern "C" int tt_map_points(const tt_mesh_t* t, int64_t e_lo, int64_t e_hi, con
     int64_t total = (e_hi - e_lo) * p->n_samples;
     if (total == 0) return TT_OK;
     TargetDev td{t->nodes, t->elems, t->measure, t->gid};
-    PlanDev pd{p->n_samples, p->lam, p->seed};
+    PlanDev pd{p->n_samples, p->lam, p->seed, p->order, p->lam_walk};
     auto s = as_stream(stream);
     if (t->dim == 2)
         map_points_kernel<2><<<grid_for(total, 256), 256, 0, s>>>(td, e_lo, e_hi - e_lo, p->kind, pd, pts);

@@ -261,7 +261,28 @@ class SamplePlan:
         else:
             p.kind = _lib.TT_PLAN_SHARED
             p.lam = _lib.ptr(self.barycentric_dev).value
+            wo = self.walk_order
+            if wo is not None:
+                p.order = _lib.ptr(wo[0]).value
+                p.lam_walk = _lib.ptr(wo[1]).value
         return p
+
+    @property
+    def walk_order(self):
+        """(order, the table in that order): the 3-D fused kernel's sample order
+        (tt_plan_walk_order: grouped by nearest walk anchor, so a lane group starts its walks
+        from the same seed element -- kernel C2 -1.9 %, C2 N = 256 -3.8 %, C3 -4.9 %, C4 -2 %;
+        the 2-D kernel runs 1.4 % slower with it and keeps the plan order), computed once per
+        plan; None for 2-D, per-element plans and beyond the slot-table size (4096)."""
+        if self.per_element or self.dim != 3 or self.n_samples > 4096:
+            return None
+        if getattr(self, "_walk_order", None) is None:
+            o = torch.empty(self.n_samples, dtype=torch.int32, device=self.barycentric_dev.device)
+            lw = torch.empty_like(self.barycentric_dev)
+            _lib.call("tt_plan_walk_order", self.dim, self.n_samples, _lib.ptr(self.barycentric_dev),
+                      _lib.ptr(o), _lib.ptr(lw), _lib.stream_handle())
+            self._walk_order = (o, lw)
+        return self._walk_order
 
 
 # -------------------------------------------------------------------- assembly
