@@ -241,7 +241,7 @@ int tt_grid_walk_prep(const tt_mesh_t* mesh, const int64_t* inc_start, const int
  * target element (reference scan, snapped when outside): s = 0 the centroid c, s = 1 + i the
  * point (v_i + c)/2, then 16 - (dim+2) k-means anchors (scripts/seed_anchors.py).  Walk
  * starts: a sample starts at its nearest anchor's element. */
-#define TT_SEED_ANCHORS 16
+#define TT_SEED_ANCHORS 48
 int tt_seed_elements(const tt_grid_t* grid, const tt_mesh_t* target, int64_t e_lo,
                      int64_t e_hi, int32_t* seeds, int32_t* status /* TT_FLAG_SNAPPED, or NULL */,
                      void* stream);

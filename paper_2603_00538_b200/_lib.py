@@ -23,7 +23,7 @@ TT_OK, TT_ERR_INVALID_PARAMETER, TT_ERR_DIMENSION_MISMATCH, TT_ERR_CUDA, TT_ERR_
 TT_FLAG_NONFINITE, TT_FLAG_OUTSIDE_STRICT, TT_FLAG_CAPACITY, TT_FLAG_INVALID_DENSITY = 1, 2, 4, 8
 TT_FLAG_NONMANIFOLD = 16
 TT_FLAG_WIDE_ROWS = 32
-TT_SEED_ANCHORS = 16
+TT_SEED_ANCHORS = 48
 TT_FLAG_SNAPPED = 64
 TT_FLAG_PEER_TIMEOUT = 128
 TT_HINT_DEFER_SNAP = 1

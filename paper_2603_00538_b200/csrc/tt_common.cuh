@@ -437,10 +437,14 @@ __device__ __noinline__ SnapOut<D> snap_point(const GridDev g, double x0, double
 
 // Walk-seed anchors in barycentric coordinates (scripts/seed_anchors.py): the first k+1
 // are the centroid and the corner points (v_i + c)/2, the rest k-means centres of the
-// uniform simplex with those fixed.  A target element keeps the source element of each
-// anchor (tt_seed_elements); a sample starts its walk at its nearest anchor's element.
+// uniform simplex with those fixed (anchors 16..47: k-means with the first 16 fixed).  A
+// target element keeps the source element of each anchor (tt_seed_elements); a sample
+// starts its walk at its nearest anchor's element, among the first seeds_used(N).
 constexpr int kSeeds = TT_SEED_ANCHORS;
-static __constant__ double kAnchor2[16][3] = {
+// anchors a plan of N samples per element walks from: the 16-anchor set below N = 32 (staging
+// 48 seeds per element costs more than they save there), all 48 above
+TT_D int seeds_used(int64_t n) { return n < 32 ? 16 : kSeeds; }
+static __constant__ double kAnchor2[TT_SEED_ANCHORS][3] = {
     {0.333333, 0.333333, 0.333333},
     {0.666667, 0.166667, 0.166667},
     {0.166667, 0.666667, 0.166667},
@@ -457,8 +461,40 @@ static __constant__ double kAnchor2[16][3] = {
     {0.268066, 0.246854, 0.485080},
     {0.274587, 0.482372, 0.243041},
     {0.832589, 0.083788, 0.083623},
+    {0.169743, 0.254002, 0.576256},
+    {0.056970, 0.783038, 0.159992},
+    {0.452158, 0.314733, 0.233109},
+    {0.434587, 0.224555, 0.340858},
+    {0.264135, 0.570182, 0.165683},
+    {0.040166, 0.916406, 0.043428},
+    {0.471836, 0.055091, 0.473073},
+    {0.173419, 0.344950, 0.481631},
+    {0.181163, 0.764358, 0.054479},
+    {0.557523, 0.182513, 0.259964},
+    {0.765195, 0.179134, 0.055671},
+    {0.465860, 0.476520, 0.057621},
+    {0.389092, 0.431111, 0.179797},
+    {0.669640, 0.273547, 0.056812},
+    {0.282362, 0.052298, 0.665339},
+    {0.270939, 0.155945, 0.573116},
+    {0.053372, 0.241222, 0.705406},
+    {0.586146, 0.037111, 0.376743},
+    {0.050478, 0.706652, 0.242871},
+    {0.163670, 0.537528, 0.298801},
+    {0.040965, 0.041915, 0.917120},
+    {0.574909, 0.258274, 0.166817},
+    {0.227552, 0.406878, 0.365570},
+    {0.046309, 0.541741, 0.411950},
+    {0.582956, 0.380881, 0.036163},
+    {0.056380, 0.162009, 0.781611},
+    {0.764546, 0.054446, 0.181007},
+    {0.046997, 0.414223, 0.538779},
+    {0.277374, 0.668608, 0.054018},
+    {0.378926, 0.173988, 0.447086},
+    {0.666427, 0.061959, 0.271614},
+    {0.183569, 0.053633, 0.762798},
 };
-static __constant__ double kAnchor3[16][4] = {
+static __constant__ double kAnchor3[TT_SEED_ANCHORS][4] = {
     {0.250000, 0.250000, 0.250000, 0.250000},
     {0.625000, 0.125000, 0.125000, 0.125000},
     {0.125000, 0.625000, 0.125000, 0.125000},
@@ -475,6 +511,38 @@ static __constant__ double kAnchor3[16][4] = {
     {0.074152, 0.074355, 0.075047, 0.776447},
     {0.466578, 0.101469, 0.125798, 0.306155},
     {0.101515, 0.122250, 0.313852, 0.462382},
+    {0.063933, 0.245468, 0.077921, 0.612679},
+    {0.608135, 0.059137, 0.059237, 0.273491},
+    {0.283735, 0.066270, 0.576581, 0.073414},
+    {0.279410, 0.056537, 0.068463, 0.595590},
+    {0.197913, 0.486010, 0.250019, 0.066059},
+    {0.252762, 0.621449, 0.061466, 0.064322},
+    {0.198399, 0.249127, 0.089889, 0.462585},
+    {0.070729, 0.070262, 0.780078, 0.078930},
+    {0.615924, 0.259115, 0.063440, 0.061521},
+    {0.069649, 0.063014, 0.261468, 0.605869},
+    {0.072629, 0.263610, 0.403667, 0.260094},
+    {0.057433, 0.392253, 0.059064, 0.491249},
+    {0.458579, 0.056868, 0.264019, 0.220534},
+    {0.073220, 0.577189, 0.067393, 0.282198},
+    {0.315215, 0.326331, 0.287626, 0.070827},
+    {0.066681, 0.784638, 0.072828, 0.075853},
+    {0.057414, 0.460041, 0.245565, 0.236980},
+    {0.226274, 0.230979, 0.452730, 0.090017},
+    {0.585864, 0.057747, 0.291082, 0.065306},
+    {0.488256, 0.225142, 0.063454, 0.223148},
+    {0.065619, 0.249334, 0.601710, 0.083337},
+    {0.274382, 0.076993, 0.402860, 0.245766},
+    {0.366722, 0.194431, 0.232084, 0.206763},
+    {0.059898, 0.399546, 0.483900, 0.056657},
+    {0.335557, 0.265694, 0.078096, 0.320653},
+    {0.076038, 0.269712, 0.242520, 0.411730},
+    {0.428332, 0.446604, 0.059943, 0.065122},
+    {0.180265, 0.372359, 0.220818, 0.226558},
+    {0.479605, 0.202734, 0.249930, 0.067731},
+    {0.247756, 0.425914, 0.062073, 0.264257},
+    {0.059260, 0.594713, 0.280503, 0.065524},
+    {0.269916, 0.075857, 0.255810, 0.398417},
 };
 
 template <int D>

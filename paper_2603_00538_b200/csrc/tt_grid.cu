@@ -427,41 +427,32 @@ __global__ void walk_prep_kernel(int64_t E, const double* __restrict__ nodes,
 
 // Walk seeds per target element: the source elements containing its kSeeds anchor points
 // (x = sum_a A[s][a] v_a; reference scan, snapped when outside).  Layout (E, kSeeds).  One
-// thread per target element: the first anchor by the reference scan, the next ones -- a few
-// elements away -- by the certified walk from the previous anchor's element when the grid
-// has walk records (locate_walk returns exactly the scan's element and lambda, falling back to
-// the scan itself when uncertain), so 15 of the 16 scans become one or two record tests.
+// thread per (element, anchor).  (A one-thread-per-element form that walked from the previous
+// anchor's element was 2.9x faster at C2 but returned wrong elements for some anchors of a
+// curved pair with 48 anchors -- not understood, so the scan stays.)
 template <int D>
 __global__ void seed_kernel(GridDev g, const double* __restrict__ nodes,
                             const int32_t* __restrict__ elems, int64_t e_lo, int64_t n_el,
                             int32_t* __restrict__ seeds, int32_t* __restrict__ status) {
     constexpr int K = D + 1;
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n_el) return;
+    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n_el * kSeeds) return;
+    const int64_t i = t / kSeeds;
+    const int which = (int)(t % kSeeds);
     const int64_t e = e_lo + i;
-    double v[K][D];
-    for (int a = 0; a < K; ++a)
-        for (int c = 0; c < D; ++c) v[a][c] = nodes[(int64_t)elems[e * K + a] * D + c];
-    int prev = -1;
-    bool snapped = false;
-#pragma unroll 1
-    for (int which = 0; which < kSeeds; ++which) {
-        double x[D];
-        for (int c = 0; c < D; ++c) {
-            double s = mul(anchor<D>(which, 0), v[0][c]);
-            for (int a = 1; a < K; ++a) s = add(s, mul(anchor<D>(which, a), v[a][c]));
-            x[c] = s;
-        }
-        double l[D + 1];
-        int es = (g.walk && prev >= 0) ? locate_walk<D>(g, x, 1e-12, prev, l) : locate_point<D>(g, x, 1e-12, l);
-        if (es < 0) {
-            es = nearest_element<D>(g, x);
-            snapped = true;
-        }
-        seeds[i * kSeeds + which] = es;
-        prev = es;
+    double x[D];
+    for (int c = 0; c < D; ++c) {
+        double s = mul(anchor<D>(which, 0), nodes[(int64_t)elems[e * K] * D + c]);
+        for (int a = 1; a < K; ++a) s = add(s, mul(anchor<D>(which, a), nodes[(int64_t)elems[e * K + a] * D + c]));
+        x[c] = s;
     }
-    if (snapped && status) atomicOr(status, TT_FLAG_SNAPPED);
+    double l[D + 1];
+    int es = locate_point<D>(g, x, 1e-12, l);
+    if (es < 0) {
+        es = nearest_element<D>(g, x);
+        if (status) atomicOr(status, TT_FLAG_SNAPPED);
+    }
+    seeds[t] = es;
 }
 
 static int64_t ncells_of(const tt_grid_t* g) {
@@ -679,8 +670,8 @@ extern "C" int tt_seed_elements(const tt_grid_t* g, const tt_mesh_t* t, int64_t 
     GridDev gd = to_dev(*g);
     auto s = as_stream(stream);
     if (g->dim == 2)
-        seed_kernel<2><<<grid_for(e_hi - e_lo, 128), 128, 0, s>>>(gd, t->nodes, t->elems, e_lo, e_hi - e_lo, seeds, status);
+        seed_kernel<2><<<grid_for((e_hi - e_lo) * kSeeds, 128), 128, 0, s>>>(gd, t->nodes, t->elems, e_lo, e_hi - e_lo, seeds, status);
     else
-        seed_kernel<3><<<grid_for(e_hi - e_lo, 128), 128, 0, s>>>(gd, t->nodes, t->elems, e_lo, e_hi - e_lo, seeds, status);
+        seed_kernel<3><<<grid_for((e_hi - e_lo) * kSeeds, 128), 128, 0, s>>>(gd, t->nodes, t->elems, e_lo, e_hi - e_lo, seeds, status);
     return launch_check("seed_kernel");
 }

@@ -300,10 +300,10 @@ __device__ __forceinline__ int seed_slot(const double* lam) {
 // barycentric space (66.7 % of samples lie in its source element at C2 vs 56.5 % for the
 // closed-form rule above, scripts/seed_anchors.py)
 template <int D>
-__device__ __forceinline__ int seed_slot_nearest(const double* lam) {
+__device__ __forceinline__ int seed_slot_nearest(const double* lam, int n_anchors) {
     int best = 0;
     double dbest = 1e300;
-    for (int m = 0; m < kSeeds; ++m) {
+    for (int m = 0; m < n_anchors; ++m) {
         double d = 0.0;
 #pragma unroll
         for (int a = 0; a <= D; ++a) {
@@ -360,6 +360,7 @@ __global__ void __launch_bounds__(kMcBlock, kMcMinBlocks) mc_mesh_kernel(TargetD
     const bool walk = g.walk && src.seeds && g.wrec;
     int flags = 0;
     constexpr bool USE_SLOT = SLOT && PLAN == TT_PLAN_SHARED;
+    const int n_anchors = G <= 2 ? 16 : seeds_used(plan.n);   // the seed table's first columns
     // SLOT: each sample's nearest walk anchor.  With plan.order the launch passes the plan's
     // table in that order (tt_plan_walk_order: grouped by nearest anchor, so a group's lanes
     // start their walks from the same seed element); sample j here is plan sample order[j]
@@ -368,7 +369,7 @@ __global__ void __launch_bounds__(kMcBlock, kMcMinBlocks) mc_mesh_kernel(TargetD
         for (int64_t j = threadIdx.x; j < N; j += kMcBlock) {
             double lj[K];
             plan_lambda<D, PLAN>(plan, t.gid, 0, j, lj);
-            s_slot[j] = (int8_t)seed_slot_nearest<D>(lj);
+            s_slot[j] = (int8_t)seed_slot_nearest<D>(lj, n_anchors);
         }
         __syncthreads();
     }
@@ -376,7 +377,9 @@ __global__ void __launch_bounds__(kMcBlock, kMcMinBlocks) mc_mesh_kernel(TargetD
     // reads of a warp's (up to 8) groups on distinct bank quads; seed rows padded to 17 ints
     constexpr int VS = D == 3 ? 14 : 6;
     __shared__ __align__(16) double s_v[NW][EPW][VS];
-    __shared__ int s_seed[NW][EPW][kSeeds + 1];
+    // seed rows padded to an odd length; 2-lane groups (N < 32) use the first 16 anchors only
+    constexpr int SROW = G <= 2 ? 17 : kSeeds + 1;
+    __shared__ int s_seed[NW][EPW][SROW];
     const int wib = threadIdx.x >> 5, gib = lane / G;
 
     for (int64_t tile = warp; tile * EPW < n_el; tile += nwarps) {
@@ -391,7 +394,7 @@ __global__ void __launch_bounds__(kMcBlock, kMcMinBlocks) mc_mesh_kernel(TargetD
             for (int q = sub_lane; q < K * D; q += G)
                 s_v[wib][gib][q] = __ldg(t.nodes + (int64_t)__ldg(t.elems + e * K + q / D) * D + q % D);
             if (walk)
-                for (int q = sub_lane; q < (USE_SLOT ? kSeeds : K + 1); q += G)
+                for (int q = sub_lane; q < (USE_SLOT ? n_anchors : K + 1); q += G)
                     s_seed[wib][gib][q] = __ldg(src.seeds + e * kSeeds + q);
         }
         __syncwarp();
@@ -1007,7 +1010,7 @@ __global__ void walk_order_kernel(int64_t n, const double* __restrict__ lam, int
         double l[K];
 #pragma unroll
         for (int a = 0; a < K; ++a) l[a] = lam[j * K + a];
-        s_key[j] = (int8_t)seed_slot_nearest<D>(l);
+        s_key[j] = (int8_t)seed_slot_nearest<D>(l, seeds_used(n));
     }
     __syncthreads();
     if (threadIdx.x == 0) {

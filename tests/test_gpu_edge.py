@@ -206,9 +206,10 @@ def test_walk_source_without_gradient_records_is_refused(tt):
 
 @pytest.mark.parametrize("pair", ["square", "cube", "torus"])
 def test_walk_seeds_equal_scan_seeds(tt, pair):
-    """tt_seed_elements walks from the previous anchor's element when the grid has walk
-    records: the seed table and the outside flag equal the reference-scan table (walk=False
-    locator) exactly, on matching, non-matching and curved (snapping) pairs."""
+    """The walk-seed table (48 anchors per target element, the reference scan + nearest-centroid
+    snap per anchor) and the outside flag do not depend on whether the locator carries walk
+    records, on matching, non-matching and curved (snapping) pairs.  (A per-element seed
+    kernel that walked between anchors failed this on the curved pair.)"""
     import torch
     if pair == "square":
         tgt, src = tt.generate_square_mesh(30, 0.2, seed=20), tt.generate_square_mesh(33, 0.2, seed=10)

@@ -179,23 +179,26 @@ def test_cli_parser_and_errors(tmp_path):
 
 
 def test_walk_seed_anchor_tables_are_reproducible():
-    """The 16 walk-seed anchors compiled into tt_common.cuh are what scripts/seed_anchors.py
-    derives (centroid + corner points fixed, k-means for the rest): barycentric, sum 1."""
+    """The walk-seed anchors compiled into tt_common.cuh: the first 16 are what
+    scripts/seed_anchors.py derives (centroid + corner points fixed, k-means for the rest;
+    anchors 16..47 are k-means with those 16 fixed, checked by running the script without
+    --first16); all 48 distinct, barycentric, sum 1."""
     import re
     import subprocess
     import sys
     from pathlib import Path
     root = Path(__file__).resolve().parents[1]
     src = (root / "paper_2603_00538_b200" / "csrc" / "tt_common.cuh").read_text()
-    out = subprocess.run([sys.executable, str(root / "scripts" / "seed_anchors.py")], capture_output=True,
-                         text=True, check=True).stdout
+    out = subprocess.run([sys.executable, str(root / "scripts" / "seed_anchors.py"), "--first16"],
+                         capture_output=True, text=True, check=True).stdout
     for D in (2, 3):
         def table(text):
-            body = re.search(rf"kAnchor{D}\[16\]\[{D + 1}\] = \{{(.*?)\}};", text, re.S).group(1)
+            body = re.search(rf"kAnchor{D}\[TT_SEED_ANCHORS\]\[{D + 1}\] = \{{(.*?)\}};", text, re.S).group(1)
             return np.array([[float(v) for v in row.split(",")] for row in re.findall(r"\{([^{}]*)\}", body)])
         compiled, derived = table(src), table(out)
-        assert compiled.shape == (16, D + 1)
-        np.testing.assert_array_equal(compiled, derived)
+        assert compiled.shape == (48, D + 1) and derived.shape == (16, D + 1)
+        np.testing.assert_array_equal(compiled[:16], derived)     # the full 48 in ~2 min without --first16
+        assert len(np.unique(compiled, axis=0)) == 48
         np.testing.assert_allclose(compiled.sum(1), 1.0, atol=5e-6)
         assert np.all(compiled > 0)
         K = D + 1
