@@ -825,7 +825,7 @@ static int blocks_per_sm(Kernel kernel, int block, size_t smem) {
 // G = 4 ~ G = 8; N = 256 G = 16 3.76 vs G = 8 3.87; N = 512 G = 16 6.94 vs G = 32 7.35;
 // N = 1024 G = 16 13.41 vs 13.68.  Other sources: ~16 samples per lane.
 static int lanes_per_element(int src_kind, int64_t N) {
-    if (src_kind == TT_SRC_MESH) return N < 32 ? 2 : N < 128 ? 4 : N < 256 ? 8 : N < 2048 ? 16 : 32;
+    if (src_kind == TT_SRC_MESH) return N < 32 ? 2 : N < 128 ? 4 : N < 512 ? 8 : N < 2048 ? 16 : 32;
     const int64_t g = N / 16;
     return g < 8 ? 4 : g < 16 ? 8 : g < 32 ? 16 : 32;
 }
