@@ -283,17 +283,60 @@ __device__ unsigned long long g_mc_stats[8];
 
 constexpr int kSlotCap = 4096;  // per-block seed-slot table capacity (samples)
 
-// Walk-seed slot of a sample without a slot table: the corner anchor (v_i + c)/2 of the
-// vertex with the largest barycentric weight when that weight exceeds 0.45, else the
-// centroid anchor (slot 0).
-template <int K>
-__device__ __forceinline__ int seed_slot(const double* lam) {
-    int imax = 0;
-    double lmax = lam[0];
-#pragma unroll
-    for (int i = 1; i < K; ++i)
-        if (lam[i] > lmax) { lmax = lam[i]; imax = i; }
-    return lmax > 0.45 ? 1 + imax : 0;
+// Per-element (Philox) plans have no slot table: a lookup table of the nearest anchor over a
+// grid of barycentric space (3-D: 16^3 cells of (l0, l1, l2); 2-D: 64^2 of (l0, l1)), built
+// once per process for 16 and for kSeeds anchors, gives each sample a near-nearest walk
+// anchor for one L1-resident byte load (the seed is only a walk start: its choice never
+// changes a result).
+constexpr int kAnchorTab = 4096;
+__device__ uint8_t g_anchor_tab[2][2][kAnchorTab];   // [dim - 2][all anchors][cell]
+
+template <int D>
+__global__ void anchor_tab_kernel(int n_anchors, uint8_t* __restrict__ tab) {
+    constexpr int K = D + 1;
+    constexpr int Q = D == 3 ? 16 : 64;
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= kAnchorTab) return;
+    double l[K];
+    if constexpr (D == 3) {
+        l[0] = ((c / (Q * Q)) + 0.5) / Q; l[1] = (((c / Q) % Q) + 0.5) / Q; l[2] = ((c % Q) + 0.5) / Q;
+    } else {
+        l[0] = ((c / Q) + 0.5) / Q; l[1] = ((c % Q) + 0.5) / Q;
+    }
+    double rest = 1.0;
+    for (int a = 0; a < D; ++a) rest -= l[a];
+    l[D] = rest;
+    int best = 0;
+    double dbest = 1e300;
+    for (int m = 0; m < n_anchors; ++m) {
+        double d = 0.0;
+        for (int a = 0; a <= D; ++a) { const double u = l[a] - anchor<D>(m, a); d += u * u; }
+        if (d < dbest) { dbest = d; best = m; }
+    }
+    tab[c] = (uint8_t)best;
+}
+
+template <int D>
+__device__ __forceinline__ int seed_slot_tab(const double* lam, int all) {
+    constexpr int Q = D == 3 ? 16 : 64;
+    const auto q = [](double v) { int i = (int)(v * Q); return i < 0 ? 0 : (i > Q - 1 ? Q - 1 : i); };
+    const int c = D == 3 ? (q(lam[0]) * Q + q(lam[1])) * Q + q(lam[2]) : q(lam[0]) * Q + q(lam[1]);
+    return g_anchor_tab[D - 2][all][c];
+}
+
+static int anchor_tables_ready(cudaStream_t st) {
+    static int done = 0;   // one process per GPU: built once on its device
+    if (done) return TT_OK;
+    uint8_t* tab = nullptr;
+    int rc = cuda_status(cudaGetSymbolAddress((void**)&tab, g_anchor_tab), "anchor table");
+    if (rc) return rc;
+    anchor_tab_kernel<2><<<kAnchorTab / 256, 256, 0, st>>>(16, tab);
+    anchor_tab_kernel<2><<<kAnchorTab / 256, 256, 0, st>>>(kSeeds, tab + kAnchorTab);
+    anchor_tab_kernel<3><<<kAnchorTab / 256, 256, 0, st>>>(16, tab + 2 * kAnchorTab);
+    anchor_tab_kernel<3><<<kAnchorTab / 256, 256, 0, st>>>(kSeeds, tab + 3 * kAnchorTab);
+    rc = launch_check("anchor_tab_kernel");
+    if (!rc) done = 1;
+    return rc;
 }
 
 // With a per-block slot table (shared plans): the nearest of all kSeeds anchors in
@@ -394,7 +437,7 @@ __global__ void __launch_bounds__(kMcBlock, kMcMinBlocks) mc_mesh_kernel(TargetD
             for (int q = sub_lane; q < K * D; q += G)
                 s_v[wib][gib][q] = __ldg(t.nodes + (int64_t)__ldg(t.elems + e * K + q / D) * D + q % D);
             if (walk)
-                for (int q = sub_lane; q < (USE_SLOT ? n_anchors : K + 1); q += G)
+                for (int q = sub_lane; q < n_anchors; q += G)
                     s_seed[wib][gib][q] = __ldg(src.seeds + e * kSeeds + q);
         }
         __syncwarp();
@@ -427,7 +470,7 @@ __global__ void __launch_bounds__(kMcBlock, kMcMinBlocks) mc_mesh_kernel(TargetD
                     if (walk) {
                         int slot;
                         if constexpr (USE_SLOT) slot = s_slot[j];
-                        else slot = seed_slot<K>(lam);
+                        else slot = seed_slot_tab<D>(lam, n_anchors > 16);   // Philox: lookup table
                         cur = s_seed[wib][gib][slot];
                     }
                     steps = 0;
@@ -842,6 +885,10 @@ static int launch_mesh(const TargetDev& td, int64_t e_lo, int64_t e_hi, const Pl
     // better than 16 waves at C2, N = 64); 32-lane groups (N >= 512) keep 16 waves (+1 %)
     const int waves = G >= 32 ? 16 : 1;
     const bool slot = PLAN == TT_PLAN_SHARED && pd.n <= kSlotCap;
+    if (!slot) {   // per-element plans: the nearest-anchor lookup tables (built once)
+        const int rc = anchor_tables_ready(st);
+        if (rc) return rc;
+    }
     // the walk order (tt_plan_walk_order) applies to the slot-table kernels only
     PlanDev pw = pd;
     if (!slot || !pd.order || !pd.lam_walk) pw.order = nullptr;
