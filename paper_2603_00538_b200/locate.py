@@ -131,8 +131,8 @@ class UniformGridLocator:
         return g
 
     def seeds_for(self, target) -> torch.Tensor:
-        """Walk starts per target element (E, 16): source elements containing the
-        element's 16 anchor points -- centroid c, the points (v_i + c)/2, k-means anchors
+        """Walk starts per target element (E, 48): source elements containing the
+        element's 48 anchor points -- centroid c, the points (v_i + c)/2, k-means anchors
         (tt_seed_elements; cached per target while it lives, meshes are immutable)."""
         hit = self._seeds.get(target)
         if hit is not None:
