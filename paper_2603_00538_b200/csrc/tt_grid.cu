@@ -426,33 +426,59 @@ __global__ void walk_prep_kernel(int64_t E, const double* __restrict__ nodes,
 }
 
 // Walk seeds per target element: the source elements containing its kSeeds anchor points
-// (x = sum_a A[s][a] v_a; reference scan, snapped when outside).  Layout (E, kSeeds).  One
-// thread per (element, anchor).  (A one-thread-per-element form that walked from the previous
-// anchor's element was 2.9x faster at C2 but returned wrong elements for some anchors of a
-// curved pair with 48 anchors -- not understood, so the scan stays.)
+// (x = sum_a A[s][a] v_a; reference scan, snapped when outside).  Layout (E, kSeeds).
+// Two passes, one thread per (element, anchor): anchor 0 (the centroid) by the reference scan;
+// then the others, when the grid has walk records and the centroid was found inside, by the
+// certified walk from the centroid's element (locate_walk: exactly the scan's element,
+// falling back to the scan when uncertain), else by the scan.  (A one-thread-per-element form
+// that chained walks from each previous anchor -- snapped ones included -- returned wrong
+// elements on a curved pair and was dropped.)
 template <int D>
-__global__ void seed_kernel(GridDev g, const double* __restrict__ nodes,
-                            const int32_t* __restrict__ elems, int64_t e_lo, int64_t n_el,
-                            int32_t* __restrict__ seeds, int32_t* __restrict__ status) {
+__device__ __forceinline__ void anchor_point(const double* __restrict__ nodes, const int32_t* __restrict__ elems,
+                                             int64_t e, int which, double* x) {
     constexpr int K = D + 1;
-    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (t >= n_el * kSeeds) return;
-    const int64_t i = t / kSeeds;
-    const int which = (int)(t % kSeeds);
-    const int64_t e = e_lo + i;
-    double x[D];
     for (int c = 0; c < D; ++c) {
         double s = mul(anchor<D>(which, 0), nodes[(int64_t)elems[e * K] * D + c]);
         for (int a = 1; a < K; ++a) s = add(s, mul(anchor<D>(which, a), nodes[(int64_t)elems[e * K + a] * D + c]));
         x[c] = s;
     }
+}
+
+template <int D>
+__global__ void seed_kernel(GridDev g, const double* __restrict__ nodes,
+                            const int32_t* __restrict__ elems, int64_t e_lo, int64_t n_el, int pass,
+                            int32_t* __restrict__ seeds, int32_t* __restrict__ status) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int per = pass == 0 ? 1 : kSeeds - 1;
+    if (t >= n_el * per) return;
+    const int64_t i = t / per;
+    const int which = pass == 0 ? 0 : 1 + (int)(t % per);
+    double x[D];
+    anchor_point<D>(nodes, elems, e_lo + i, which, x);
     double l[D + 1];
-    int es = locate_point<D>(g, x, 1e-12, l);
-    if (es < 0) {
+    int es;
+    if (pass == 0) {
+        es = locate_point<D>(g, x, 1e-12, l);
+    } else {
+        const int c0 = seeds[i * kSeeds];
+        // c0 is the centroid's element when it was found inside (pass 0 stores snapped
+        // centroids as -(e + 2))
+        es = (g.walk && c0 >= 0) ? locate_walk<D>(g, x, 1e-12, c0, l) : locate_point<D>(g, x, 1e-12, l);
+    }
+    const bool snapped = es < 0;
+    if (snapped) {
         es = nearest_element<D>(g, x);
         if (status) atomicOr(status, TT_FLAG_SNAPPED);
     }
-    seeds[t] = es;
+    seeds[i * kSeeds + which] = (pass == 0 && snapped) ? -(es + 2) : es;
+}
+
+// pass 2: decode snapped centroids
+__global__ void seed_fix_kernel(int64_t n_el, int32_t* __restrict__ seeds) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n_el) return;
+    const int v = seeds[i * kSeeds];
+    if (v < -1) seeds[i * kSeeds] = -v - 2;
 }
 
 static int64_t ncells_of(const tt_grid_t* g) {
@@ -669,9 +695,14 @@ extern "C" int tt_seed_elements(const tt_grid_t* g, const tt_mesh_t* t, int64_t 
     if (e_hi == e_lo) return TT_OK;
     GridDev gd = to_dev(*g);
     auto s = as_stream(stream);
-    if (g->dim == 2)
-        seed_kernel<2><<<grid_for((e_hi - e_lo) * kSeeds, 128), 128, 0, s>>>(gd, t->nodes, t->elems, e_lo, e_hi - e_lo, seeds, status);
-    else
-        seed_kernel<3><<<grid_for((e_hi - e_lo) * kSeeds, 128), 128, 0, s>>>(gd, t->nodes, t->elems, e_lo, e_hi - e_lo, seeds, status);
+    const int64_t n_el = e_hi - e_lo;
+    for (int pass = 0; pass < 2; ++pass) {
+        const int64_t nt = n_el * (pass == 0 ? 1 : kSeeds - 1);
+        if (g->dim == 2)
+            seed_kernel<2><<<grid_for(nt, 128), 128, 0, s>>>(gd, t->nodes, t->elems, e_lo, n_el, pass, seeds, status);
+        else
+            seed_kernel<3><<<grid_for(nt, 128), 128, 0, s>>>(gd, t->nodes, t->elems, e_lo, n_el, pass, seeds, status);
+    }
+    seed_fix_kernel<<<grid_for(n_el, 256), 256, 0, s>>>(n_el, seeds);
     return launch_check("seed_kernel");
 }
