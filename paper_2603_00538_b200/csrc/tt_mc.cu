@@ -325,8 +325,11 @@ __device__ __forceinline__ int seed_slot_tab(const double* lam, int all) {
 }
 
 static int anchor_tables_ready(cudaStream_t st) {
-    static int done = 0;   // one process per GPU: built once on its device
-    if (done) return TT_OK;
+    static unsigned long long done = 0;   // per device (bit = device ordinal)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (done & bit) return TT_OK;
     uint8_t* tab = nullptr;
     int rc = cuda_status(cudaGetSymbolAddress((void**)&tab, g_anchor_tab), "anchor table");
     if (rc) return rc;
@@ -335,7 +338,7 @@ static int anchor_tables_ready(cudaStream_t st) {
     anchor_tab_kernel<3><<<kAnchorTab / 256, 256, 0, st>>>(16, tab + 2 * kAnchorTab);
     anchor_tab_kernel<3><<<kAnchorTab / 256, 256, 0, st>>>(kSeeds, tab + 3 * kAnchorTab);
     rc = launch_check("anchor_tab_kernel");
-    if (!rc) done = 1;
+    if (!rc) done |= bit;
     return rc;
 }
 
